@@ -1,0 +1,265 @@
+// C ABI of the pyramid filter + the reference's surface primitives.
+#include <string>
+
+#include "pyr_launch.cuh"
+
+namespace ssb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_check(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(where) + ": " + cudaGetErrorString(e));
+        return SSB_ECUDA;
+    }
+    return SSB_OK;
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static int logit_channels(const ssb_pyr_desc* d, int l) {
+    const int taps = d->ksize * d->ksize;
+    int n = taps;
+    if (l < d->levels - 1) n += d->blend_mode == SSB_BLEND_TIED ? 1 : 4;
+    if (l == 0 && d->has_prev) n += taps;
+    return n;
+}
+
+int make_plan(const ssb_pyr_desc* d, PyrPlan* p) {
+    if (!d) {
+        set_error("null descriptor");
+        return SSB_EINVAL;
+    }
+    if (d->batch < 1 || d->channels < 1 || d->height < 1 || d->width < 1) {
+        set_error("batch, channels, height and width must be >= 1");
+        return SSB_EINVAL;
+    }
+    if (d->levels < 1 || d->levels > SSB_MAX_LEVELS) {
+        set_error("levels must be in [1, SSB_MAX_LEVELS]");
+        return SSB_EINVAL;
+    }
+    if (d->ksize != 3 && d->ksize != 5 && d->ksize != 7) {
+        set_error("ksize must be 3, 5 or 7");
+        return SSB_EUNSUPPORTED;
+    }
+    if (d->blend_mode != SSB_BLEND_NATIVE && d->blend_mode != SSB_BLEND_TIED) {
+        set_error("unknown blend_mode");
+        return SSB_EINVAL;
+    }
+    const bool ok_types = (d->image_dtype == SSB_F32 &&
+                           (d->logit_dtype == SSB_F32 || d->logit_dtype == SSB_BF16)) ||
+                          (d->image_dtype == SSB_F64 && d->logit_dtype == SSB_F64);
+    if (!ok_types) {
+        set_error("supported (image, logit) dtypes: (f32, f32), (f32, bf16), (f64, f64)");
+        return SSB_EUNSUPPORTED;
+    }
+    p->B = d->batch;
+    p->C = d->channels;
+    p->H = d->height;
+    p->W = d->width;
+    p->L = d->levels;
+    p->K = d->ksize;
+    p->esz = d->image_dtype == SSB_F64 ? 8 : 4;
+    p->lgesz = d->logit_dtype == SSB_F64 ? 8 : (d->logit_dtype == SSB_BF16 ? 2 : 4);
+    p->hl[0] = d->height;
+    p->wl[0] = d->width;
+    for (int l = 1; l < p->L; ++l) {
+        p->hl[l] = (p->hl[l - 1] + 1) / 2;
+        p->wl[l] = (p->wl[l - 1] + 1) / 2;
+    }
+    size_t t = 0, w = 0;
+    for (int l = 0; l < p->L; ++l) {
+        p->nlog[l] = logit_channels(d, l);
+        p->pool_off[l] = p->lhat_off[l] = p->ghat_off[l] = p->gl_off[l] = 0;
+        if (l == 0) continue;
+        const size_t bytes = align256((size_t)p->B * p->C * p->hl[l] * p->wl[l] * p->esz);
+        p->pool_off[l] = t;
+        t += bytes;
+        p->lhat_off[l] = t;
+        t += bytes;
+        p->ghat_off[l] = w;
+        w += bytes;
+        p->gl_off[l] = w;
+        w += bytes;
+    }
+    p->tape_bytes = t;
+    p->ws_bytes = w;
+    return SSB_OK;
+}
+
+}  // namespace ssb
+
+using namespace ssb;
+
+extern "C" {
+
+int ssb_version(void) { return SSB_VERSION; }
+
+const char* ssb_last_error(void) { return g_last_error.c_str(); }
+
+int ssb_pyr_logit_channels(const ssb_pyr_desc* d, int level) {
+    PyrPlan p;
+    int rc = make_plan(d, &p);
+    if (rc) return rc;
+    if (level < 0 || level >= p.L) {
+        set_error("level out of range");
+        return SSB_EINVAL;
+    }
+    return p.nlog[level];
+}
+
+int ssb_pyr_level_dims(const ssb_pyr_desc* d, int level, int32_t* h, int32_t* w) {
+    PyrPlan p;
+    int rc = make_plan(d, &p);
+    if (rc) return rc;
+    if (level < 0 || level >= p.L || !h || !w) {
+        set_error("level out of range or null output");
+        return SSB_EINVAL;
+    }
+    *h = p.hl[level];
+    *w = p.wl[level];
+    return SSB_OK;
+}
+
+int ssb_pyr_tape_bytes(const ssb_pyr_desc* d, size_t* bytes) {
+    PyrPlan p;
+    int rc = make_plan(d, &p);
+    if (rc) return rc;
+    if (!bytes) {
+        set_error("null output");
+        return SSB_EINVAL;
+    }
+    *bytes = p.tape_bytes;
+    return SSB_OK;
+}
+
+int ssb_pyr_workspace_bytes(const ssb_pyr_desc* d, size_t* bytes) {
+    PyrPlan p;
+    int rc = make_plan(d, &p);
+    if (rc) return rc;
+    if (!bytes) {
+        set_error("null output");
+        return SSB_EINVAL;
+    }
+    *bytes = p.ws_bytes;
+    return SSB_OK;
+}
+
+}  // extern "C"
+
+namespace ssb {
+template <int K, typename TL, typename T>
+int run_forward(const ssb_pyr_desc*, const PyrPlan&, const ssb_pyr_fwd_io*, void*, cudaStream_t);
+template <int K, typename TL, typename T>
+int run_backward(const ssb_pyr_desc*, const PyrPlan&, const ssb_pyr_bwd_io*, const void*, void*,
+                 cudaStream_t);
+
+template <typename Fn>
+static int by_types(const ssb_pyr_desc* d, Fn&& fn) {
+    // fn.template operator()<K, TL, T>() dispatched on (ksize, logit dtype)
+    switch (d->ksize) {
+#define CASE_K(KV)                                                                   \
+    case KV:                                                                         \
+        if (d->logit_dtype == SSB_F32) return fn.template call<KV, float, float>();  \
+        if (d->logit_dtype == SSB_BF16)                                              \
+            return fn.template call<KV, __nv_bfloat16, float>();                     \
+        return fn.template call<KV, double, double>();
+        CASE_K(3)
+        CASE_K(5)
+        CASE_K(7)
+#undef CASE_K
+    }
+    set_error("unsupported ksize");
+    return SSB_EUNSUPPORTED;
+}
+
+struct FwdCall {
+    const ssb_pyr_desc* d;
+    const PyrPlan* p;
+    const ssb_pyr_fwd_io* io;
+    void* tape;
+    cudaStream_t s;
+    template <int K, typename TL, typename T>
+    int call() { return run_forward<K, TL, T>(d, *p, io, tape, s); }
+};
+
+struct BwdCall {
+    const ssb_pyr_desc* d;
+    const PyrPlan* p;
+    const ssb_pyr_bwd_io* io;
+    const void* tape;
+    void* ws;
+    cudaStream_t s;
+    template <int K, typename TL, typename T>
+    int call() { return run_backward<K, TL, T>(d, *p, io, tape, ws, s); }
+};
+}  // namespace ssb
+
+extern "C" {
+
+int ssb_pyr_forward(const ssb_pyr_desc* d, const ssb_pyr_fwd_io* io, void* tape,
+                    ssb_stream_t stream) {
+    PyrPlan p;
+    int rc = make_plan(d, &p);
+    if (rc) return rc;
+    if (!io || !io->noisy || !io->out) {
+        set_error("ssb_pyr_forward: noisy and out are required");
+        return SSB_EINVAL;
+    }
+    if ((d->has_demod != 0) != (io->demod != nullptr) || (d->has_prev != 0) != (io->prev != nullptr)) {
+        set_error("ssb_pyr_forward: demod/prev pointers must match has_demod/has_prev");
+        return SSB_EINVAL;
+    }
+    for (int l = 0; l < p.L; ++l)
+        if (!io->logits[l]) {
+            set_error("ssb_pyr_forward: missing logits for a level");
+            return SSB_EINVAL;
+        }
+    if (p.L > 1 && !tape) {
+        set_error("ssb_pyr_forward: tape required for levels > 1");
+        return SSB_EINVAL;
+    }
+    FwdCall c{d, &p, io, tape, (cudaStream_t)stream};
+    return by_types(d, c);
+}
+
+int ssb_pyr_backward(const ssb_pyr_desc* d, const ssb_pyr_bwd_io* io, const void* tape,
+                     void* workspace, ssb_stream_t stream) {
+    PyrPlan p;
+    int rc = make_plan(d, &p);
+    if (rc) return rc;
+    if (!io || !io->noisy || !io->upstream || !io->g_noisy) {
+        set_error("ssb_pyr_backward: noisy, upstream and g_noisy are required");
+        return SSB_EINVAL;
+    }
+    if ((d->has_demod != 0) != (io->demod != nullptr) || (d->has_prev != 0) != (io->prev != nullptr)) {
+        set_error("ssb_pyr_backward: demod/prev pointers must match has_demod/has_prev");
+        return SSB_EINVAL;
+    }
+    if (d->has_prev && !io->g_prev) {
+        set_error("ssb_pyr_backward: g_prev required when has_prev");
+        return SSB_EINVAL;
+    }
+    const bool want = io->g_logits[0] != nullptr;
+    for (int l = 0; l < p.L; ++l) {
+        if (!io->logits[l] || (want && !io->g_logits[l])) {
+            set_error("ssb_pyr_backward: logits (and g_logits when wanted) needed per level");
+            return SSB_EINVAL;
+        }
+    }
+    if (io->g_demod && d->has_demod && !io->out) {
+        set_error("ssb_pyr_backward: forward output required for the demod gradient");
+        return SSB_EINVAL;
+    }
+    if (p.L > 1 && (!tape || !workspace)) {
+        set_error("ssb_pyr_backward: tape and workspace required for levels > 1");
+        return SSB_EINVAL;
+    }
+    BwdCall c{d, &p, io, tape, workspace, (cudaStream_t)stream};
+    return by_types(d, c);
+}
+
+}  // extern "C"

@@ -1,0 +1,742 @@
+// Gather-pyramid filter kernels (forward, backward, pooling, final sweep).
+//
+// Reference semantics: pkg/src/sparse_sampler/pyramid.py (Appendix A of
+// arXiv 2602.08642).  Design notes (DESIGN.md section "Kernels"):
+//  * images planar (B, C, H, W); level-l logits planar (B, C_l, H_l, W_l);
+//  * forward: one kernel per level, 2-D tile, per-pixel softmax in registers,
+//    k x k gather from a clamp-padded shared-memory tile, upsample taps read
+//    from the (L2-resident) coarse partial reconstruction;
+//  * backward: one kernel per level that walks a column strip top->bottom in
+//    steps of S rows.  Each step computes the softmax of S new rows (strip +
+//    r halo columns) once, then (B1) the logit gradients of the strip's own
+//    pixels, (B2) the gather-transpose into a ring of per-row accumulators
+//    (clamp "fold" applied at the image border, pyramid.py:206-213) and
+//    (B3) the upsample-transpose into a ring of coarse-row accumulators.
+//    Finished rows are flushed to HBM.  No atomics: every accumulator cell is
+//    owned by exactly one thread per phase.
+#pragma once
+
+#include "common.cuh"
+
+namespace ssb {
+
+constexpr int kMaxCh = 3;  // channels per launch; larger C is split by the host
+
+struct FwdLevel {
+    int nc, H, W, Hc, Wc;
+    const void* logits;
+    long long lg_b;  // batch stride of logits (elements)
+    const void* lin;  // L^l (l > 0) or noisy (l == 0)
+    long long in_b, in_c;
+    const void* demod;  // l == 0 only (same strides as lin); may be null
+    const void* prev;   // l == 0 temporal history (same strides); may be null
+    const void* lhat_c;  // coarse Lhat^{l+1}
+    long long c_b, c_c;
+    void* out;  // Lhat^l (l > 0) or out (l == 0); same strides as lin
+};
+
+struct BwdLevel {
+    int nc, H, W, Hc, Wc;
+    int seg_h;
+    int want_params;
+    int accum;
+    const void* logits;
+    long long lg_b;
+    void* glogits;
+    const void* lin;  // L^l or noisy
+    long long in_b, in_c;
+    const void* demod;
+    const void* prev;
+    const void* gin;   // ghat^l (l > 0) or upstream (l == 0)
+    const void* outp;  // l == 0: forward output (for the demod gradient); may be null
+    void* gl_out;      // l > 0: g of L^l via this level's gather; l == 0: partial g_noisy
+    void* gdc_out;     // l == 0: partial gradient w.r.t. d; may be null
+    void* gprev_out;   // l == 0 with history: g_prev (final)
+    const void* lhat_c;
+    long long c_b, c_c;
+    void* ghat_c;  // coarse ghat^{l+1}
+};
+
+// ===========================================================================
+// Forward level kernel
+// ===========================================================================
+constexpr int FWD_TX = 32, FWD_TY = 8;
+
+template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
+__global__ void __launch_bounds__(FWD_TX* FWD_TY)
+    k_pyr_fwd(const FwdLevel a) {
+    constexpr int R = K / 2, NT = K * K;
+    constexpr int NUP = UP ? 4 : 0;
+    constexpr int NLUP = UP ? (TIED ? 1 : 4) : 0;
+    constexpr int NTM = PREV ? NT : 0;
+    constexpr int NW = NT + NUP + NTM;
+    constexpr int RXF = FWD_TX + 2 * R, RYF = FWD_TY + 2 * R;
+    __shared__ T s_in[kMaxCh][RYF][RXF];
+    __shared__ T s_pv[PREV ? kMaxCh : 1][PREV ? RYF : 1][PREV ? RXF : 1];
+
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * FWD_TX, y0 = blockIdx.y * FWD_TY;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * FWD_TX + tx;
+    const int nc = a.nc, H = a.H, W = a.W;
+
+    const T* lin = (const T*)a.lin + b * a.in_b;
+    const T* dem = (L0 && a.demod) ? (const T*)a.demod + b * a.in_b : nullptr;
+    const T* prv = PREV ? (const T*)a.prev + b * a.in_b : nullptr;
+    for (int i = tid; i < RYF * RXF; i += FWD_TX * FWD_TY) {
+        const int ry = i / RXF, rx = i - ry * RXF;
+        const int gy = clampi(y0 - R + ry, 0, H - 1), gx = clampi(x0 - R + rx, 0, W - 1);
+        const long long off = (long long)gy * W + gx;
+#pragma unroll
+        for (int c = 0; c < kMaxCh; ++c) {
+            if (c < nc) {
+                T v = lin[c * a.in_c + off];
+                T dc = (T)1;
+                if (dem) {
+                    dc = demod_clamp(dem[c * a.in_c + off]);
+                    v = v / dc;
+                }
+                s_in[c][ry][rx] = v;
+                if constexpr (PREV) {
+                    T p = prv[c * a.in_c + off];
+                    if (dem) p = p / dc;
+                    s_pv[c][ry][rx] = p;
+                }
+            }
+        }
+    }
+
+    const int x = x0 + tx, y = y0 + ty;
+    const bool valid = (x < W) && (y < H);
+    T e[NW];
+    T sum = (T)0;
+    if (valid) {
+        const long long hw = (long long)H * W, off = (long long)y * W + x;
+        const TL* lg = (const TL*)a.logits + b * a.lg_b + off;
+        T m;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(lg + t * hw);
+        if constexpr (UP) {
+            if constexpr (TIED) {
+                T v = ld_logit<T>(lg + NT * hw);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) e[NT + i] = v;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) e[NT + i] = ld_logit<T>(lg + (NT + i) * hw);
+            }
+        }
+        if constexpr (PREV) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) e[NT + NUP + t] = ld_logit<T>(lg + (NT + NLUP + t) * hw);
+        }
+        m = e[0];
+#pragma unroll
+        for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
+#pragma unroll
+        for (int t = 0; t < NW; ++t) {
+            e[t] = sexp(e[t] - m);
+            sum += e[t];
+        }
+    }
+    __syncthreads();
+    if (!valid) return;
+
+    const T inv = (T)1 / sum;
+    const long long off = (long long)y * W + x;
+    T* outp = (T*)a.out + b * a.in_b;
+    const T* lhc = UP ? (const T*)a.lhat_c + b * a.c_b : nullptr;
+    int cy0 = 0, cy1 = 0, cx0 = 0, cx1 = 0;
+    if constexpr (UP) {
+        cy0 = min(y >> 1, a.Hc - 1);
+        cy1 = min((y + 1) >> 1, a.Hc - 1);
+        cx0 = min(x >> 1, a.Wc - 1);
+        cx1 = min((x + 1) >> 1, a.Wc - 1);
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCh; ++c) {
+        if (c >= nc) break;
+        T acc = (T)0;
+#pragma unroll
+        for (int dy = -R; dy <= R; ++dy)
+#pragma unroll
+            for (int dx = -R; dx <= R; ++dx)
+                acc += e[(dy + R) * K + dx + R] * s_in[c][ty + R + dy][tx + R + dx];
+        if constexpr (UP) {
+            const T* cp = lhc + c * a.c_c;
+            acc += e[NT + 0] * cp[cy0 * a.Wc + cx0];
+            acc += e[NT + 1] * cp[cy0 * a.Wc + cx1];
+            acc += e[NT + 2] * cp[cy1 * a.Wc + cx0];
+            acc += e[NT + 3] * cp[cy1 * a.Wc + cx1];
+        }
+        if constexpr (PREV) {
+#pragma unroll
+            for (int dy = -R; dy <= R; ++dy)
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx)
+                    acc += e[NT + NUP + (dy + R) * K + dx + R] * s_pv[c][ty + R + dy][tx + R + dx];
+        }
+        acc *= inv;
+        if (L0 && dem) acc *= demod_clamp(dem[c * a.in_c + off]);
+        outp[c * a.in_c + off] = acc;
+    }
+}
+
+// ===========================================================================
+// Backward level kernel (column-strip walker)
+// ===========================================================================
+constexpr int BWD_THREADS = 256;
+constexpr int BWD_RX = 64;  // region columns per strip (own columns + 2r halo)
+constexpr int BWD_LR = 16;  // image ring rows (>= 2S + 2r)
+constexpr int BWD_AR = 16;  // accumulator ring rows (>= S + 2r)
+constexpr int BWD_CR = 4;   // coarse accumulator ring rows (>= S/2 + 1)
+
+template <int K, bool UP, bool PREV, typename T>
+struct BwdShape {
+    static constexpr int R = K / 2, NT = K * K;
+    static constexpr int NUP = UP ? 4 : 0;
+    static constexpr int NTM = PREV ? NT : 0;
+    static constexpr int NW = NT + NUP + NTM;
+    static constexpr int TXB = BWD_RX - 2 * R;
+    static constexpr size_t bytes_for(int S) {
+        return sizeof(T) * ((size_t)NW * S * BWD_RX + (size_t)kMaxCh * S * BWD_RX +
+                            (size_t)kMaxCh * BWD_LR * BWD_RX * (PREV ? 2 : 1) +
+                            (size_t)kMaxCh * BWD_AR * TXB * (PREV ? 2 : 1) +
+                            (size_t)kMaxCh * BWD_CR * (TXB / 2));
+    }
+    static constexpr int S = bytes_for(4) <= 200 * 1024 ? 4 : 2;
+    static constexpr size_t SMEM = bytes_for(S);
+    static constexpr bool REG_GW = NW <= 56;
+};
+
+template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
+__global__ void __launch_bounds__(BWD_THREADS)
+    k_pyr_bwd(const BwdLevel a) {
+    using SH = BwdShape<K, UP, PREV, T>;
+    constexpr int R = SH::R, NT = SH::NT, NUP = SH::NUP, NW = SH::NW, TXB = SH::TXB, S = SH::S;
+    constexpr int NLUP = UP ? (TIED ? 1 : 4) : 0;
+    constexpr int NLOG = NT + NLUP + SH::NTM;
+    constexpr int RUP = (R + 1) & ~1;  // rows of top halo, rounded up to even
+    constexpr int LRM = BWD_LR - 1, ARM = BWD_AR - 1, CRM = BWD_CR - 1;
+    constexpr int TXC = TXB / 2;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* s_w = reinterpret_cast<T*>(smem_raw);             // [NW][S][RX]
+    T* s_g = s_w + NW * S * BWD_RX;                      // [3][S][RX]
+    T* s_lin = s_g + kMaxCh * S * BWD_RX;                // [3][LR][RX]
+    T* s_prv = s_lin + kMaxCh * BWD_LR * BWD_RX;         // [3][LR][RX] (PREV)
+    T* s_acc = s_prv + (PREV ? kMaxCh * BWD_LR * BWD_RX : 0);  // [3][AR][TXB]
+    T* s_pac = s_acc + kMaxCh * BWD_AR * TXB;            // [3][AR][TXB] (PREV)
+    T* s_cac = s_pac + (PREV ? kMaxCh * BWD_AR * TXB : 0);     // [3][CR][TXC]
+#define SW(t, s, ri) s_w[((t) * S + (s)) * BWD_RX + (ri)]
+#define SG(c, s, ri) s_g[((c) * S + (s)) * BWD_RX + (ri)]
+#define SLIN(c, r, ri) s_lin[((c) * BWD_LR + ((r) & LRM)) * BWD_RX + (ri)]
+#define SPRV(c, r, ri) s_prv[((c) * BWD_LR + ((r) & LRM)) * BWD_RX + (ri)]
+#define SACC(c, p, xi) s_acc[((c) * BWD_AR + ((p) & ARM)) * TXB + (xi)]
+#define SPAC(c, p, xi) s_pac[((c) * BWD_AR + ((p) & ARM)) * TXB + (xi)]
+#define SCAC(c, y, xi) s_cac[((c) * BWD_CR + ((y) & CRM)) * TXC + (xi)]
+
+    const int tid = threadIdx.x;
+    const int b = blockIdx.z;
+    const int nc = a.nc, H = a.H, W = a.W;
+    const int x0 = blockIdx.x * TXB, xr0 = x0 - R;
+    const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
+    const int qstart = max(y0 - RUP, 0);
+    const int qend = min(y1 + R, H);
+    const long long hw = (long long)H * W;
+
+    const TL* lg = (const TL*)a.logits + b * a.lg_b;
+    TL* glg = a.want_params ? (TL*)a.glogits + b * a.lg_b : nullptr;
+    const T* lin = (const T*)a.lin + b * a.in_b;
+    const T* gin = (const T*)a.gin + b * a.in_b;
+    const T* dem = (L0 && a.demod) ? (const T*)a.demod + b * a.in_b : nullptr;
+    const T* prv = PREV ? (const T*)a.prev + b * a.in_b : nullptr;
+    const T* lhc = UP ? (const T*)a.lhat_c + b * a.c_b : nullptr;
+
+    // ---- prologue: zero accumulators, preload image ring rows [qstart-R, qstart+R)
+    for (int i = tid; i < kMaxCh * BWD_AR * TXB; i += BWD_THREADS) {
+        s_acc[i] = (T)0;
+        if constexpr (PREV) s_pac[i] = (T)0;
+    }
+    for (int i = tid; i < kMaxCh * BWD_CR * TXC; i += BWD_THREADS) s_cac[i] = (T)0;
+
+    auto load_image_row = [&](int r, int ri) {
+        const int gy = clampi(r, 0, H - 1), gx = clampi(xr0 + ri, 0, W - 1);
+        const long long off = (long long)gy * W + gx;
+#pragma unroll
+        for (int c = 0; c < kMaxCh; ++c) {
+            if (c < nc) {
+                T v = lin[c * a.in_c + off];
+                T dc = (T)1;
+                if (dem) {
+                    dc = demod_clamp(dem[c * a.in_c + off]);
+                    v = v / dc;
+                }
+                SLIN(c, r, ri) = v;
+                if constexpr (PREV) {
+                    T p = prv[c * a.in_c + off];
+                    if (dem) p = p / dc;
+                    SPRV(c, r, ri) = p;
+                }
+            }
+        }
+    };
+    for (int i = tid; i < 2 * R * BWD_RX; i += BWD_THREADS) {
+        const int rr = i / BWD_RX, ri = i - rr * BWD_RX;
+        load_image_row(qstart - R + rr, ri);
+    }
+
+    int next_flush = max(qstart - R, 0);
+    int cnext = qstart >> 1;
+    __syncthreads();
+
+    for (int qs = qstart; qs < qend; qs += S) {
+        // ------------------------------------------------ phase A: new rows
+        if (tid < S * BWD_RX) {
+            const int s = tid / BWD_RX, ri = tid - s * BWD_RX;
+            const int qy = qs + s, qx = xr0 + ri;
+            const bool in = (qy < H) && (qx >= 0) && (qx < W);
+            if (in) {
+                const long long off = (long long)qy * W + qx;
+                const TL* lp = lg + off;
+                T e[NW];
+                if constexpr (NW <= 56) {
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(lp + t * hw);
+                    if constexpr (UP) {
+                        if constexpr (TIED) {
+                            T v = ld_logit<T>(lp + NT * hw);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) e[NT + i] = v;
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) e[NT + i] = ld_logit<T>(lp + (NT + i) * hw);
+                        }
+                    }
+                    if constexpr (PREV) {
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            e[NT + NUP + t] = ld_logit<T>(lp + (NT + NLUP + t) * hw);
+                    }
+                    T m = e[0];
+#pragma unroll
+                    for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
+                    T sum = (T)0;
+#pragma unroll
+                    for (int t = 0; t < NW; ++t) {
+                        e[t] = sexp(e[t] - m);
+                        sum += e[t];
+                    }
+                    const T inv = (T)1 / sum;
+#pragma unroll
+                    for (int t = 0; t < NW; ++t) SW(t, s, ri) = e[t] * inv;
+                } else {
+                    // large footprints: stage raw logits through shared memory
+                    T m = (T)-INFINITY;
+                    for (int t = 0; t < NW; ++t) {
+                        int ch;
+                        if (t < NT) ch = t;
+                        else if (t < NT + NUP) ch = TIED ? NT : t;
+                        else ch = t - NUP + NLUP;
+                        const T v = ld_logit<T>(lp + ch * hw);
+                        SW(t, s, ri) = v;
+                        m = tmax(m, v);
+                    }
+                    T sum = (T)0;
+                    for (int t = 0; t < NW; ++t) {
+                        const T ev = sexp(SW(t, s, ri) - m);
+                        SW(t, s, ri) = ev;
+                        sum += ev;
+                    }
+                    const T inv = (T)1 / sum;
+                    for (int t = 0; t < NW; ++t) SW(t, s, ri) *= inv;
+                }
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) {
+                    if (c < nc) {
+                        T g = gin[c * a.in_c + off];
+                        if (dem) g *= demod_clamp(dem[c * a.in_c + off]);
+                        SG(c, s, ri) = g;
+                    }
+                }
+            } else {
+                for (int t = 0; t < NW; ++t) SW(t, s, ri) = (T)0;
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) SG(c, s, ri) = (T)0;
+            }
+            load_image_row(qs + R + s, ri);
+        }
+        __syncthreads();
+
+        // ------------------------------------------------ B1: logit gradients
+        if (glg && tid < S * TXB) {
+            const int s = tid / TXB, xi = tid - s * TXB;
+            const int qy = qs + s, qx = x0 + xi;
+            if (qy >= y0 && qy < y1 && qx < W) {
+                const int ri = xi + R;
+                T gv[kMaxCh];
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) gv[c] = (c < nc) ? SG(c, s, ri) : (T)0;
+                const long long off = (long long)qy * W + qx;
+                TL* gp = glg + off;
+                int cy[2], cx[2];
+                if constexpr (UP) {
+                    cy[0] = min(qy >> 1, a.Hc - 1);
+                    cy[1] = min((qy + 1) >> 1, a.Hc - 1);
+                    cx[0] = min(qx >> 1, a.Wc - 1);
+                    cx[1] = min((qx + 1) >> 1, a.Wc - 1);
+                }
+                auto gw_of = [&](int t) -> T {
+                    T acc = (T)0;
+                    if (t < NT) {
+                        const int dy = t / K - R, dx = t % K - R;
+#pragma unroll
+                        for (int c = 0; c < kMaxCh; ++c)
+                            if (c < nc) acc += gv[c] * SLIN(c, qy + dy, ri + dx);
+                    } else if (t < NT + NUP) {
+                        const int i = (t - NT) >> 1, j = (t - NT) & 1;
+#pragma unroll
+                        for (int c = 0; c < kMaxCh; ++c)
+                            if (c < nc) acc += gv[c] * lhc[c * a.c_c + cy[i] * a.Wc + cx[j]];
+                    } else {
+                        const int tt = t - NT - NUP;
+                        const int dy = tt / K - R, dx = tt % K - R;
+#pragma unroll
+                        for (int c = 0; c < kMaxCh; ++c)
+                            if (c < nc) acc += gv[c] * SPRV(c, qy + dy, ri + dx);
+                    }
+                    return acc;
+                };
+                if constexpr (SH::REG_GW) {
+                    T gw[NW];
+#pragma unroll
+                    for (int t = 0; t < NW; ++t) gw[t] = gw_of(t);
+                    T inner = (T)0;
+#pragma unroll
+                    for (int t = 0; t < NW; ++t) inner += SW(t, s, ri) * gw[t];
+                    T gb = (T)0;
+#pragma unroll
+                    for (int t = 0; t < NW; ++t) {
+                        const T g = SW(t, s, ri) * (gw[t] - inner);
+                        if (TIED && t >= NT && t < NT + NUP) {
+                            gb += g;
+                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, a.accum);
+                        } else {
+                            const int ch = t < NT ? t : t - NUP + NLUP;
+                            st_glogit(gp + ch * hw, g, a.accum);
+                        }
+                    }
+                } else {
+                    T inner = (T)0;
+                    for (int t = 0; t < NW; ++t) inner += SW(t, s, ri) * gw_of(t);
+                    T gb = (T)0;
+                    for (int t = 0; t < NW; ++t) {
+                        const T g = SW(t, s, ri) * (gw_of(t) - inner);
+                        if (TIED && t >= NT && t < NT + NUP) {
+                            gb += g;
+                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, a.accum);
+                        } else {
+                            const int ch = t < NT ? t : t - NUP + NLUP;
+                            st_glogit(gp + ch * hw, g, a.accum);
+                        }
+                    }
+                }
+            }
+        }
+
+        // ------------------------------------------------ B2: gather transpose
+        for (int i = tid; i < (S + 2 * R) * TXB; i += BWD_THREADS) {
+            const int arow = i / TXB, xi = i - arow * TXB;
+            const int P = qs - R + arow;
+            const int gx = x0 + xi;
+            if (gx >= W) continue;
+            T acc[kMaxCh], pac[kMaxCh];
+#pragma unroll
+            for (int c = 0; c < kMaxCh; ++c) acc[c] = pac[c] = (T)0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int dy = P - (qs + s);
+                if (dy < -R || dy > R) continue;
+                const int tb = (dy + R) * K;
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) {
+                    const int ri = xi + R - dx;
+                    const T wv = SW(tb + dx + R, s, ri);
+#pragma unroll
+                    for (int c = 0; c < kMaxCh; ++c) acc[c] += wv * SG(c, s, ri);
+                    if constexpr (PREV) {
+                        const T pv = SW(NT + NUP + tb + dx + R, s, ri);
+#pragma unroll
+                        for (int c = 0; c < kMaxCh; ++c) pac[c] += pv * SG(c, s, ri);
+                    }
+                }
+                // clamp fold along x: logical columns beyond the border land on it
+                if (gx == 0 || gx == W - 1) {
+                    for (int side = 0; side < 2; ++side) {
+                        if (side == 0 && gx != 0) continue;
+                        if (side == 1 && gx != W - 1) continue;
+                        for (int e = 1; e <= R; ++e) {
+                            const int Pc = side == 0 ? -e : W - 1 + e;
+                            for (int dx = -R; dx <= R; ++dx) {
+                                const int qx = Pc - dx;
+                                if (qx < 0 || qx >= W) continue;
+                                const int ri = qx - xr0;
+                                const T wv = SW(tb + dx + R, s, ri);
+#pragma unroll
+                                for (int c = 0; c < kMaxCh; ++c) acc[c] += wv * SG(c, s, ri);
+                                if constexpr (PREV) {
+                                    const T pv = SW(NT + NUP + tb + dx + R, s, ri);
+#pragma unroll
+                                    for (int c = 0; c < kMaxCh; ++c) pac[c] += pv * SG(c, s, ri);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kMaxCh; ++c) {
+                SACC(c, P, xi) += acc[c];
+                if constexpr (PREV) SPAC(c, P, xi) += pac[c];
+            }
+        }
+
+        // ------------------------------------------------ B3: upsample transpose
+        if constexpr (UP) {
+            for (int i = tid; i < (S / 2 + 1) * TXC; i += BWD_THREADS) {
+                const int cyo = i / TXC, cxi = i - cyo * TXC;
+                const int Y = (qs >> 1) + cyo, X = (x0 >> 1) + cxi;
+                if (Y >= a.Hc || X >= a.Wc) continue;
+                T acc[kMaxCh];
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) acc[c] = (T)0;
+#pragma unroll
+                for (int yy = 2 * Y - 1; yy <= 2 * Y + 1; ++yy) {
+                    if (yy < qs || yy >= qs + S || yy >= H) continue;
+                    const int s = yy - qs;
+#pragma unroll
+                    for (int ii = 0; ii < 2; ++ii) {
+                        if (min((yy + ii) >> 1, a.Hc - 1) != Y) continue;
+#pragma unroll
+                        for (int xx = 2 * X - 1; xx <= 2 * X + 1; ++xx) {
+                            if (xx < 0 || xx >= W) continue;
+                            const int ri = xx - xr0;
+#pragma unroll
+                            for (int jj = 0; jj < 2; ++jj) {
+                                if (min((xx + jj) >> 1, a.Wc - 1) != X) continue;
+                                const T wv = SW(NT + ii * 2 + jj, s, ri);
+#pragma unroll
+                                for (int c = 0; c < kMaxCh; ++c) acc[c] += wv * SG(c, s, ri);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) SCAC(c, Y, cxi) += acc[c];
+            }
+        }
+        __syncthreads();
+
+        // ------------------------------------------------ flush finished rows
+        const bool bottom = qs + S >= H;
+        const int pend = bottom ? H : qs + S - R;
+        for (int i = tid; i < (pend - next_flush) * TXB; i += BWD_THREADS) {
+            const int rr = i / TXB, xi = i - rr * TXB;
+            const int P = next_flush + rr, gx = x0 + xi;
+            T v[kMaxCh], pv[kMaxCh];
+#pragma unroll
+            for (int c = 0; c < kMaxCh; ++c) {
+                v[c] = SACC(c, P, xi);
+                SACC(c, P, xi) = (T)0;
+                pv[c] = (T)0;
+                if constexpr (PREV) {
+                    pv[c] = SPAC(c, P, xi);
+                    SPAC(c, P, xi) = (T)0;
+                }
+            }
+            if (P == 0) {  // fold logical rows -R..-1 onto row 0
+                for (int e = 1; e <= R; ++e) {
+#pragma unroll
+                    for (int c = 0; c < kMaxCh; ++c) {
+                        v[c] += SACC(c, -e, xi);
+                        SACC(c, -e, xi) = (T)0;
+                        if constexpr (PREV) {
+                            pv[c] += SPAC(c, -e, xi);
+                            SPAC(c, -e, xi) = (T)0;
+                        }
+                    }
+                }
+            }
+            if (P == H - 1) {  // fold logical rows H..H+R-1 onto the last row
+                for (int e = 1; e <= R; ++e) {
+#pragma unroll
+                    for (int c = 0; c < kMaxCh; ++c) {
+                        v[c] += SACC(c, H - 1 + e, xi);
+                        SACC(c, H - 1 + e, xi) = (T)0;
+                        if constexpr (PREV) {
+                            pv[c] += SPAC(c, H - 1 + e, xi);
+                            SPAC(c, H - 1 + e, xi) = (T)0;
+                        }
+                    }
+                }
+            }
+            if (P < y0 || P >= y1 || gx >= W) continue;
+            const long long off = (long long)P * W + gx;
+            T* glo = (T*)a.gl_out + b * a.in_b;
+            if constexpr (L0) {
+                T* gdo = a.gdc_out ? (T*)a.gdc_out + b * a.in_b : nullptr;
+                T* gpo = PREV ? (T*)a.gprev_out + b * a.in_b : nullptr;
+                const T* up = (const T*)a.gin + b * a.in_b;
+                const T* op = a.outp ? (const T*)a.outp + b * a.in_b : nullptr;
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) {
+                    if (c >= nc) break;
+                    const long long o = c * a.in_c + off;
+                    if (dem) {
+                        const T dc = demod_clamp(dem[o]);
+                        glo[o] = v[c] / dc;
+                        if (gdo) {
+                            const T x0v = SLIN(c, P, xi + R);
+                            T gd = up[o] * (op[o] / dc) - v[c] * x0v / dc;
+                            if constexpr (PREV) gd -= pv[c] * SPRV(c, P, xi + R) / dc;
+                            gdo[o] = gd;
+                        }
+                        if constexpr (PREV) gpo[o] = pv[c] / dc;
+                    } else {
+                        glo[o] = v[c];
+                        if constexpr (PREV) gpo[o] = pv[c];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c)
+                    if (c < nc) glo[c * a.in_c + off] = v[c];
+            }
+        }
+        next_flush = pend;
+
+        if constexpr (UP) {
+            const int cend = bottom ? a.Hc : (qs + S) >> 1;
+            const int own0 = y0 >> 1, own1 = (y1 + 1) >> 1;
+            for (int i = tid; i < (cend - cnext) * TXC; i += BWD_THREADS) {
+                const int rr = i / TXC, cxi = i - rr * TXC;
+                const int Y = cnext + rr, X = (x0 >> 1) + cxi;
+                T v[kMaxCh];
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c) {
+                    v[c] = SCAC(c, Y, cxi);
+                    SCAC(c, Y, cxi) = (T)0;
+                }
+                if (Y < own0 || Y >= own1 || X >= a.Wc) continue;
+                T* gc = (T*)a.ghat_c + b * a.c_b + (long long)Y * a.Wc + X;
+#pragma unroll
+                for (int c = 0; c < kMaxCh; ++c)
+                    if (c < nc) gc[c * a.c_c] = v[c];
+            }
+            cnext = cend;
+        }
+        if (bottom) break;
+    }
+#undef SW
+#undef SG
+#undef SLIN
+#undef SPRV
+#undef SACC
+#undef SPAC
+#undef SCAC
+}
+
+// ===========================================================================
+// Pooling (level l -> l+1), count-correct 2x2 mean; level 0 demodulates first
+// ===========================================================================
+template <typename T>
+__global__ void k_pool2(int nc, int H, int W, const T* __restrict__ in, long long in_b,
+                        long long in_c, const T* __restrict__ dem, T* __restrict__ out,
+                        long long out_b, long long out_c) {
+    const int Hc = (H + 1) >> 1, Wc = (W + 1) >> 1;
+    const int X = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int b = blockIdx.z;
+    if (X >= Wc || Y >= Hc) return;
+    const int yb = 2 * Y, xb = 2 * X;
+    const bool hy = yb + 1 < H, hx = xb + 1 < W;
+    const T cnt = (T)((hy ? 2 : 1) * (hx ? 2 : 1));
+    for (int c = 0; c < nc; ++c) {
+        const T* p = in + b * in_b + c * in_c;
+        const T* d = dem ? dem + b * in_b + c * in_c : nullptr;
+        auto val = [&](int y, int x) -> T {
+            T v = p[(long long)y * W + x];
+            if (d) v = v / demod_clamp(d[(long long)y * W + x]);
+            return v;
+        };
+        // pyramid.py:144 sums the 2x2 block (zeros outside) then divides
+        T s00 = val(yb, xb);
+        T s01 = hx ? val(yb, xb + 1) : (T)0;
+        T s10 = hy ? val(yb + 1, xb) : (T)0;
+        T s11 = (hx && hy) ? val(yb + 1, xb + 1) : (T)0;
+        out[b * out_b + c * out_c + (long long)Y * Wc + X] = ((s00 + s01) + (s10 + s11)) / cnt;
+    }
+}
+
+// ===========================================================================
+// Final coarse->fine sweep: g^{L-1} = gL_{L-1}; g^l = pool^T(g^{l+1}) + gL_l;
+// then the level-0 combination with the partials written by the level-0
+// backward kernel (pyramid.py:415-447).  One thread per level-0 pixel walks
+// its ancestor chain, so the per-element arithmetic order equals the
+// reference's level-by-level loop.
+// ===========================================================================
+struct FinalArgs {
+    int nc, H, W, levels;
+    int dims_h[SSB_MAX_LEVELS], dims_w[SSB_MAX_LEVELS];
+    const void* gl[SSB_MAX_LEVELS];  // gL_l for l >= 1 (B, C, H_l, W_l), group-offset
+    long long gl_b[SSB_MAX_LEVELS], gl_c[SSB_MAX_LEVELS];
+    const void* noisy;
+    const void* demod;
+    long long in_b, in_c;
+    void* g_noisy;  // in: partial, out: final
+    void* g_demod;  // in: partial gdc, out: final (masked); may be null
+};
+
+template <typename T>
+__global__ void k_pyr_final(const FinalArgs a) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int b = blockIdx.z;
+    if (x >= a.W || y >= a.H) return;
+    const long long off = (long long)y * a.W + x;
+    for (int c = 0; c < a.nc; ++c) {
+        T pb = (T)0;
+        if (a.levels > 1) {
+            const int top = a.levels - 1;
+            const T* gt = (const T*)a.gl[top] + b * a.gl_b[top] + c * a.gl_c[top];
+            T v = gt[(long long)(y >> top) * a.dims_w[top] + (x >> top)];
+            for (int l = top - 1; l >= 0; --l) {
+                // count of the level-(l+1) ancestor's children at level l
+                const int Y = y >> (l + 1), X = x >> (l + 1);
+                const int hy = (2 * Y + 1 < a.dims_h[l]) ? 2 : 1;
+                const int hx = (2 * X + 1 < a.dims_w[l]) ? 2 : 1;
+                v = v / (T)(hy * hx);
+                if (l == 0) break;
+                const T* gl = (const T*)a.gl[l] + b * a.gl_b[l] + c * a.gl_c[l];
+                v = v + gl[(long long)(y >> l) * a.dims_w[l] + (x >> l)];
+            }
+            pb = v;
+        }
+        const long long o = b * a.in_b + c * a.in_c + off;
+        T* gn = (T*)a.g_noisy;
+        if (a.demod) {
+            const T dv = ((const T*)a.demod)[o];
+            const T dc = demod_clamp(dv);
+            gn[o] = gn[o] + pb / dc;
+            if (a.g_demod) {
+                T* gd = (T*)a.g_demod;
+                const T x0 = ((const T*)a.noisy)[o] / dc;
+                const T gdc = gd[o] - pb * x0 / dc;
+                gd[o] = dv > (T)kDemodFloor ? gdc : (T)0;
+            }
+        } else {
+            gn[o] = gn[o] + pb;
+        }
+    }
+}
+
+}  // namespace ssb

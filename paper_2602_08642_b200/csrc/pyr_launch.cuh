@@ -1,0 +1,252 @@
+// Host-side launch sequences for the pyramid filter (one instantiation per k).
+#pragma once
+
+#include <string>
+
+#include "pyr_kernels.cuh"
+
+namespace ssb {
+
+void set_error(const std::string& msg);
+int cuda_check(const char* where);
+
+struct PyrPlan {
+    int B, C, H, W, L, K;
+    int hl[SSB_MAX_LEVELS], wl[SSB_MAX_LEVELS];
+    int nlog[SSB_MAX_LEVELS];
+    size_t esz;    // image element size
+    size_t lgesz;  // logit element size
+    // tape: pooled L^l and Lhat^l for l >= 1 (byte offsets)
+    size_t pool_off[SSB_MAX_LEVELS], lhat_off[SSB_MAX_LEVELS], tape_bytes;
+    // workspace: ghat^l and gL_l for l >= 1
+    size_t ghat_off[SSB_MAX_LEVELS], gl_off[SSB_MAX_LEVELS], ws_bytes;
+};
+
+int make_plan(const ssb_pyr_desc* d, PyrPlan* p);
+
+inline long long lvl_elems(const PyrPlan& p, int l) { return (long long)p.hl[l] * p.wl[l]; }
+
+template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
+void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
+    dim3 block(FWD_TX, FWD_TY);
+    dim3 grid((a.W + FWD_TX - 1) / FWD_TX, (a.H + FWD_TY - 1) / FWD_TY, B);
+    k_pyr_fwd<K, TL, T, L0, UP, TIED, PREV><<<grid, block, 0, s>>>(a);
+}
+
+template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
+void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
+    using SH = BwdShape<K, UP, PREV, T>;
+    auto kern = k_pyr_bwd<K, TL, T, L0, UP, TIED, PREV>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        attr_set = true;
+    }
+    BwdLevel a = a0;
+    const int strips = (a.W + SH::TXB - 1) / SH::TXB;
+    // segment height: keep >= ~8 CTAs per SM resident work, amortise the halo
+    int seg = 128;
+    while (seg > 16 && (long long)strips * ((a.H + seg - 1) / seg) * B < 148 * 8) seg >>= 1;
+    a.seg_h = seg;
+    dim3 grid(strips, (a.H + seg - 1) / seg, B);
+    kern<<<grid, BWD_THREADS, SH::SMEM, s>>>(a);
+}
+
+template <int K, typename TL, typename T>
+void dispatch_fwd(const FwdLevel& a, int B, bool l0, bool up, bool tied, bool prev,
+                  cudaStream_t s) {
+    if (l0) {
+        if (up) {
+            if (tied) {
+                if (prev) launch_fwd_one<K, TL, T, true, true, true, true>(a, B, s);
+                else launch_fwd_one<K, TL, T, true, true, true, false>(a, B, s);
+            } else {
+                if (prev) launch_fwd_one<K, TL, T, true, true, false, true>(a, B, s);
+                else launch_fwd_one<K, TL, T, true, true, false, false>(a, B, s);
+            }
+        } else {
+            if (prev) launch_fwd_one<K, TL, T, true, false, false, true>(a, B, s);
+            else launch_fwd_one<K, TL, T, true, false, false, false>(a, B, s);
+        }
+    } else if (up) {
+        if (tied) launch_fwd_one<K, TL, T, false, true, true, false>(a, B, s);
+        else launch_fwd_one<K, TL, T, false, true, false, false>(a, B, s);
+    } else {
+        launch_fwd_one<K, TL, T, false, false, false, false>(a, B, s);
+    }
+}
+
+template <int K, typename TL, typename T>
+void dispatch_bwd(const BwdLevel& a, int B, bool l0, bool up, bool tied, bool prev,
+                  cudaStream_t s) {
+    if (l0) {
+        if (up) {
+            if (tied) {
+                if (prev) launch_bwd_one<K, TL, T, true, true, true, true>(a, B, s);
+                else launch_bwd_one<K, TL, T, true, true, true, false>(a, B, s);
+            } else {
+                if (prev) launch_bwd_one<K, TL, T, true, true, false, true>(a, B, s);
+                else launch_bwd_one<K, TL, T, true, true, false, false>(a, B, s);
+            }
+        } else {
+            if (prev) launch_bwd_one<K, TL, T, true, false, false, true>(a, B, s);
+            else launch_bwd_one<K, TL, T, true, false, false, false>(a, B, s);
+        }
+    } else if (up) {
+        if (tied) launch_bwd_one<K, TL, T, false, true, true, false>(a, B, s);
+        else launch_bwd_one<K, TL, T, false, true, false, false>(a, B, s);
+    } else {
+        launch_bwd_one<K, TL, T, false, false, false, false>(a, B, s);
+    }
+}
+
+template <typename T>
+void launch_pool(int B, int nc, int H, int W, const T* in, long long in_b, long long in_c,
+                 const T* dem, T* out, long long out_b, long long out_c, cudaStream_t s) {
+    const int Hc = (H + 1) >> 1, Wc = (W + 1) >> 1;
+    dim3 block(32, 8);
+    dim3 grid((Wc + 31) / 32, (Hc + 7) / 8, B);
+    k_pool2<T><<<grid, block, 0, s>>>(nc, H, W, in, in_b, in_c, dem, out, out_b, out_c);
+}
+
+template <int K, typename TL, typename T>
+int run_forward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_fwd_io* io, void* tape,
+                cudaStream_t s) {
+    char* tp = (char*)tape;
+    const bool tied = d->blend_mode == SSB_BLEND_TIED;
+    const long long img_b = (long long)p.C * p.H * p.W;
+    for (int c0 = 0; c0 < p.C; c0 += kMaxCh) {
+        const int nc = p.C - c0 < kMaxCh ? p.C - c0 : kMaxCh;
+        const long long coff0 = (long long)c0 * p.H * p.W;
+        const T* noisy = (const T*)io->noisy + coff0;
+        const T* dem = io->demod ? (const T*)io->demod + coff0 : nullptr;
+        // pooled pyramid of the demodulated input
+        for (int l = 1; l < p.L; ++l) {
+            const long long e_prev = lvl_elems(p, l - 1), e_l = lvl_elems(p, l);
+            const T* src = l == 1 ? noisy
+                                  : (const T*)(tp + p.pool_off[l - 1]) + (long long)c0 * e_prev;
+            T* dst = (T*)(tp + p.pool_off[l]) + (long long)c0 * e_l;
+            const long long sb = l == 1 ? img_b : (long long)p.C * e_prev;
+            launch_pool<T>(p.B, nc, p.hl[l - 1], p.wl[l - 1], src, sb, e_prev,
+                           l == 1 ? dem : nullptr, dst, (long long)p.C * e_l, e_l, s);
+        }
+        // coarse -> fine
+        for (int l = p.L - 1; l >= 0; --l) {
+            FwdLevel a{};
+            a.nc = nc;
+            a.H = p.hl[l];
+            a.W = p.wl[l];
+            const long long e_l = lvl_elems(p, l);
+            a.logits = io->logits[l];
+            a.lg_b = (long long)p.nlog[l] * e_l;
+            a.in_b = (long long)p.C * e_l;
+            a.in_c = e_l;
+            if (l == 0) {
+                a.lin = noisy;
+                a.demod = dem;
+                a.prev = io->prev ? (const T*)io->prev + coff0 : nullptr;
+                a.out = (T*)io->out + coff0;
+            } else {
+                a.lin = (const T*)(tp + p.pool_off[l]) + (long long)c0 * e_l;
+                a.out = (T*)(tp + p.lhat_off[l]) + (long long)c0 * e_l;
+            }
+            const bool up = l < p.L - 1;
+            if (up) {
+                const long long e_c = lvl_elems(p, l + 1);
+                a.Hc = p.hl[l + 1];
+                a.Wc = p.wl[l + 1];
+                a.lhat_c = (const T*)(tp + p.lhat_off[l + 1]) + (long long)c0 * e_c;
+                a.c_b = (long long)p.C * e_c;
+                a.c_c = e_c;
+            }
+            dispatch_fwd<K, TL, T>(a, p.B, l == 0, up, tied, l == 0 && d->has_prev, s);
+        }
+    }
+    return cuda_check("ssb_pyr_forward");
+}
+
+template <int K, typename TL, typename T>
+int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io,
+                 const void* tape, void* ws, cudaStream_t s) {
+    const char* tp = (const char*)tape;
+    char* wp = (char*)ws;
+    const bool tied = d->blend_mode == SSB_BLEND_TIED;
+    const bool want = io->g_logits[0] != nullptr;
+    for (int c0 = 0; c0 < p.C; c0 += kMaxCh) {
+        const int nc = p.C - c0 < kMaxCh ? p.C - c0 : kMaxCh;
+        const long long coff0 = (long long)c0 * p.H * p.W;
+        const int accum = (io->accumulate_logits || c0 > 0) ? 1 : 0;
+        for (int l = 0; l < p.L; ++l) {
+            BwdLevel a{};
+            a.nc = nc;
+            a.H = p.hl[l];
+            a.W = p.wl[l];
+            const long long e_l = lvl_elems(p, l);
+            a.want_params = want ? 1 : 0;
+            a.accum = accum;
+            a.logits = io->logits[l];
+            a.lg_b = (long long)p.nlog[l] * e_l;
+            a.glogits = want ? io->g_logits[l] : nullptr;
+            a.in_b = (long long)p.C * e_l;
+            a.in_c = e_l;
+            if (l == 0) {
+                a.lin = (const T*)io->noisy + coff0;
+                a.demod = io->demod ? (const T*)io->demod + coff0 : nullptr;
+                a.prev = io->prev ? (const T*)io->prev + coff0 : nullptr;
+                a.gin = (const T*)io->upstream + coff0;
+                a.outp = io->out ? (const T*)io->out + coff0 : nullptr;
+                a.gl_out = (T*)io->g_noisy + coff0;
+                a.gdc_out = (io->g_demod && io->demod) ? (T*)io->g_demod + coff0 : nullptr;
+                a.gprev_out = io->g_prev ? (T*)io->g_prev + coff0 : nullptr;
+            } else {
+                a.lin = (const T*)(tp + p.pool_off[l]) + (long long)c0 * e_l;
+                a.gin = (const T*)(wp + p.ghat_off[l]) + (long long)c0 * e_l;
+                a.gl_out = (T*)(wp + p.gl_off[l]) + (long long)c0 * e_l;
+            }
+            const bool up = l < p.L - 1;
+            if (up) {
+                const long long e_c = lvl_elems(p, l + 1);
+                a.Hc = p.hl[l + 1];
+                a.Wc = p.wl[l + 1];
+                a.lhat_c = (const T*)(tp + p.lhat_off[l + 1]) + (long long)c0 * e_c;
+                a.ghat_c = (T*)(wp + p.ghat_off[l + 1]) + (long long)c0 * e_c;
+                a.c_b = (long long)p.C * e_c;
+                a.c_c = e_c;
+            }
+            dispatch_bwd<K, TL, T>(a, p.B, l == 0, up, tied, l == 0 && d->has_prev, s);
+        }
+        FinalArgs f{};
+        f.nc = nc;
+        f.H = p.H;
+        f.W = p.W;
+        f.levels = p.L;
+        for (int l = 0; l < p.L; ++l) {
+            f.dims_h[l] = p.hl[l];
+            f.dims_w[l] = p.wl[l];
+            if (l >= 1) {
+                const long long e_l = lvl_elems(p, l);
+                f.gl[l] = (const T*)(wp + p.gl_off[l]) + (long long)c0 * e_l;
+                f.gl_b[l] = (long long)p.C * e_l;
+                f.gl_c[l] = e_l;
+            }
+        }
+        f.noisy = (const T*)io->noisy + coff0;
+        f.demod = io->demod ? (const T*)io->demod + coff0 : nullptr;
+        f.in_b = (long long)p.C * p.H * p.W;
+        f.in_c = (long long)p.H * p.W;
+        f.g_noisy = (T*)io->g_noisy + coff0;
+        f.g_demod = (io->g_demod && io->demod) ? (T*)io->g_demod + coff0 : nullptr;
+        dim3 block(32, 8);
+        dim3 grid((p.W + 31) / 32, (p.H + 7) / 8, p.B);
+        k_pyr_final<T><<<grid, block, 0, s>>>(f);
+    }
+    return cuda_check("ssb_pyr_backward");
+}
+
+#define SSB_INSTANTIATE_PYR(K, TL, T)                                                       \
+    template int run_forward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,                 \
+                                       const ssb_pyr_fwd_io*, void*, cudaStream_t);         \
+    template int run_backward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,                \
+                                        const ssb_pyr_bwd_io*, const void*, void*, cudaStream_t);
+
+}  // namespace ssb

@@ -1,0 +1,413 @@
+"""Torch-tensor API over the sm_100a kernels (device-resident, planar layout).
+
+Layouts (all contiguous CUDA tensors):
+  images  (B, C, H, W)   float32 or float64, any C
+  logits  list over levels l of (B, C_l, H_l, W_l), H_l = ceil(H / 2^l),
+          C_l = k*k (+4 upsample logits, or +1 tied blend logit, if l < L-1)
+          (+k*k temporal logits at l = 0 when a history `prev` is given)
+          float32 / bfloat16 (with float32 images) or float64 (with float64)
+
+Every call goes through libssb200.so (include/ssb_api.h) on the current torch
+stream.  There is no eager/PyTorch fallback for any op in this module.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+_DT = {torch.float32: _lib.SSB_F32, torch.bfloat16: _lib.SSB_BF16, torch.float64: _lib.SSB_F64}
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _need(t, name, device=None, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} must live on {device}")
+    return t
+
+
+# ---------------------------------------------------------------------------
+# geometry
+
+
+def level_shapes(height: int, width: int, levels: int) -> list[tuple[int, int]]:
+    shapes = [(height, width)]
+    while len(shapes) < levels:
+        h, w = shapes[-1]
+        shapes.append(((h + 1) // 2, (w + 1) // 2))
+    return shapes
+
+
+def logit_channels(level: int, levels: int, ksize: int, has_prev: bool = False,
+                   blend: str = "native") -> int:
+    n = ksize * ksize
+    if level < levels - 1:
+        n += 4 if blend == "native" else 1
+    if level == 0 and has_prev:
+        n += ksize * ksize
+    return n
+
+
+def _desc(noisy, logits, demod, prev, ksize, blend) -> _lib.PyrDesc:
+    B, Cc, H, W = noisy.shape
+    L = len(logits)
+    if L < 1 or L > _lib.SSB_MAX_LEVELS:
+        raise ValueError(f"need 1..{_lib.SSB_MAX_LEVELS} levels of logits")
+    if ksize is None:
+        k2 = logits[-1].shape[1]
+        ksize = int(round(k2 ** 0.5))
+    if blend not in ("native", "tied"):
+        raise ValueError("blend must be 'native' or 'tied'")
+    for l, ((h, w), z) in enumerate(zip(level_shapes(H, W, L), logits)):
+        expect = (B, logit_channels(l, L, ksize, prev is not None, blend), h, w)
+        if tuple(z.shape) != expect:
+            raise ValueError(f"level {l} logits must have shape {expect}, got {tuple(z.shape)}")
+        if z.dtype != logits[0].dtype:
+            raise ValueError("all logit levels must share one dtype")
+    d = _lib.PyrDesc()
+    d.batch, d.channels, d.height, d.width = B, Cc, H, W
+    d.levels, d.ksize = L, ksize
+    d.image_dtype = _DT[noisy.dtype]
+    d.logit_dtype = _DT[logits[0].dtype]
+    d.has_prev = int(prev is not None)
+    d.has_demod = int(demod is not None)
+    d.blend_mode = _lib.SSB_BLEND_TIED if blend == "tied" else _lib.SSB_BLEND_NATIVE
+    return d
+
+
+@dataclass
+class PyramidTape:
+    """Device tape of one forward call (opaque to callers, like the reference's
+    ReconTape): pooled levels and partial reconstructions plus the inputs."""
+    desc: _lib.PyrDesc
+    buf: torch.Tensor | None
+    noisy: torch.Tensor
+    logits: list
+    demod: torch.Tensor | None
+    prev: torch.Tensor | None
+    out: torch.Tensor
+
+    @property
+    def levels(self) -> int:
+        return self.desc.levels
+
+
+@dataclass
+class PyramidGrads:
+    logits: list | None
+    demod: torch.Tensor | None
+    input: torch.Tensor
+    prev: torch.Tensor | None
+
+
+def pyramid_forward(noisy, logits, demod=None, prev=None, *, ksize=None, blend="native",
+                    out=None) -> tuple[torch.Tensor, PyramidTape]:
+    """Coarse-to-fine reconstruction (ref pyramid.py `reconstruct_core`)."""
+    lib = _lib.load()
+    _need(noisy, "noisy")
+    if noisy.dim() != 4 or noisy.dtype not in (torch.float32, torch.float64):
+        raise ValueError("noisy must be (B, C, H, W) float32/float64")
+    dev = noisy.device
+    logits = [_need(z, f"logits[{l}]", dev) for l, z in enumerate(logits)]
+    for name, t in (("demod", demod), ("prev", prev)):
+        if t is not None:
+            _need(t, name, dev, noisy.dtype)
+            if t.shape != noisy.shape:
+                raise ValueError(f"{name} must match noisy's shape")
+    d = _desc(noisy, logits, demod, prev, ksize, blend)
+    tb = C.c_size_t()
+    check(lib.ssb_pyr_tape_bytes(C.byref(d), C.byref(tb)), "ssb_pyr_tape_bytes")
+    buf = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=dev)
+    if out is None:
+        out = torch.empty_like(noisy)
+    io = _lib.PyrFwdIO()
+    io.noisy, io.demod, io.prev, io.out = (_ptr(noisy), _ptr(demod), _ptr(prev), _ptr(out))
+    for l, z in enumerate(logits):
+        io.logits[l] = z.data_ptr()
+    with torch.cuda.device(dev):
+        check(lib.ssb_pyr_forward(C.byref(d), C.byref(io), _ptr(buf), _stream(dev)),
+              "ssb_pyr_forward")
+    return out, PyramidTape(d, buf, noisy, logits, demod, prev, out)
+
+
+def pyramid_backward(tape: PyramidTape, upstream, want_param_grads: bool = True,
+                     accumulate_into: list | None = None) -> PyramidGrads:
+    """Exact gradients of sum(upstream * out) (ref `reconstruct_backward`).
+
+    accumulate_into: optional list of per-level logit-gradient tensors that
+    receive ``+=`` (frame-summed parameter gradients without an extra pass)."""
+    lib = _lib.load()
+    dev = tape.noisy.device
+    _need(upstream, "upstream", dev, tape.noisy.dtype)
+    if upstream.shape != tape.noisy.shape:
+        raise ValueError("upstream must match the filter output's shape")
+    d = tape.desc
+    wb = C.c_size_t()
+    check(lib.ssb_pyr_workspace_bytes(C.byref(d), C.byref(wb)), "ssb_pyr_workspace_bytes")
+    ws = torch.empty(max(wb.value, 1), dtype=torch.uint8, device=dev)
+    g_noisy = torch.empty_like(tape.noisy)
+    g_demod = torch.empty_like(tape.noisy) if (want_param_grads and tape.demod is not None) else None
+    g_prev = torch.empty_like(tape.noisy) if tape.prev is not None else None
+    io = _lib.PyrBwdIO()
+    io.noisy, io.demod, io.prev = _ptr(tape.noisy), _ptr(tape.demod), _ptr(tape.prev)
+    io.out, io.upstream = _ptr(tape.out), _ptr(upstream)
+    io.g_noisy, io.g_demod, io.g_prev = _ptr(g_noisy), _ptr(g_demod), _ptr(g_prev)
+    g_logits = None
+    if want_param_grads:
+        if accumulate_into is not None:
+            g_logits = [_need(g, f"accumulate_into[{l}]", dev, z.dtype)
+                        for l, (g, z) in enumerate(zip(accumulate_into, tape.logits))]
+            io.accumulate_logits = 1
+        else:
+            g_logits = [torch.empty_like(z) for z in tape.logits]
+        for l, g in enumerate(g_logits):
+            io.g_logits[l] = g.data_ptr()
+    for l, z in enumerate(tape.logits):
+        io.logits[l] = z.data_ptr()
+    with torch.cuda.device(dev):
+        check(lib.ssb_pyr_backward(C.byref(d), C.byref(io), _ptr(tape.buf), _ptr(ws), _stream(dev)),
+              "ssb_pyr_backward")
+    return PyramidGrads(g_logits, g_demod, g_noisy, g_prev)
+
+
+class _PyramidFilterFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, noisy, demod, prev, ksize, blend, *logits):
+        out, tape = pyramid_forward(noisy, list(logits), demod, prev, ksize=ksize, blend=blend)
+        ctx.tape = tape
+        ctx.has_demod = demod is not None
+        ctx.has_prev = prev is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, gout):
+        want = any(ctx.needs_input_grad[5:]) or (ctx.has_demod and ctx.needs_input_grad[1])
+        g = pyramid_backward(ctx.tape, gout.contiguous(), want_param_grads=want)
+        glog = g.logits if g.logits is not None else [None] * ctx.tape.levels
+        return (g.input, g.demod, g.prev, None, None, *glog)
+
+
+def pyramid_filter(noisy, logits, demod=None, prev=None, *, ksize=None, blend="native"):
+    """Autograd-enabled filter: out = remod(pyramid(demod(noisy), softmax(logits)))."""
+    return _PyramidFilterFn.apply(noisy, demod, prev, ksize, blend, *logits)
+
+
+# ---------------------------------------------------------------------------
+# primitives (ref pyramid.py surface helpers)
+
+
+def softmax_channels(logits, active=None):
+    lib = _lib.load()
+    _need(logits, "logits")
+    B, Cc, H, W = logits.shape
+    out = torch.empty_like(logits)
+    with torch.cuda.device(logits.device):
+        check(lib.ssb_softmax_channels(_DT[logits.dtype], B, Cc, H, W, Cc if active is None else active,
+                                       _ptr(logits), _ptr(out), _stream(logits.device)),
+              "ssb_softmax_channels")
+    return out
+
+
+def gather(image, weights, ksize):
+    lib = _lib.load()
+    _need(image, "image")
+    _need(weights, "weights", image.device, image.dtype)
+    B, Cc, H, W = image.shape
+    if tuple(weights.shape) != (B, ksize * ksize, H, W):
+        raise ValueError("weights must be (B, k*k, H, W)")
+    out = torch.empty_like(image)
+    with torch.cuda.device(image.device):
+        check(lib.ssb_gather(_DT[image.dtype], B, Cc, H, W, ksize, _ptr(image), _ptr(weights),
+                             _ptr(out), _stream(image.device)), "ssb_gather")
+    return out
+
+
+def upsample2(coarse, weights):
+    lib = _lib.load()
+    _need(coarse, "coarse")
+    _need(weights, "weights", coarse.device, coarse.dtype)
+    B, Cc, Hc, Wc = coarse.shape
+    Hf, Wf = weights.shape[2:]
+    if weights.shape[:2] != (B, 4):
+        raise ValueError("weights must be (B, 4, Hf, Wf)")
+    out = torch.empty((B, Cc, Hf, Wf), dtype=coarse.dtype, device=coarse.device)
+    with torch.cuda.device(coarse.device):
+        check(lib.ssb_upsample2(_DT[coarse.dtype], B, Cc, Hc, Wc, Hf, Wf, _ptr(coarse),
+                                _ptr(weights), _ptr(out), _stream(coarse.device)), "ssb_upsample2")
+    return out
+
+
+def avgpool2(img):
+    lib = _lib.load()
+    _need(img, "img")
+    B, Cc, H, W = img.shape
+    out = torch.empty((B, Cc, (H + 1) // 2, (W + 1) // 2), dtype=img.dtype, device=img.device)
+    with torch.cuda.device(img.device):
+        check(lib.ssb_avgpool2(_DT[img.dtype], B, Cc, H, W, _ptr(img), _ptr(out),
+                               _stream(img.device)), "ssb_avgpool2")
+    return out
+
+
+def build_pyramid(img, levels):
+    lv = [img]
+    for _ in range(levels - 1):
+        lv.append(avgpool2(lv[-1]))
+    return lv
+
+
+# ---------------------------------------------------------------------------
+# placement (ref rng.py, density.py, estimators.py)
+
+
+def uniform_grid(seed: int, height: int, width: int, frame0: int = 0, batch: int = 1,
+                 frames=None, stream_id: int = 0, device="cuda"):
+    lib = _lib.load()
+    dev = torch.device(device)
+    fr = None
+    if frames is not None:
+        fr = torch.as_tensor(frames, dtype=torch.int64, device=dev).contiguous()
+        batch = fr.numel()
+    u = torch.empty((batch, height, width), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib.ssb_uniform_grid(seed & (2**64 - 1), frame0, _ptr(fr), batch, height, width,
+                                   stream_id & (2**64 - 1), _ptr(u), _stream(dev)),
+              "ssb_uniform_grid")
+    return u
+
+
+def normalize_density(scores, budget: float):
+    lib = _lib.load()
+    _need(scores, "scores", dtype=torch.float64)
+    if scores.dim() == 2:
+        scores = scores[None]
+    B, H, W = scores.shape
+    wb = C.c_size_t()
+    check(lib.ssb_density_workspace_bytes(B, H, W, C.byref(wb)), "ssb_density_workspace_bytes")
+    ws = torch.empty(wb.value, dtype=torch.uint8, device=scores.device)
+    spp = torch.empty_like(scores)
+    with torch.cuda.device(scores.device):
+        check(lib.ssb_normalize_density(B, H, W, _ptr(scores), float(budget), _ptr(spp), _ptr(ws),
+                                        _stream(scores.device)), "ssb_normalize_density")
+    return spp
+
+
+def allocate(spp, mode="stochastic", rank=None, frame0=0, seed=0, rule="stochastic",
+             gumbel_temp=1.0):
+    lib = _lib.load()
+    _need(spp, "spp", dtype=torch.float64)
+    if spp.dim() == 2:
+        spp = spp[None]
+    B, H, W = spp.shape
+    if rule not in _lib.RULES:
+        raise ValueError(f"unknown take rule {rule!r}")
+    if mode not in ("stochastic", "dithered"):
+        raise ValueError(f"unknown allocation mode {mode!r}")
+    d = _lib.AllocDesc(B, H, W, _lib.RULES[rule], int(mode == "dithered"), 0, seed & (2**64 - 1),
+                       frame0, float(gumbel_temp))
+    rk = None
+    if mode == "dithered":
+        if rank is None:
+            raise ValueError("dithered allocation requires a mask")
+        rk = torch.as_tensor(rank, dtype=torch.int64, device=spp.device).contiguous()
+        d.mask_size = rk.shape[0]
+    base = torch.empty(spp.shape, dtype=torch.int64, device=spp.device)
+    frac = torch.empty_like(spp)
+    u = torch.empty_like(spp)
+    taken = torch.empty(spp.shape, dtype=torch.uint8, device=spp.device)
+    with torch.cuda.device(spp.device):
+        check(lib.ssb_allocate(C.byref(d), _ptr(spp), _ptr(rk), _ptr(base), _ptr(frac), _ptr(u),
+                               _ptr(taken), _stream(spp.device)), "ssb_allocate")
+    return base, frac, u, taken.bool()
+
+
+def _est_desc(variant, B, H, W, capacity, lam, gumbel_temp, density_floor):
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"{variant!r} is not a stochastic variant")
+    return _lib.EstimateDesc(B, H, W, _lib.VARIANTS[variant], capacity, 0, float(lam),
+                             float(gumbel_temp), float(density_floor))
+
+
+def stochastic_core(variant, spp, frac, u, base_sum, holdout, lam=10.0, gumbel_temp=1.0,
+                    density_floor=1e-8):
+    lib = _lib.load()
+    for n, t in (("spp", spp), ("frac", frac), ("u", u), ("base_sum", base_sum),
+                 ("holdout", holdout)):
+        _need(t, n, dtype=torch.float64)
+    shape = spp.shape
+    n = spp.numel()
+    d = _est_desc(variant, 1, 1, n, 1, lam, gumbel_temp, density_floor)
+    noisy = torch.empty(shape + (3,), dtype=torch.float64, device=spp.device)
+    grad, contrib = torch.empty_like(noisy), torch.empty_like(noisy)
+    drawn = torch.empty(shape, dtype=torch.uint8, device=spp.device)
+    with torch.cuda.device(spp.device):
+        check(lib.ssb_stochastic_core(C.byref(d), _ptr(spp), _ptr(frac), _ptr(u), _ptr(base_sum),
+                                      _ptr(holdout), _ptr(noisy), _ptr(grad), _ptr(contrib),
+                                      _ptr(drawn), _stream(spp.device)), "ssb_stochastic_core")
+    return noisy, grad, contrib, drawn.bool()
+
+
+def estimate(variant, spp, base, frac, u, samples, lam=10.0, gumbel_temp=1.0,
+             density_floor=1e-8, want_planar32=False):
+    """Bank read + stochastic_core (ref `_stochastic_estimate`); samples are
+    (B, H, W, S, 3) float64 like SampleBank.samples."""
+    lib = _lib.load()
+    if spp.dim() == 2:
+        spp, base, frac, u, samples = spp[None], base[None], frac[None], u[None], samples[None]
+    B, H, W = spp.shape
+    S = samples.shape[3]
+    _need(samples, "samples", dtype=torch.float64)
+    d = _est_desc(variant, B, H, W, S, lam, gumbel_temp, density_floor)
+    noisy = torch.empty((B, H, W, 3), dtype=torch.float64, device=spp.device)
+    grad, contrib = torch.empty_like(noisy), torch.empty_like(noisy)
+    used = torch.empty((B, H, W), dtype=torch.int64, device=spp.device)
+    n32 = torch.empty((B, 3, H, W), dtype=torch.float32, device=spp.device) if want_planar32 else None
+    with torch.cuda.device(spp.device):
+        check(lib.ssb_estimate(C.byref(d), _ptr(spp), _ptr(base), _ptr(frac), _ptr(u),
+                               _ptr(samples), _ptr(noisy), _ptr(grad), _ptr(contrib), _ptr(used),
+                               _ptr(n32), _stream(spp.device)), "ssb_estimate")
+    return noisy, grad, contrib, used, n32
+
+
+def place_fused(scores, bank, budget: float, seed: int = 0, frame0: int = 0, noisy=None,
+                want_spp=False, want_taken=False, workspace=None):
+    """Inference placement: scores (B,H,W) f32, bank (B,S,3,H,W) f32 ->
+    noisy (B,3,H,W) f32 (sample-count-weighted radiance at the allocated counts)."""
+    lib = _lib.load()
+    _need(scores, "scores", dtype=torch.float32)
+    _need(bank, "bank", scores.device, torch.float32)
+    B, H, W = scores.shape
+    S = bank.shape[1]
+    if tuple(bank.shape) != (B, S, 3, H, W):
+        raise ValueError("bank must be (B, S, 3, H, W)")
+    if noisy is None:
+        noisy = torch.empty((B, 3, H, W), dtype=torch.float32, device=scores.device)
+    spp = torch.empty((B, H, W), dtype=torch.float32, device=scores.device) if want_spp else None
+    taken = torch.empty((B, H, W), dtype=torch.uint8, device=scores.device) if want_taken else None
+    if workspace is None:
+        wb = C.c_size_t()
+        check(lib.ssb_density_workspace_bytes(B, H, W, C.byref(wb)), "ssb_density_workspace_bytes")
+        workspace = torch.empty(wb.value, dtype=torch.uint8, device=scores.device)
+    d = _lib.PlaceDesc(B, H, W, S, 0, 0, seed & (2**64 - 1), frame0, float(budget))
+    with torch.cuda.device(scores.device):
+        check(lib.ssb_place_fused(C.byref(d), _ptr(scores), _ptr(bank), _ptr(noisy), _ptr(spp),
+                                  _ptr(taken), _ptr(workspace), _stream(scores.device)),
+              "ssb_place_fused")
+    return noisy, spp, taken

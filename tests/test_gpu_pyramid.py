@@ -1,0 +1,286 @@
+"""GPU parity of the gather-pyramid filter (forward + backward) vs the reference.
+
+Golden fixtures are outputs of the unmodified reference; larger and k != 5
+cases compare against the oracle restatement (itself pinned to the fixtures).
+Tolerances (north star): float64 path ~1e-10; float32 path rtol 1e-5 with an
+atol floor of 1e-5 * max|ref| (softmax-backward cancellation); bf16 logits
+rtol 2e-2 with a 2e-2 * max|ref| floor.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import pyramid as op  # noqa: E402
+from tests._conv import (assert_close, device_glogits_to_ref, hwc_to_planar,  # noqa: E402
+                         planar_to_hwc, ref_logits_to_device)
+from tests._golden import case_logits, load, pyramid_cases  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_08642_b200 import ops as _ops
+    return _ops
+
+
+def run_case(ops, noisy, logits_ref, demod, prev, up, k, dtype, logit_dtype=None, want=True,
+             blend="native"):
+    temporal = prev is not None
+    ldt = logit_dtype or dtype
+    n = hwc_to_planar(noisy, dtype)
+    lg = ref_logits_to_device(logits_ref, k, temporal, ldt)
+    dm = hwc_to_planar(demod, dtype) if demod is not None else None
+    pv = hwc_to_planar(prev, dtype) if prev is not None else None
+    out, tape = ops.pyramid_forward(n, lg, dm, pv, ksize=k, blend=blend)
+    g = ops.pyramid_backward(tape, hwc_to_planar(up, dtype), want_param_grads=want)
+    torch.cuda.synchronize()
+    res = {"out": planar_to_hwc(out), "g_input": planar_to_hwc(g.input)}
+    if want:
+        res["g_logits"] = device_glogits_to_ref(g.logits, logits_ref, k, temporal)
+        if g.demod is not None:
+            res["g_demod"] = planar_to_hwc(g.demod)
+    if g.prev is not None:
+        res["g_prev"] = planar_to_hwc(g.prev)
+    return res
+
+
+def compare(res, ref, rtol, levels, want):
+    assert_close(res["out"], ref["out"], rtol, "out")
+    assert_close(res["g_input"], ref["g_input"], rtol, "g_input")
+    if want:
+        for l in range(levels):
+            assert_close(res["g_logits"][l], ref["g_logits"][l], rtol, f"g_logits{l}")
+        if "g_demod" in ref:
+            assert_close(res["g_demod"], ref["g_demod"], rtol, "g_demod")
+    if "g_prev" in ref:
+        assert_close(res["g_prev"], ref["g_prev"], rtol, "g_prev")
+
+
+@pytest.mark.parametrize("name", pyramid_cases())
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_golden_cases(ops, name, precision):
+    d = load(name)
+    want = bool(d["want"])
+    dtype = torch.float64 if precision == "f64" else torch.float32
+    if precision == "f32":
+        # feed the fp32-rounded inputs to the reference arithmetic (oracle)
+        rnd = lambda a: None if a is None else a.astype(np.float32).astype(np.float64)  # noqa: E731
+        inputs = dict(noisy=rnd(d["noisy"]), demod=rnd(d.get("demod")), prev=rnd(d.get("prev")),
+                      up=rnd(d["upstream"]))
+        logits = [rnd(z) for z in case_logits(d)]
+        out, tape = op.forward(inputs["noisy"], logits, inputs["prev"], inputs["demod"])
+        g = op.backward(tape, inputs["up"], want_param_grads=want)
+        ref = {"out": out, "g_input": g.input, "g_logits": g.logits, "g_demod": g.demod,
+               "g_prev": g.prev}
+        ref = {k: v for k, v in ref.items() if v is not None}
+        rtol = 1e-5
+    else:
+        inputs = dict(noisy=d["noisy"], demod=d.get("demod"), prev=d.get("prev"), up=d["upstream"])
+        logits = case_logits(d)
+        ref = {"out": d["out"], "g_input": d["g_input"]}
+        if want:
+            ref["g_logits"] = [d[f"g_logits{l}"] for l in range(int(d["levels"]))]
+            if "g_demod" in d:
+                ref["g_demod"] = d["g_demod"]
+        if "g_prev" in d:
+            ref["g_prev"] = d["g_prev"]
+        rtol = 1e-10
+    res = run_case(ops, inputs["noisy"], logits, inputs["demod"], inputs["prev"], inputs["up"], 5,
+                   dtype, want=want)
+    compare(res, ref, rtol, int(d["levels"]), want)
+
+
+def oracle_case(h, w, L, k, seed, demod=True, prev=False, blend="native", scale=1.0):
+    rng = np.random.default_rng(seed)
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    logits = [f32(z) for z in op.random_logits(h, w, L, k, rng, temporal=prev, blend=blend,
+                                               scale=scale)]
+    noisy = f32(rng.lognormal(-1.0, 1.5, (h, w, 3)))
+    dm = f32(rng.uniform(0.05, 1.0, (h, w, 3))) if demod else None
+    pv = f32(rng.uniform(0.01, 2.0, (h, w, 3))) if prev else None
+    up = f32(rng.normal(size=(h, w, 3)))
+    out, tape = op.forward(noisy, logits, pv, dm, k=k, blend=blend)
+    g = op.backward(tape, up)
+    ref = {"out": out, "g_input": g.input, "g_logits": g.logits}
+    if dm is not None:
+        ref["g_demod"] = g.demod
+    if pv is not None:
+        ref["g_prev"] = g.prev
+    return noisy, logits, dm, pv, up, ref
+
+
+@pytest.mark.parametrize("h,w,L,k,prev,blend", [
+    (64, 80, 3, 5, False, "native"),
+    (67, 45, 4, 5, False, "native"),
+    (130, 70, 3, 7, False, "native"),
+    (41, 77, 4, 3, False, "native"),
+    (33, 29, 3, 7, True, "native"),
+    (50, 61, 3, 5, True, "native"),
+    (48, 40, 3, 5, False, "tied"),
+    (37, 52, 4, 7, False, "tied"),
+    (3, 2, 2, 7, False, "native"),
+    (1, 9, 2, 5, False, "native"),
+    (200, 1, 3, 5, True, "native"),
+    (256, 256, 4, 5, False, "native"),
+])
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_oracle_cases(ops, h, w, L, k, prev, blend, precision):
+    noisy, logits, dm, pv, up, ref = oracle_case(h, w, L, k, seed=h * 1000 + w + k, prev=prev,
+                                                 blend=blend)
+    dtype = torch.float32 if precision == "f32" else torch.float64
+    temporal = prev
+    n = hwc_to_planar(noisy, dtype)
+    lg = [hwc_to_planar(z, dtype) for z in logits]
+    d = hwc_to_planar(dm, dtype) if dm is not None else None
+    p = hwc_to_planar(pv, dtype) if pv is not None else None
+    out, tape = ops.pyramid_forward(n, lg, d, p, ksize=k, blend=blend)
+    g = ops.pyramid_backward(tape, hwc_to_planar(up, dtype))
+    rtol = 1e-5 if precision == "f32" else 1e-10
+    assert_close(planar_to_hwc(out), ref["out"], rtol, "out")
+    assert_close(planar_to_hwc(g.input), ref["g_input"], rtol, "g_input")
+    for l in range(L):
+        assert_close(planar_to_hwc(g.logits[l]), ref["g_logits"][l], rtol, f"g_logits{l}")
+    if dm is not None:
+        assert_close(planar_to_hwc(g.demod), ref["g_demod"], rtol, "g_demod")
+    if temporal:
+        assert_close(planar_to_hwc(g.prev), ref["g_prev"], rtol, "g_prev")
+
+
+@pytest.mark.parametrize("k,L", [(5, 3), (7, 4)])
+def test_bf16_logits(ops, k, L):
+    """bf16 logits, fp32 radiance and accumulation: within 2e-2 of the oracle
+    fed the bf16-rounded logits."""
+    h, w = 90, 132
+    rng = np.random.default_rng(7)
+    lg32 = [torch.from_numpy(z.astype(np.float32)) for z in
+            op.random_logits(h, w, L, k, rng, temporal=False)]
+    lgb = [z.to(torch.bfloat16) for z in lg32]
+    logits = [z.double().numpy() for z in lgb]
+    noisy = rng.lognormal(-1.0, 1.5, (h, w, 3)).astype(np.float32).astype(np.float64)
+    dm = rng.uniform(0.05, 1.0, (h, w, 3)).astype(np.float32).astype(np.float64)
+    up = rng.normal(size=(h, w, 3)).astype(np.float32).astype(np.float64)
+    out_r, tape = op.forward(noisy, logits, None, dm, k=k)
+    g_r = op.backward(tape, up)
+    dev_lg = [hwc_to_planar(z.numpy(), torch.bfloat16) for z in lgb]
+    out, t = ops.pyramid_forward(hwc_to_planar(noisy, torch.float32), dev_lg,
+                                 hwc_to_planar(dm, torch.float32), ksize=k)
+    g = ops.pyramid_backward(t, hwc_to_planar(up, torch.float32))
+    assert g.logits[0].dtype == torch.bfloat16
+    assert_close(planar_to_hwc(out), out_r, 2e-2)
+    assert_close(planar_to_hwc(g.input), g_r.input, 2e-2)
+    assert_close(planar_to_hwc(g.demod), g_r.demod, 2e-2)
+    for l in range(L):
+        assert_close(planar_to_hwc(g.logits[l]), g_r.logits[l], 2e-2)
+
+
+def test_many_channels_batched_draws(ops):
+    """C = 3K channels share one weight set (the batched-draws convention,
+    ref optimize.py:433-437): parity incl. g_logits summed over all channels."""
+    rng = np.random.default_rng(3)
+    h, w, L, k, K = 40, 36, 3, 5, 5
+    logits = op.random_logits(h, w, L, k, rng, temporal=False)
+    noisy = rng.uniform(0.01, 2, (h, w, 3 * K))
+    dm = np.tile(rng.uniform(0.1, 1, (h, w, 3)), (1, 1, K))
+    up = rng.normal(size=(h, w, 3 * K))
+    out_r, tape = op.forward(noisy, logits, None, dm, k=k)
+    g_r = op.backward(tape, up)
+    out, t = ops.pyramid_forward(hwc_to_planar(noisy), [hwc_to_planar(z) for z in logits],
+                                 hwc_to_planar(dm), ksize=k)
+    g = ops.pyramid_backward(t, hwc_to_planar(up))
+    assert_close(planar_to_hwc(out), out_r, 1e-10)
+    assert_close(planar_to_hwc(g.input), g_r.input, 1e-10)
+    assert_close(planar_to_hwc(g.demod), g_r.demod, 1e-10)
+    for l in range(L):
+        assert_close(planar_to_hwc(g.logits[l]), g_r.logits[l], 1e-10)
+
+
+def test_batch_equals_single_frames_bitwise(ops):
+    rng = np.random.default_rng(11)
+    B, h, w, L, k = 3, 70, 90, 3, 5
+    dev = "cuda"
+    noisy = torch.rand(B, 3, h, w, device=dev) + 0.01
+    dm = torch.rand(B, 3, h, w, device=dev) * 0.9 + 0.05
+    lg = [torch.randn(B, ops.logit_channels(l, L, k), hh, ww, device=dev)
+          for l, (hh, ww) in enumerate(ops.level_shapes(h, w, L))]
+    up = torch.randn(B, 3, h, w, device=dev)
+    out, t = ops.pyramid_forward(noisy, lg, dm, ksize=k)
+    g = ops.pyramid_backward(t, up)
+    for b in range(B):
+        o1, t1 = ops.pyramid_forward(noisy[b:b + 1].contiguous(), [z[b:b + 1].contiguous() for z in lg],
+                                     dm[b:b + 1].contiguous(), ksize=k)
+        g1 = ops.pyramid_backward(t1, up[b:b + 1].contiguous())
+        assert torch.equal(o1[0], out[b])
+        assert torch.equal(g1.input[0], g.input[b])
+        assert torch.equal(g1.demod[0], g.demod[b])
+        for l in range(L):
+            assert torch.equal(g1.logits[l][0], g.logits[l][b])
+    del rng
+
+
+@pytest.mark.parametrize("h,w,L,k,ldt", [(1080, 1920, 3, 5, torch.float32),
+                                         (2160, 3840, 4, 7, torch.bfloat16)])
+def test_full_size_properties(ops, h, w, L, k, ldt):
+    """Size-independent checks at the BASELINE sizes: adjointness
+    <up, out> = <g_noisy, noisy> (out is linear in noisy for fixed logits),
+    per-pixel sum of logit gradients = 0 (softmax), constant-input
+    preservation, and run-to-run determinism."""
+    torch.manual_seed(0)
+    dev = "cuda"
+    noisy = torch.rand(1, 3, h, w, device=dev) * 2
+    dm = torch.rand(1, 3, h, w, device=dev) * 0.95 + 0.05
+    lg = [torch.randn(1, ops.logit_channels(l, L, k), hh, ww, device=dev).to(ldt)
+          for l, (hh, ww) in enumerate(ops.level_shapes(h, w, L))]
+    up = torch.randn(1, 3, h, w, device=dev)
+    out, t = ops.pyramid_forward(noisy, lg, dm, ksize=k)
+    g = ops.pyramid_backward(t, up)
+    lhs = (up.double() * out.double()).sum().item()
+    rhs = (g.input.double() * noisy.double()).sum().item()
+    assert abs(lhs - rhs) <= 1e-4 * abs(lhs)
+    for l in range(L):
+        s = g.logits[l].float().sum(dim=1)
+        scale = g.logits[l].float().abs().amax(dim=1) + 1e-30
+        tol = 1e-4 if ldt == torch.float32 else 5e-2
+        assert (s.abs() / scale).max().item() < tol
+    out2, t2 = ops.pyramid_forward(noisy, lg, dm, ksize=k)
+    g2 = ops.pyramid_backward(t2, up)
+    assert torch.equal(out, out2) and torch.equal(g.input, g2.input)
+    assert all(torch.equal(a, b) for a, b in zip(g.logits, g2.logits))
+    c = torch.full_like(noisy, 0.7)
+    oc, _ = ops.pyramid_forward(c, lg, None, ksize=k)
+    assert (oc - 0.7).abs().max().item() < 1e-5
+
+
+def test_autograd_function(ops):
+    rng = np.random.default_rng(5)
+    h, w, L, k = 24, 30, 3, 5
+    noisy, logits, dm, _, up, ref = oracle_case(h, w, L, k, seed=5)
+    n = hwc_to_planar(noisy).requires_grad_()
+    d = hwc_to_planar(dm).requires_grad_()
+    lg = [hwc_to_planar(z).requires_grad_() for z in logits]
+    out = ops.pyramid_filter(n, lg, d, ksize=k)
+    (out * hwc_to_planar(up)).sum().backward()
+    assert_close(planar_to_hwc(n.grad), ref["g_input"], 1e-10)
+    assert_close(planar_to_hwc(d.grad), ref["g_demod"], 1e-10)
+    for l in range(L):
+        assert_close(planar_to_hwc(lg[l].grad), ref["g_logits"][l], 1e-10)
+    del rng
+
+
+def test_primitives_match_reference(ops):
+    d = load("primitives")
+    img = hwc_to_planar(d["gather_img"])
+    wts = hwc_to_planar(d["gather_w"])
+    np.testing.assert_allclose(planar_to_hwc(ops.gather(img, wts, 5)), d["gather_out"], rtol=1e-13)
+    up = ops.upsample2(hwc_to_planar(d["up_coarse"]), hwc_to_planar(d["up_w"]))
+    np.testing.assert_allclose(planar_to_hwc(up), d["up_out"], rtol=1e-13)
+    lv = ops.build_pyramid(hwc_to_planar(d["pyr_in"]), 5)
+    for l in range(5):
+        np.testing.assert_allclose(planar_to_hwc(lv[l]), d[f"pyr_level{l}"], rtol=1e-13)
+    z = hwc_to_planar(d["nk_logits0"])
+    np.testing.assert_allclose(planar_to_hwc(ops.softmax_channels(z)), d["nk_wt0"], rtol=1e-13)
+    np.testing.assert_allclose(planar_to_hwc(ops.softmax_channels(z, active=29)), d["nk_wf0"],
+                               rtol=1e-13, atol=0)
