@@ -1,0 +1,598 @@
+"""Benchmark of the B200 hot path: gather-pyramid filter fwd+bwd (BASELINE metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4a|c3|c2|c1] [--no-e2e] [--no-cpu] [--no-also]
+
+Default workload (BASELINE.json configs[4a], the metric's 1080p multi-GPU
+config): 64 frames of 1920x1080, 3-level 5x5 pyramid, fp32, forward + backward
+with parameter gradients, sharded by frame over N GPUs (64/N frames per GPU;
+strong scaling, no collective on the data path).  Inputs are synthetic with the
+BASELINE distributions (seeded): noisy radiance from the fused placement op at
+0.25 spp over a log-normal bank with 1% x100 fireflies, albedo demodulation
+U[0.05,1], N(0,1) logits and upstream gradient.  The working set (~50 GB at
+N=1) is far larger than the 126 MB L2, so no explicit flush is needed.
+
+One JSON line (rank 0).  `value` = device-timed Mpix/s over all ranks (max over
+ranks of the CUDA-event time).  `roofline` = the dominant kernel (level-0
+backward) timed live with CUDA events on its own stream; `step_roofline` =
+SURVEY.md 8(d)'s fwd+bwd algorithmic bytes per step over the step time.
+`e2e` = same metric through the host-buffer path (pinned H2D of every input,
+D2H of every result, copies inside the timed region).  `cpu_baseline` /
+`--impl reference` = the reference algorithm (oracle port, numpy float64) on
+the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (frames_total, H, W, L, k, logit dtype, description)
+    "c4a": (64, 1080, 1920, 3, 5, "f32",
+            "c4a: 64 x 1920x1080 frames, 3-level 5x5 pyramid, fp32 logits+radiance, fwd+bwd "
+            "(logit, radiance and demod grads), sharded by frame"),
+    "c3": (1, 2160, 3840, 4, 7, "bf16",
+           "c3: 1 x 3840x2160, 4-level 7x7 pyramid, bf16 logits, fp32 radiance/accumulate, fwd+bwd"),
+    "c2": (64, 256, 256, 4, 5, "f32",
+           "c2: 64 x 256x256 crops, 4-level 5x5 pyramid, fp32, fwd+bwd"),
+}
+CPU_SAMPLE = (540, 960, 3, 5)  # per-worker sample of the c4a workload (H, W, L, k)
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+
+
+def level_shapes(h, w, L):
+    s = [(h, w)]
+    while len(s) < L:
+        s.append(((s[-1][0] + 1) // 2, (s[-1][1] + 1) // 2))
+    return s
+
+
+def logit_channels(l, L, k):
+    return k * k + (4 if l < L - 1 else 0)
+
+
+def algorithmic_bytes(h, w, L, k, sl, sg, channels=3):
+    """(FWD, BWD, dominant-kernel) bytes per frame.  FWD/BWD follow 8(d):
+    each pass reads its inputs and writes its outputs once, intermediates
+    excluded.  Dominant kernel = level-0 backward: logits0 read, g_logits0
+    write, upstream/noisy/demod/out read, g_noisy/g_demod written."""
+    img = 4 * channels
+    dims = level_shapes(h, w, L)
+    n0 = h * w
+    lg = sum(a * b * logit_channels(l, L, k) for l, (a, b) in enumerate(dims))
+    fwd = n0 * 3 * img + lg * sl
+    bwd = n0 * 6 * img + lg * (sl + sg)
+    dom = n0 * (logit_channels(0, L, k) * (sl + sg) + 6 * img)
+    return fwd, bwd, dom
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the reference algorithm (oracle port, float64) on host cores
+
+
+def _cpu_worker(seed):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+
+    from oracle import pyramid as op
+    h, w, L, k = CPU_SAMPLE
+    rng = np.random.default_rng(seed)
+    logits = op.random_logits(h, w, L, k, rng, temporal=True)
+    noisy = rng.lognormal(-1.0, 1.5, (h, w, 3)) * (rng.uniform(size=(h, w, 1)) < 0.25)
+    demod = rng.uniform(0.05, 1.0, (h, w, 3))
+    up = rng.normal(size=(h, w, 3))
+    t0 = time.perf_counter()
+    out, tape = op.forward(noisy, logits, None, demod, k=k)
+    op.backward(tape, up)
+    return time.perf_counter() - t0
+
+
+def cpu_pool_size():
+    cores = len(os.sched_getaffinity(0))
+    try:
+        import psutil
+        ram = psutil.virtual_memory().available
+    except Exception:
+        ram = 8 << 30
+    per_proc = 2.2 * (1 << 30)  # measured ~1.7 GB RSS for one 960x540 L3 fwd+bwd
+    return max(1, min(cores, int(ram // per_proc)))
+
+
+class CpuPool:
+    def __init__(self, procs):
+        self.procs = procs
+        ctx = mp.get_context("spawn")
+        env_threads = os.environ.get("OMP_NUM_THREADS")
+        os.environ["OMP_NUM_THREADS"] = "1"
+        self.pool = ctx.Pool(procs)
+        if env_threads is None:
+            os.environ.pop("OMP_NUM_THREADS", None)
+        else:
+            os.environ["OMP_NUM_THREADS"] = env_threads
+
+    def step(self, seed):
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_worker, [seed * 1000 + i for i in range(self.procs)])
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample_desc(procs):
+    h, w, L, k = CPU_SAMPLE
+    return (f"{procs} worker processes x one {w}x{h} L{L} k{k} fwd+bwd (float64 numpy oracle "
+            f"port of the reference, OMP_NUM_THREADS=1 each) per step; CPU {cpu_model()}")
+
+
+def run_cpu(steps, warmup):
+    procs = cpu_pool_size()
+    pool = CpuPool(procs)
+    try:
+        for i in range(warmup):
+            pool.step(100 + i)
+        times = [pool.step(i) for i in range(steps)]
+    finally:
+        pool.close()
+    h, w, _, _ = CPU_SAMPLE
+    t = sum(times) / len(times)
+    return {"value": procs * h * w / t / 1e6, "procs": procs, "sec_per_step": t}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def synthetic_inputs(B, H, W, L, k, ldt, device, seed):
+    """BASELINE distributions: density softplus(GRF sigma=8) standardised,
+    0.25 spp placement over a log-normal(-1, 1.5) bank with 1% x100
+    fireflies (fused placement op), albedo U[0.05,1], N(0,1) logits."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2602_08642_b200 import ops
+    g = torch.Generator(device=device).manual_seed(seed)
+    noisy = torch.empty(B, 3, H, W, device=device)
+    sig = 8.0
+    r = int(3 * sig)
+    xs = torch.arange(-r, r + 1, device=device, dtype=torch.float32)
+    ker = torch.exp(-xs ** 2 / (2 * sig * sig))
+    ker = ker / ker.sum()
+    S = 2
+    for b in range(B):
+        z = torch.randn(1, 1, H, W, generator=g, device=device)
+        z = F.conv2d(F.pad(z, (r, r, 0, 0), mode="circular"), ker.view(1, 1, 1, -1))
+        z = F.conv2d(F.pad(z, (0, 0, r, r), mode="circular"), ker.view(1, 1, -1, 1))
+        z = (z - z.mean()) / z.std()
+        scores = torch.log(F.softplus(z))[0].contiguous()
+        bank = torch.exp(-1.0 + 1.5 * torch.randn(1, S, 3, H, W, generator=g, device=device))
+        fire = torch.rand(1, S, 1, H, W, generator=g, device=device) < 0.01
+        bank = torch.where(fire, bank * 100.0, bank).contiguous()
+        ops.place_fused(scores, bank, 0.25, seed=seed, frame0=b, noisy=noisy[b:b + 1])
+        del z, scores, bank, fire
+    demod = torch.rand(B, 3, H, W, generator=g, device=device) * 0.95 + 0.05
+    ltype = {"f32": torch.float32, "bf16": torch.bfloat16}[ldt]
+    logits = [torch.randn(B, logit_channels(l, L, k), h, w, generator=g, device=device).to(ltype)
+              for l, (h, w) in enumerate(level_shapes(H, W, L))]
+    up = torch.randn(B, 3, H, W, generator=g, device=device)
+    return noisy, demod, logits, up
+
+
+class Runner:
+    """Pre-allocated fwd+bwd through the C ABI (no per-step allocation)."""
+
+    def __init__(self, noisy, demod, logits, up, k):
+        import torch
+
+        from paper_2602_08642_b200 import _lib, ops
+        self.lib = _lib.load()
+        self.check = _lib.check
+        self.noisy, self.demod, self.logits, self.up = noisy, demod, logits, up
+        self.desc = ops._desc(noisy, logits, demod, None, k, "native")
+        tb, wb = C.c_size_t(), C.c_size_t()
+        self.check(self.lib.ssb_pyr_tape_bytes(C.byref(self.desc), C.byref(tb)), "tape")
+        self.check(self.lib.ssb_pyr_workspace_bytes(C.byref(self.desc), C.byref(wb)), "ws")
+        dev = noisy.device
+        self.tape = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=dev)
+        self.ws = torch.empty(max(wb.value, 1), dtype=torch.uint8, device=dev)
+        self.out = torch.empty_like(noisy)
+        self.g_noisy = torch.empty_like(noisy)
+        self.g_demod = torch.empty_like(noisy)
+        self.g_logits = [torch.empty_like(z) for z in logits]
+        self.fio = _lib.PyrFwdIO()
+        self.fio.noisy, self.fio.demod, self.fio.out = noisy.data_ptr(), demod.data_ptr(), self.out.data_ptr()
+        self.bio = _lib.PyrBwdIO()
+        self.bio.noisy, self.bio.demod = noisy.data_ptr(), demod.data_ptr()
+        self.bio.out, self.bio.upstream = self.out.data_ptr(), up.data_ptr()
+        self.bio.g_noisy, self.bio.g_demod = self.g_noisy.data_ptr(), self.g_demod.data_ptr()
+        for l, (z, gz) in enumerate(zip(logits, self.g_logits)):
+            self.fio.logits[l] = z.data_ptr()
+            self.bio.logits[l] = z.data_ptr()
+            self.bio.g_logits[l] = gz.data_ptr()
+        self.tape_p = C.c_void_p(self.tape.data_ptr())
+        self.ws_p = C.c_void_p(self.ws.data_ptr())
+
+    def step(self, stream):
+        s = C.c_void_p(stream)
+        rc = self.lib.ssb_pyr_forward(C.byref(self.desc), C.byref(self.fio), self.tape_p, s)
+        if rc:
+            self.check(rc, "ssb_pyr_forward")
+        rc = self.lib.ssb_pyr_backward(C.byref(self.desc), C.byref(self.bio), self.tape_p, self.ws_p, s)
+        if rc:
+            self.check(rc, "ssb_pyr_backward")
+
+
+def launches_per_step(L):
+    # forward: (L-1) pooling + L level kernels; backward: L level kernels + final sweep
+    names = [f"pool{l}->{l + 1}" for l in range(L - 1)]
+    names += [f"fwd_l{l}" for l in range(L - 1, -1, -1)]
+    names += [f"bwd_l{l}" for l in range(L)] + ["bwd_final"]
+    return names
+
+
+def time_device(runner, steps, warmup, L, dist, world):
+    import torch
+    lib = runner.lib
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    for _ in range(warmup):
+        runner.step(sp)
+    torch.cuda.synchronize()
+    names = launches_per_step(L)
+    per = len(names)
+    cap = per * steps
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * cap)]
+    ev_arr = (C.c_void_p * (2 * cap))(*[e.cuda_event for e in evs])
+    count = C.c_int(0)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = lib.ssb_launch_count()
+    lib.ssb_set_launch_events(ev_arr, cap, C.byref(count))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        runner.step(sp)
+    t1.record(stream)
+    lib.ssb_set_launch_events(None, 0, None)
+    torch.cuda.synchronize()
+    launches = lib.ssb_launch_count() - n0
+    ms = t0.elapsed_time(t1)
+    if dist:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+        dist.barrier()
+    durs = {nm: [] for nm in names}
+    for i in range(count.value):
+        durs[names[i % per]].append(evs[2 * i].elapsed_time(evs[2 * i + 1]))
+    mean = {nm: (sum(v) / len(v) if v else None) for nm, v in durs.items()}
+    return ms / steps, mean, launches
+
+
+def time_e2e(dev, frames, steps, k, H, W, L, ldt, chunk=4, pool_frames=16):
+    """Host-buffer path: per frame chunk, H2D of noisy/demod/logits/upstream
+    from pinned memory, fwd+bwd, D2H of out/g_logits/g_noisy/g_demod.  Copies
+    run on their own streams and overlap compute of the neighbouring chunk."""
+    import torch
+
+    chunk = max(1, min(chunk, frames))
+    pool_frames = max(chunk, min(pool_frames, frames))
+    pool_frames -= pool_frames % chunk
+    lt = torch.float32 if ldt == "f32" else torch.bfloat16
+    lvl = level_shapes(H, W, L)
+
+    def host(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+    h_in = {"noisy": host((pool_frames, 3, H, W), torch.float32),
+            "demod": host((pool_frames, 3, H, W), torch.float32),
+            "up": host((pool_frames, 3, H, W), torch.float32)}
+    h_lg = [host((pool_frames, logit_channels(l, L, k), h, w), lt) for l, (h, w) in enumerate(lvl)]
+    h_out = {n: host((pool_frames, 3, H, W), torch.float32) for n in ("out", "g_noisy", "g_demod")}
+    h_glg = [host((pool_frames, logit_channels(l, L, k), h, w), lt) for l, (h, w) in enumerate(lvl)]
+    for t in list(h_in.values()) + h_lg:
+        t.uniform_(0.05, 1.0)
+    # two device chunk buffers (double buffering)
+    bufs = []
+    for _ in range(2):
+        d_n = torch.empty(chunk, 3, H, W, device=dev)
+        d_d = torch.empty_like(d_n)
+        d_u = torch.empty_like(d_n)
+        d_lg = [torch.empty(chunk, logit_channels(l, L, k), h, w, device=dev, dtype=lt)
+                for l, (h, w) in enumerate(lvl)]
+        r = Runner(d_n, d_d, d_lg, d_u, k)
+        bufs.append(r)
+    s_h2d, s_comp, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    in_bytes = sum(t[0:1].numel() * t.element_size() for t in list(h_in.values()) + h_lg) * frames
+    out_bytes = sum(t[0:1].numel() * t.element_size() for t in list(h_out.values()) + h_glg) * frames
+
+    def one_step():
+        ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        ev_comp = [torch.cuda.Event() for _ in range(2)]
+        ev_d2h = [None, None]
+        for ci, f0 in enumerate(range(0, frames, chunk)):
+            r = bufs[ci % 2]
+            p0 = f0 % pool_frames
+            sl = slice(p0, p0 + chunk)
+            with torch.cuda.stream(s_h2d):
+                if ev_d2h[ci % 2] is not None:
+                    s_h2d.wait_event(ev_d2h[ci % 2])
+                r.noisy.copy_(h_in["noisy"][sl], non_blocking=True)
+                r.demod.copy_(h_in["demod"][sl], non_blocking=True)
+                r.up.copy_(h_in["up"][sl], non_blocking=True)
+                for z, hz in zip(r.logits, h_lg):
+                    z.copy_(hz[sl], non_blocking=True)
+                ev_h2d[ci % 2].record(s_h2d)
+            s_comp.wait_event(ev_h2d[ci % 2])
+            r.step(s_comp.cuda_stream)
+            ev_comp[ci % 2].record(s_comp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_comp[ci % 2])
+                h_out["out"][sl].copy_(r.out, non_blocking=True)
+                h_out["g_noisy"][sl].copy_(r.g_noisy, non_blocking=True)
+                h_out["g_demod"][sl].copy_(r.g_demod, non_blocking=True)
+                for hz, gz in zip(h_glg, r.g_logits):
+                    hz[sl].copy_(gz, non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_d2h)
+                ev_d2h[ci % 2] = e
+        torch.cuda.synchronize()
+
+    one_step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    dt = (time.perf_counter() - t0) / steps
+    return dt, in_bytes, out_bytes
+
+
+def gpu_arm(args, rank, world, local_rank, dist):
+    import torch
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    frames_total, H, W, L, k, ldt, desc = WORKLOADS[args.workload]
+    if frames_total % world and frames_total > 1:
+        raise SystemExit(f"{frames_total} frames do not split over {world} GPUs")
+    B = max(1, frames_total // world)
+    noisy, demod, logits, up = synthetic_inputs(B, H, W, L, k, ldt, dev, seed=1234 + rank)
+    runner = Runner(noisy, demod, logits, up, k)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    ms, kern, launches = time_device(runner, args.steps, args.warmup, L, dist, world)
+    clocks = sampler.stop()
+    sl = 2 if ldt == "bf16" else 4
+    fwd_b, bwd_b, dom_b = algorithmic_bytes(H, W, L, k, sl, sl)
+    px_total = B * world * H * W
+    value = px_total / (ms * 1e-3) / 1e6
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    dom_ms = kern.get("bwd_l0")
+    dom_gbs = dom_b * B / (dom_ms * 1e-3) / 1e9 if dom_ms else None
+    step_gbs = (fwd_b + bwd_b) * B / (ms * 1e-3) / 1e9
+    res = {
+        "metric": f"pyramidal filter fwd+bwd throughput ({args.workload})",
+        "value": round(value, 3),
+        "unit": "Mpix/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong" if frames_total > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if ldt == "f32" else "f32 (bf16 logits)",
+        "data": "synthetic, BASELINE config distributions (seeded); no dataset",
+        "config": {"workload": desc, "frames_total": frames_total * (1 if frames_total > 1 else world),
+                   "frames_per_gpu": B, "height": H, "width": W, "levels": L, "ksize": k,
+                   "logit_dtype": ldt, "parallelism": f"frame-sharded x{world}, no collective",
+                   "l2": "working set >> 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "kernel": "bwd_l0 (level-0 backward: softmax recompute, "
+                     "logit grads, gather-transpose, upsample-transpose)",
+                     "achieved": round(dom_gbs, 1) if dom_gbs else None, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(dom_gbs / peak, 4) if dom_gbs else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": dom_b * B,
+                     "ms_per_launch": round(dom_ms, 4) if dom_ms else None,
+                     "share_of_step": round(dom_ms / ms, 3) if dom_ms else None},
+        "step_roofline": {"achieved": round(step_gbs, 1), "peak": peak, "unit": "GB/s",
+                          "frac": round(step_gbs / peak, 4),
+                          "bytes_per_frame": {"fwd": fwd_b, "bwd": bwd_b}},
+        "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    return res, runner
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4a")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-also", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        frames_total, H, W, L, k, ldt, desc = WORKLOADS[args.workload]
+        # the reference CPU path is float64 numpy; bounded samples per step
+        steps = args.steps
+        warm = min(args.warmup, 1)
+        r = run_cpu(steps, warm)
+        h, w, _, _ = CPU_SAMPLE
+        res = {"impl": "reference", "metric": f"pyramidal filter fwd+bwd throughput ({args.workload})",
+               "value": round(r["value"], 4), "unit": "Mpix/s", "n_gpus": world, "steps": steps,
+               "warmup": warm, "ms_per_step": round(r["sec_per_step"] * 1e3, 1),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic, BASELINE config distributions (seeded)",
+               "config": {"workload": desc, "sample": cpu_sample_desc(r["procs"])},
+               "cpu_baseline": {"value": round(r["value"], 4), "unit": "Mpix/s",
+                                "cores": r["procs"], "kind": "port",
+                                "sample": cpu_sample_desc(r["procs"])},
+               "e2e": {"value": round(r["value"], 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(res), flush=True)
+        return
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        tdist.init_process_group("nccl")
+        dist = tdist
+    res, runner = gpu_arm(args, rank, world, local_rank, dist)
+    frames_total, H, W, L, k, ldt, _ = WORKLOADS[args.workload]
+
+    # e2e through the host-buffer path
+    if not args.no_e2e:
+        B = max(1, frames_total // world)
+        del runner
+        import torch
+        torch.cuda.empty_cache()
+        dt, ib, ob = time_e2e(torch.device("cuda", local_rank), B, max(1, min(args.steps, 3)),
+                              k, H, W, L, ldt)
+        if dist:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = tt.item()
+        res["e2e"] = {"value": round(B * world * H * W / dt / 1e6, 3), "unit": "Mpix/s",
+                      "h2d_bytes_per_step": ib * world, "d2h_bytes_per_step": ob * world,
+                      "path": "ops C-ABI from pinned host buffers, chunked H2D/compute/D2H overlap"}
+    else:
+        res["e2e"] = None
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = run_cpu(1, 0)
+        res["cpu_baseline"] = {"value": round(r["value"], 4), "unit": "Mpix/s", "cores": r["procs"],
+                               "kind": "port", "sample": cpu_sample_desc(r["procs"])}
+    if rank == 0 and world == 1 and not args.no_also and args.workload == "c4a":
+        res["also"] = also_measurements()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def also_measurements():
+    """Second BASELINE config on the same box: c3 (4K, L4, k7, bf16 logits)."""
+    import torch
+    out = {}
+    frames, H, W, L, k, ldt, desc = WORKLOADS["c3"]
+    noisy, demod, logits, up = synthetic_inputs(1, H, W, L, k, ldt, torch.device("cuda"), seed=99)
+    r = Runner(noisy, demod, logits, up, k)
+    ms, kern, _ = time_device(r, 20, 3, L, None, 1)
+    fwd_b, bwd_b, dom_b = algorithmic_bytes(H, W, L, k, 2, 2)
+    peak = 6556.8
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    out["c3"] = {"workload": desc, "mpix_s": round(H * W / (ms * 1e-3) / 1e6, 2),
+                 "ms_per_step": round(ms, 4),
+                 "step_frac_of_hbm": round((fwd_b + bwd_b) / (ms * 1e-3) / 1e9 / peak, 4),
+                 "bwd_l0_frac_of_hbm": round(dom_b / (kern["bwd_l0"] * 1e-3) / 1e9 / peak, 4),
+                 "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
+    return out
+
+
+if __name__ == "__main__":
+    main()

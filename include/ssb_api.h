@@ -42,6 +42,15 @@ enum { SSB_BLEND_NATIVE = 0, SSB_BLEND_TIED = 1 };
 int ssb_version(void);
 const char* ssb_last_error(void);
 
+/* Measurement hooks (bench/profiling only; not needed for computation).
+ * ssb_launch_count: kernels launched by this process so far.
+ * ssb_set_launch_events: while `events` is non-NULL, the i-th kernel this
+ * thread launches is bracketed by cudaEventRecord(events[2i]) and
+ * cudaEventRecord(events[2i+1]) on its stream, for i < capacity; *count
+ * receives the number bracketed.  Pass NULL to disable. */
+unsigned long long ssb_launch_count(void);
+int ssb_set_launch_events(void* const* events, int capacity, int* count);
+
 /* ------------------------------------------------------------------------
  * (c) gather pyramid filter -- replaces pyramid.py `reconstruct_core`
  * (:292-345), `reconstruct` (:348-359) and `reconstruct_backward` (:362-449),

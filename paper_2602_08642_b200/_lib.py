@@ -21,7 +21,7 @@ VARIANTS = {"stochastic": 0, "relaxed": 1, "straight-through": 2, "gumbel": 3}
 
 # every symbol include/ssb_api.h declares (tests check the .so exports them all)
 EXPORTS = (
-    "ssb_version", "ssb_last_error",
+    "ssb_version", "ssb_last_error", "ssb_launch_count", "ssb_set_launch_events",
     "ssb_pyr_logit_channels", "ssb_pyr_level_dims", "ssb_pyr_tape_bytes",
     "ssb_pyr_workspace_bytes", "ssb_pyr_forward", "ssb_pyr_backward",
     "ssb_softmax_channels", "ssb_gather", "ssb_upsample2", "ssb_avgpool2",
@@ -99,6 +99,8 @@ def load(build_if_missing: bool = False):
         sigs = {
             "ssb_version": (C.c_int, []),
             "ssb_last_error": (C.c_char_p, []),
+            "ssb_launch_count": (C.c_ulonglong, []),
+            "ssb_set_launch_events": (C.c_int, [vp, C.c_int, P(C.c_int)]),
             "ssb_pyr_logit_channels": (C.c_int, [P(PyrDesc), C.c_int]),
             "ssb_pyr_level_dims": (C.c_int, [P(PyrDesc), C.c_int, P(C.c_int32), P(C.c_int32)]),
             "ssb_pyr_tape_bytes": (C.c_int, [P(PyrDesc), P(C.c_size_t)]),

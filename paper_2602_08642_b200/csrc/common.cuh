@@ -52,4 +52,17 @@ __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
 template <typename T>
 __device__ __forceinline__ T demod_clamp(T d) { return d > (T)kDemodFloor ? d : (T)kDemodFloor; }
 
+// launch accounting (pyr_api.cu): every kernel launch is wrapped in
+// SSB_LAUNCH(stream, kernel<<<...>>>(...)) so the bench can count launches and
+// time individual kernels with CUDA events on their own stream.
+void launch_begin(cudaStream_t s);
+void launch_end(cudaStream_t s);
+
 }  // namespace ssb
+
+#define SSB_LAUNCH(stream, ...)          \
+    do {                                 \
+        ::ssb::launch_begin(stream);     \
+        __VA_ARGS__;                     \
+        ::ssb::launch_end(stream);       \
+    } while (0)

@@ -316,8 +316,8 @@ template <typename TS>
 static void launch_reductions(int B, long long n, const TS* scores, double* pmax, double* psum,
                               cudaStream_t s) {
     dim3 grid(kRedBlocks, B);
-    k_partial_max<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax);
-    k_partial_sum<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax, psum);
+    SSB_LAUNCH(s, k_partial_max<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax));
+    SSB_LAUNCH(s, k_partial_sum<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax, psum));
 }
 
 }  // namespace ssb
@@ -333,7 +333,7 @@ int ssb_uniform_grid(uint64_t seed, int64_t frame0, const int64_t* frames, int B
         return SSB_EINVAL;
     }
     dim3 block(32, 8), grid((W + 31) / 32, (H + 7) / 8, B);
-    k_uniform_grid<<<grid, block, 0, (cudaStream_t)stream>>>(seed, frame0, frames, H, W, stream_id, u);
+    SSB_LAUNCH((cudaStream_t)stream, k_uniform_grid<<<grid, block, 0, (cudaStream_t)stream>>>(seed, frame0, frames, H, W, stream_id, u));
     return cuda_check("ssb_uniform_grid");
 }
 
@@ -361,7 +361,7 @@ int ssb_normalize_density(int B, int H, int W, const double* scores, double budg
     double* psum = pmax + (size_t)B * kRedBlocks;
     cudaStream_t s = (cudaStream_t)stream;
     launch_reductions<double>(B, n, scores, pmax, psum, s);
-    k_density_apply<<<dim3(kRedBlocks, B), kRedThreads, 0, s>>>(n, scores, pmax, psum, budget, spp);
+    SSB_LAUNCH(s, k_density_apply<<<dim3(kRedBlocks, B), kRedThreads, 0, s>>>(n, scores, pmax, psum, budget, spp));
     return cuda_check("ssb_normalize_density");
 }
 
@@ -380,7 +380,7 @@ int ssb_allocate(const ssb_alloc_desc* d, const double* spp, const int64_t* rank
         return SSB_EINVAL;
     }
     dim3 block(32, 8), grid((d->W + 31) / 32, (d->H + 7) / 8, d->B);
-    k_allocate<<<grid, block, 0, (cudaStream_t)stream>>>(*d, spp, rank, base, frac, u, taken);
+    SSB_LAUNCH((cudaStream_t)stream, k_allocate<<<grid, block, 0, (cudaStream_t)stream>>>(*d, spp, rank, base, frac, u, taken));
     return cuda_check("ssb_allocate");
 }
 
@@ -407,8 +407,8 @@ int ssb_stochastic_core(const ssb_estimate_desc* d, const double* spp, const dou
         return SSB_EINVAL;
     }
     const long long n = (long long)d->B * d->H * d->W;
-    k_stochastic_core<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        *d, n, spp, frac, u, base_sum, holdout, noisy, grad, contrib, drawn);
+    SSB_LAUNCH((cudaStream_t)stream, k_stochastic_core<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        *d, n, spp, frac, u, base_sum, holdout, noisy, grad, contrib, drawn));
     return cuda_check("ssb_stochastic_core");
 }
 
@@ -423,8 +423,8 @@ int ssb_estimate(const ssb_estimate_desc* d, const double* spp, const int64_t* b
         return SSB_EINVAL;
     }
     const long long n = (long long)d->B * d->H * d->W;
-    k_estimate<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        *d, d->H, d->W, spp, base, frac, u, samples, noisy, grad, contrib, used, noisy32);
+    SSB_LAUNCH((cudaStream_t)stream, k_estimate<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        *d, d->H, d->W, spp, base, frac, u, samples, noisy, grad, contrib, used, noisy32));
     return cuda_check("ssb_estimate");
 }
 
@@ -449,7 +449,7 @@ int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* b
     cudaStream_t s = (cudaStream_t)stream;
     launch_reductions<float>(d->B, n, scores, pmax, psum, s);
     dim3 block(32, 8), grid((d->W + 31) / 32, (d->H + 7) / 8, d->B);
-    k_place_fused<<<grid, block, 0, s>>>(*d, scores, pmax, psum, bank, noisy, spp_out, taken_out);
+    SSB_LAUNCH(s, k_place_fused<<<grid, block, 0, s>>>(*d, scores, pmax, psum, bank, noisy, spp_out, taken_out));
     return cuda_check("ssb_place_fused");
 }
 

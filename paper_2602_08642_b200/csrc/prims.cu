@@ -71,7 +71,7 @@ template <typename T>
 static int prim_softmax(int B, int C, int H, int W, int active, const void* in, void* out,
                         cudaStream_t s) {
     dim3 block(32, 8), grid((W + 31) / 32, (H + 7) / 8, B);
-    k_softmax_channels<T><<<grid, block, 0, s>>>(C, H, W, active, (const T*)in, (T*)out);
+    SSB_LAUNCH(s, k_softmax_channels<T><<<grid, block, 0, s>>>(C, H, W, active, (const T*)in, (T*)out));
     return cuda_check("ssb_softmax_channels");
 }
 
@@ -117,11 +117,11 @@ int ssb_gather(int dtype, int B, int C, int H, int W, int ksize, const void* ima
     dim3 block(32, 8), grid((W + 31) / 32, (H + 7) / 8, B);
     cudaStream_t s = (cudaStream_t)stream;
     if (dtype == SSB_F32)
-        k_gather<float><<<grid, block, 0, s>>>(C, H, W, ksize, (const float*)image,
-                                               (const float*)weights, (float*)out);
+        SSB_LAUNCH(s, k_gather<float><<<grid, block, 0, s>>>(C, H, W, ksize, (const float*)image,
+                                               (const float*)weights, (float*)out));
     else
-        k_gather<double><<<grid, block, 0, s>>>(C, H, W, ksize, (const double*)image,
-                                                (const double*)weights, (double*)out);
+        SSB_LAUNCH(s, k_gather<double><<<grid, block, 0, s>>>(C, H, W, ksize, (const double*)image,
+                                                (const double*)weights, (double*)out));
     return cuda_check("ssb_gather");
 }
 
@@ -136,11 +136,11 @@ int ssb_upsample2(int dtype, int B, int C, int Hc, int Wc, int Hf, int Wf, const
     dim3 block(32, 8), grid((Wf + 31) / 32, (Hf + 7) / 8, B);
     cudaStream_t s = (cudaStream_t)stream;
     if (dtype == SSB_F32)
-        k_upsample2<float><<<grid, block, 0, s>>>(C, Hc, Wc, Hf, Wf, (const float*)coarse,
-                                                  (const float*)weights, (float*)out);
+        SSB_LAUNCH(s, k_upsample2<float><<<grid, block, 0, s>>>(C, Hc, Wc, Hf, Wf, (const float*)coarse,
+                                                  (const float*)weights, (float*)out));
     else
-        k_upsample2<double><<<grid, block, 0, s>>>(C, Hc, Wc, Hf, Wf, (const double*)coarse,
-                                                   (const double*)weights, (double*)out);
+        SSB_LAUNCH(s, k_upsample2<double><<<grid, block, 0, s>>>(C, Hc, Wc, Hf, Wf, (const double*)coarse,
+                                                   (const double*)weights, (double*)out));
     return cuda_check("ssb_upsample2");
 }
 
@@ -157,11 +157,11 @@ int ssb_avgpool2(int dtype, int B, int C, int H, int W, const void* in, void* ou
     cudaStream_t s = (cudaStream_t)stream;
     dim3 block(32, 8), grid(((W + 1) / 2 + 31) / 32, ((H + 1) / 2 + 7) / 8, B);
     if (dtype == SSB_F32)
-        k_pool2<float><<<grid, block, 0, s>>>(C, H, W, (const float*)in, C * hw, hw, nullptr,
-                                              (float*)out, C * hwc, hwc);
+        SSB_LAUNCH(s, k_pool2<float><<<grid, block, 0, s>>>(C, H, W, (const float*)in, C * hw, hw, nullptr,
+                                              (float*)out, C * hwc, hwc));
     else
-        k_pool2<double><<<grid, block, 0, s>>>(C, H, W, (const double*)in, C * hw, hw, nullptr,
-                                               (double*)out, C * hwc, hwc);
+        SSB_LAUNCH(s, k_pool2<double><<<grid, block, 0, s>>>(C, H, W, (const double*)in, C * hw, hw, nullptr,
+                                               (double*)out, C * hwc, hwc));
     return cuda_check("ssb_avgpool2");
 }
 

@@ -1,4 +1,5 @@
 // C ABI of the pyramid filter + the reference's surface primitives.
+#include <atomic>
 #include <string>
 
 #include "pyr_launch.cuh"
@@ -16,6 +17,27 @@ int cuda_check(const char* where) {
         return SSB_ECUDA;
     }
     return SSB_OK;
+}
+
+// ---- launch accounting (see ssb_set_launch_events) ----
+static std::atomic<unsigned long long> g_launches{0};
+struct LaunchHook {
+    cudaEvent_t const* ev = nullptr;
+    int cap = 0;
+    int* count = nullptr;
+};
+static thread_local LaunchHook g_hook;
+
+void launch_begin(cudaStream_t s) {
+    if (g_hook.ev && *g_hook.count < g_hook.cap) cudaEventRecord(g_hook.ev[2 * *g_hook.count], s);
+}
+
+void launch_end(cudaStream_t s) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (g_hook.ev && *g_hook.count < g_hook.cap) {
+        cudaEventRecord(g_hook.ev[2 * *g_hook.count + 1], s);
+        ++*g_hook.count;
+    }
 }
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -99,6 +121,20 @@ extern "C" {
 int ssb_version(void) { return SSB_VERSION; }
 
 const char* ssb_last_error(void) { return g_last_error.c_str(); }
+
+unsigned long long ssb_launch_count(void) { return g_launches.load(); }
+
+int ssb_set_launch_events(void* const* events, int capacity, int* count) {
+    if (events && (capacity < 0 || !count)) {
+        set_error("ssb_set_launch_events: need capacity >= 0 and a count pointer");
+        return SSB_EINVAL;
+    }
+    g_hook.ev = reinterpret_cast<cudaEvent_t const*>(events);
+    g_hook.cap = events ? capacity : 0;
+    g_hook.count = events ? count : nullptr;
+    if (count) *count = 0;
+    return SSB_OK;
+}
 
 int ssb_pyr_logit_channels(const ssb_pyr_desc* d, int level) {
     PyrPlan p;

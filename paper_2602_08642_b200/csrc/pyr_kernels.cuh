@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(BWD_THREADS)
 
         // ------------------------------------------------ flush finished rows
         const bool bottom = qs + S >= H;
-        const int pend = bottom ? H : qs + S - R;
+        const int pend = max(bottom ? H : qs + S - R, next_flush);
         for (int i = tid; i < (pend - next_flush) * TXB; i += BWD_THREADS) {
             const int rr = i / TXB, xi = i - rr * TXB;
             const int P = next_flush + rr, gx = x0 + xi;

@@ -30,7 +30,7 @@ template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV
 void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
     dim3 block(FWD_TX, FWD_TY);
     dim3 grid((a.W + FWD_TX - 1) / FWD_TX, (a.H + FWD_TY - 1) / FWD_TY, B);
-    k_pyr_fwd<K, TL, T, L0, UP, TIED, PREV><<<grid, block, 0, s>>>(a);
+    SSB_LAUNCH(s, k_pyr_fwd<K, TL, T, L0, UP, TIED, PREV><<<grid, block, 0, s>>>(a));
 }
 
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
@@ -49,7 +49,7 @@ void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
     while (seg > 16 && (long long)strips * ((a.H + seg - 1) / seg) * B < 148 * 8) seg >>= 1;
     a.seg_h = seg;
     dim3 grid(strips, (a.H + seg - 1) / seg, B);
-    kern<<<grid, BWD_THREADS, SH::SMEM, s>>>(a);
+    SSB_LAUNCH(s, kern<<<grid, BWD_THREADS, SH::SMEM, s>>>(a));
 }
 
 template <int K, typename TL, typename T>
@@ -106,7 +106,7 @@ void launch_pool(int B, int nc, int H, int W, const T* in, long long in_b, long 
     const int Hc = (H + 1) >> 1, Wc = (W + 1) >> 1;
     dim3 block(32, 8);
     dim3 grid((Wc + 31) / 32, (Hc + 7) / 8, B);
-    k_pool2<T><<<grid, block, 0, s>>>(nc, H, W, in, in_b, in_c, dem, out, out_b, out_c);
+    SSB_LAUNCH(s, k_pool2<T><<<grid, block, 0, s>>>(nc, H, W, in, in_b, in_c, dem, out, out_b, out_c));
 }
 
 template <int K, typename TL, typename T>
@@ -238,7 +238,7 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
         f.g_demod = (io->g_demod && io->demod) ? (T*)io->g_demod + coff0 : nullptr;
         dim3 block(32, 8);
         dim3 grid((p.W + 31) / 32, (p.H + 7) / 8, p.B);
-        k_pyr_final<T><<<grid, block, 0, s>>>(f);
+        SSB_LAUNCH(s, k_pyr_final<T><<<grid, block, 0, s>>>(f));
     }
     return cuda_check("ssb_pyr_backward");
 }

@@ -48,12 +48,20 @@ def run_case(ops, noisy, logits_ref, demod, prev, up, k, dtype, logit_dtype=None
     return res
 
 
+def gscale(glogits):
+    """Scale of the logit gradients over all levels (ref test_pyramid.py:250
+    uses the same global scale for its gradcheck)."""
+    return max(np.abs(g).max() for g in glogits)
+
+
 def compare(res, ref, rtol, levels, want):
     assert_close(res["out"], ref["out"], rtol, "out")
     assert_close(res["g_input"], ref["g_input"], rtol, "g_input")
     if want:
+        floor = rtol * gscale(ref["g_logits"])
         for l in range(levels):
-            assert_close(res["g_logits"][l], ref["g_logits"][l], rtol, f"g_logits{l}")
+            np.testing.assert_allclose(res["g_logits"][l], ref["g_logits"][l], rtol=rtol,
+                                       atol=floor, err_msg=f"g_logits{l}")
         if "g_demod" in ref:
             assert_close(res["g_demod"], ref["g_demod"], rtol, "g_demod")
     if "g_prev" in ref:
@@ -142,8 +150,10 @@ def test_oracle_cases(ops, h, w, L, k, prev, blend, precision):
     rtol = 1e-5 if precision == "f32" else 1e-10
     assert_close(planar_to_hwc(out), ref["out"], rtol, "out")
     assert_close(planar_to_hwc(g.input), ref["g_input"], rtol, "g_input")
+    floor = rtol * gscale(ref["g_logits"])
     for l in range(L):
-        assert_close(planar_to_hwc(g.logits[l]), ref["g_logits"][l], rtol, f"g_logits{l}")
+        np.testing.assert_allclose(planar_to_hwc(g.logits[l]), ref["g_logits"][l], rtol=rtol,
+                                   atol=floor, err_msg=f"g_logits{l}")
     if dm is not None:
         assert_close(planar_to_hwc(g.demod), ref["g_demod"], rtol, "g_demod")
     if temporal:
@@ -165,7 +175,7 @@ def test_bf16_logits(ops, k, L):
     up = rng.normal(size=(h, w, 3)).astype(np.float32).astype(np.float64)
     out_r, tape = op.forward(noisy, logits, None, dm, k=k)
     g_r = op.backward(tape, up)
-    dev_lg = [hwc_to_planar(z.numpy(), torch.bfloat16) for z in lgb]
+    dev_lg = [hwc_to_planar(z, torch.bfloat16) for z in logits]  # exact: values are bf16
     out, t = ops.pyramid_forward(hwc_to_planar(noisy, torch.float32), dev_lg,
                                  hwc_to_planar(dm, torch.float32), ksize=k)
     g = ops.pyramid_backward(t, hwc_to_planar(up, torch.float32))
@@ -173,8 +183,9 @@ def test_bf16_logits(ops, k, L):
     assert_close(planar_to_hwc(out), out_r, 2e-2)
     assert_close(planar_to_hwc(g.input), g_r.input, 2e-2)
     assert_close(planar_to_hwc(g.demod), g_r.demod, 2e-2)
+    floor = 2e-2 * gscale(g_r.logits)
     for l in range(L):
-        assert_close(planar_to_hwc(g.logits[l]), g_r.logits[l], 2e-2)
+        np.testing.assert_allclose(planar_to_hwc(g.logits[l]), g_r.logits[l], rtol=2e-2, atol=floor)
 
 
 def test_many_channels_batched_draws(ops):
