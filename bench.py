@@ -323,6 +323,8 @@ def time_device(runner, steps, warmup, L, dist, world):
     per = len(names)
     cap = per * steps
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * cap)]
+    for e in evs:  # torch creates the underlying cudaEvent lazily, on first record
+        e.record(stream)
     ev_arr = (C.c_void_p * (2 * cap))(*[e.cuda_event for e in evs])
     count = C.c_int(0)
     if dist:

@@ -183,11 +183,28 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
 
 // ===========================================================================
 // Backward level kernel (column-strip walker)
+//
+// CTA = one column strip of TXB own columns (+r halo columns = 64 region
+// columns) and one segment of rows; it walks the segment in steps of S rows.
+// Per step (q rows [qs, qs+S)):
+//   A  every thread owns one region pixel: joint softmax of its logits ->
+//      s_w, upstream gradient G -> s_g, next image-ring row -> s_lin;
+//   B1 own pixels: weight gradients gw_t = sum_c G_c * L_c(q + o_t) (image
+//      ring, compile-time tap offsets), upsample-tap gradients from the
+//      coarse Lhat, softmax backward, logit gradients -> HBM;
+//   B2 own columns, all S rows: horizontal transposed gather
+//      h[dy] = sum_dx w_{dy,dx}(q_y, x-dx) G(q_y, x-dx), added into a
+//      per-(row-in-step) accumulator ring at row q_y + dy (each thread owns
+//      its ring column, so no races; the vertical clamp fold is applied at
+//      flush, the horizontal one in the border columns);
+//   B3 upsample transpose into per-row coarse accumulator rings;
+//   flush rows whose contributions are complete (sum over the S rings).
+// All arithmetic runs on 3 channels (missing channels are zero-filled), so
+// the inner loops carry no channel guards.
 // ===========================================================================
 constexpr int BWD_THREADS = 256;
 constexpr int BWD_RX = 64;  // region columns per strip (own columns + 2r halo)
 constexpr int BWD_LR = 16;  // image ring rows (>= 2S + 2r)
-constexpr int BWD_AR = 16;  // accumulator ring rows (>= S + 2r)
 constexpr int BWD_CR = 4;   // coarse accumulator ring rows (>= S/2 + 1)
 
 template <int K, bool UP, bool PREV, typename T>
@@ -197,43 +214,54 @@ struct BwdShape {
     static constexpr int NTM = PREV ? NT : 0;
     static constexpr int NW = NT + NUP + NTM;
     static constexpr int TXB = BWD_RX - 2 * R;
+    static constexpr int TXC = TXB / 2;
+    // accumulator rows live at once: S + 2r, plus the fold rows above row 0
+    // when row 0 is flushed only at the second step (S <= r)
+    static constexpr int ar(int S) { return S + 2 * R + (R + 1 > S ? R + 1 - S : 0); }
     static constexpr size_t bytes_for(int S) {
         return sizeof(T) * ((size_t)NW * S * BWD_RX + (size_t)kMaxCh * S * BWD_RX +
                             (size_t)kMaxCh * BWD_LR * BWD_RX * (PREV ? 2 : 1) +
-                            (size_t)kMaxCh * BWD_AR * TXB * (PREV ? 2 : 1) +
-                            (size_t)kMaxCh * BWD_CR * (TXB / 2));
+                            (size_t)S * ar(S) * kMaxCh * TXB * (PREV ? 2 : 1) +
+                            (size_t)S * BWD_CR * kMaxCh * TXC);
     }
     static constexpr int S = bytes_for(4) <= 200 * 1024 ? 4 : 2;
+    static constexpr int AR = ar(S);
     static constexpr size_t SMEM = bytes_for(S);
+    static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
+    static constexpr int MINB = MINB_SMEM > 3 ? 3 : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
     static constexpr bool REG_GW = NW <= 56;
 };
 
+__device__ __forceinline__ float rcp_dem(float d) { return __frcp_rn(d); }
+__device__ __forceinline__ double rcp_dem(double d) { return 1.0 / d; }
+
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
-__global__ void __launch_bounds__(BWD_THREADS)
+__global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
     k_pyr_bwd(const BwdLevel a) {
     using SH = BwdShape<K, UP, PREV, T>;
-    constexpr int R = SH::R, NT = SH::NT, NUP = SH::NUP, NW = SH::NW, TXB = SH::TXB, S = SH::S;
+    constexpr int R = SH::R, NT = SH::NT, NUP = SH::NUP, NW = SH::NW;
+    constexpr int TXB = SH::TXB, TXC = SH::TXC, S = SH::S, AR = SH::AR;
+    constexpr int RX = BWD_RX, CH = kMaxCh, CR = BWD_CR;
     constexpr int NLUP = UP ? (TIED ? 1 : 4) : 0;
-    constexpr int NLOG = NT + NLUP + SH::NTM;
-    constexpr int RUP = (R + 1) & ~1;  // rows of top halo, rounded up to even
-    constexpr int LRM = BWD_LR - 1, ARM = BWD_AR - 1, CRM = BWD_CR - 1;
-    constexpr int TXC = TXB / 2;
+    constexpr int RUP = (R + 1) & ~1;  // top halo rows, rounded up to even
+    constexpr int LRM = BWD_LR - 1;
+    constexpr int LSTR = BWD_LR * RX;  // channel stride of the image rings
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* s_w = reinterpret_cast<T*>(smem_raw);             // [NW][S][RX]
-    T* s_g = s_w + NW * S * BWD_RX;                      // [3][S][RX]
-    T* s_lin = s_g + kMaxCh * S * BWD_RX;                // [3][LR][RX]
-    T* s_prv = s_lin + kMaxCh * BWD_LR * BWD_RX;         // [3][LR][RX] (PREV)
-    T* s_acc = s_prv + (PREV ? kMaxCh * BWD_LR * BWD_RX : 0);  // [3][AR][TXB]
-    T* s_pac = s_acc + kMaxCh * BWD_AR * TXB;            // [3][AR][TXB] (PREV)
-    T* s_cac = s_pac + (PREV ? kMaxCh * BWD_AR * TXB : 0);     // [3][CR][TXC]
-#define SW(t, s, ri) s_w[((t) * S + (s)) * BWD_RX + (ri)]
-#define SG(c, s, ri) s_g[((c) * S + (s)) * BWD_RX + (ri)]
-#define SLIN(c, r, ri) s_lin[((c) * BWD_LR + ((r) & LRM)) * BWD_RX + (ri)]
-#define SPRV(c, r, ri) s_prv[((c) * BWD_LR + ((r) & LRM)) * BWD_RX + (ri)]
-#define SACC(c, p, xi) s_acc[((c) * BWD_AR + ((p) & ARM)) * TXB + (xi)]
-#define SPAC(c, p, xi) s_pac[((c) * BWD_AR + ((p) & ARM)) * TXB + (xi)]
-#define SCAC(c, y, xi) s_cac[((c) * BWD_CR + ((y) & CRM)) * TXC + (xi)]
+    T* s_w = reinterpret_cast<T*>(smem_raw);               // [NW][S][RX]
+    T* s_g = s_w + NW * S * RX;                            // [CH][S][RX]
+    T* s_lin = s_g + CH * S * RX;                          // [CH][LR][RX]
+    T* s_prv = s_lin + CH * LSTR;                          // [CH][LR][RX] (PREV)
+    T* s_acc = s_prv + (PREV ? CH * LSTR : 0);             // [S][AR][CH][TXB]
+    T* s_pac = s_acc + S * AR * CH * TXB;                  // [S][AR][CH][TXB] (PREV)
+    T* s_cac = s_pac + (PREV ? S * AR * CH * TXB : 0);     // [S][CR][CH][TXC]
+#define SW(t, s, ri) s_w[((t) * S + (s)) * RX + (ri)]
+#define SG(c, s, ri) s_g[((c) * S + (s)) * RX + (ri)]
+#define SLIN(c, r, ri) s_lin[(c) * LSTR + ((r) & LRM) * RX + (ri)]
+#define SPRV(c, r, ri) s_prv[(c) * LSTR + ((r) & LRM) * RX + (ri)]
+#define SACC(s, sl, c, xi) s_acc[(((s) * AR + (sl)) * CH + (c)) * TXB + (xi)]
+#define SPAC(s, sl, c, xi) s_pac[(((s) * AR + (sl)) * CH + (c)) * TXB + (xi)]
+#define SCAC(s, sl, c, xi) s_cac[(((s) * CR + (sl)) * CH + (c)) * TXC + (xi)]
 
     const int tid = threadIdx.x;
     const int b = blockIdx.z;
@@ -243,68 +271,62 @@ __global__ void __launch_bounds__(BWD_THREADS)
     const int qstart = max(y0 - RUP, 0);
     const int qend = min(y1 + R, H);
     const long long hw = (long long)H * W;
+    auto slot = [](int P) { return (P + 8 * AR) % AR; };
 
-    const TL* lg = (const TL*)a.logits + b * a.lg_b;
+    const TL* __restrict__ lg = (const TL*)a.logits + b * a.lg_b;
     TL* glg = a.want_params ? (TL*)a.glogits + b * a.lg_b : nullptr;
-    const T* lin = (const T*)a.lin + b * a.in_b;
-    const T* gin = (const T*)a.gin + b * a.in_b;
-    const T* dem = (L0 && a.demod) ? (const T*)a.demod + b * a.in_b : nullptr;
-    const T* prv = PREV ? (const T*)a.prev + b * a.in_b : nullptr;
-    const T* lhc = UP ? (const T*)a.lhat_c + b * a.c_b : nullptr;
+    const T* __restrict__ lin = (const T*)a.lin + b * a.in_b;
+    const T* __restrict__ gin = (const T*)a.gin + b * a.in_b;
+    const T* __restrict__ dem = (L0 && a.demod) ? (const T*)a.demod + b * a.in_b : nullptr;
+    const T* __restrict__ prv = PREV ? (const T*)a.prev + b * a.in_b : nullptr;
+    const T* __restrict__ lhc = UP ? (const T*)a.lhat_c + b * a.c_b : nullptr;
 
-    // ---- prologue: zero accumulators, preload image ring rows [qstart-R, qstart+R)
-    for (int i = tid; i < kMaxCh * BWD_AR * TXB; i += BWD_THREADS) {
+    // ---- prologue
+    for (int i = tid; i < S * AR * CH * TXB; i += BWD_THREADS) {
         s_acc[i] = (T)0;
         if constexpr (PREV) s_pac[i] = (T)0;
     }
-    for (int i = tid; i < kMaxCh * BWD_CR * TXC; i += BWD_THREADS) s_cac[i] = (T)0;
+    for (int i = tid; i < S * CR * CH * TXC; i += BWD_THREADS) s_cac[i] = (T)0;
 
     auto load_image_row = [&](int r, int ri) {
         const int gy = clampi(r, 0, H - 1), gx = clampi(xr0 + ri, 0, W - 1);
         const long long off = (long long)gy * W + gx;
+        T v[CH], p[CH], rd[CH];
 #pragma unroll
-        for (int c = 0; c < kMaxCh; ++c) {
-            if (c < nc) {
-                T v = lin[c * a.in_c + off];
-                T dc = (T)1;
-                if (dem) {
-                    dc = demod_clamp(dem[c * a.in_c + off]);
-                    v = v / dc;
-                }
-                SLIN(c, r, ri) = v;
-                if constexpr (PREV) {
-                    T p = prv[c * a.in_c + off];
-                    if (dem) p = p / dc;
-                    SPRV(c, r, ri) = p;
-                }
-            }
+        for (int c = 0; c < CH; ++c) {
+            v[c] = c < nc ? lin[c * a.in_c + off] : (T)0;
+            rd[c] = (dem && c < nc) ? rcp_dem(demod_clamp(dem[c * a.in_c + off])) : (T)1;
+            if constexpr (PREV) p[c] = c < nc ? prv[c * a.in_c + off] : (T)0;
+        }
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            SLIN(c, r, ri) = v[c] * rd[c];
+            if constexpr (PREV) SPRV(c, r, ri) = p[c] * rd[c];
         }
     };
-    for (int i = tid; i < 2 * R * BWD_RX; i += BWD_THREADS) {
-        const int rr = i / BWD_RX, ri = i - rr * BWD_RX;
+    for (int i = tid; i < 2 * R * RX; i += BWD_THREADS) {
+        const int rr = i / RX, ri = i - rr * RX;
         load_image_row(qstart - R + rr, ri);
     }
-
     int next_flush = max(qstart - R, 0);
     int cnext = qstart >> 1;
     __syncthreads();
 
     for (int qs = qstart; qs < qend; qs += S) {
-        // ------------------------------------------------ phase A: new rows
-        if (tid < S * BWD_RX) {
-            const int s = tid / BWD_RX, ri = tid - s * BWD_RX;
+        // ------------------------------------------------ A: new rows
+        if (tid < S * RX) {
+            const int s = tid / RX, ri = tid - s * RX;
             const int qy = qs + s, qx = xr0 + ri;
-            const bool in = (qy < H) && (qx >= 0) && (qx < W);
-            if (in) {
+            if ((qy < H) && (qx >= 0) && (qx < W)) {
                 const long long off = (long long)qy * W + qx;
                 const TL* lp = lg + off;
-                T e[NW];
-                if constexpr (NW <= 56) {
+                if constexpr (SH::REG_GW) {
+                    T e[NW];
 #pragma unroll
                     for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(lp + t * hw);
                     if constexpr (UP) {
                         if constexpr (TIED) {
-                            T v = ld_logit<T>(lp + NT * hw);
+                            const T v = ld_logit<T>(lp + NT * hw);
 #pragma unroll
                             for (int i = 0; i < 4; ++i) e[NT + i] = v;
                         } else {
@@ -330,7 +352,6 @@ __global__ void __launch_bounds__(BWD_THREADS)
 #pragma unroll
                     for (int t = 0; t < NW; ++t) SW(t, s, ri) = e[t] * inv;
                 } else {
-                    // large footprints: stage raw logits through shared memory
                     T m = (T)-INFINITY;
                     for (int t = 0; t < NW; ++t) {
                         int ch;
@@ -350,62 +371,59 @@ __global__ void __launch_bounds__(BWD_THREADS)
                     const T inv = (T)1 / sum;
                     for (int t = 0; t < NW; ++t) SW(t, s, ri) *= inv;
                 }
+                T g[CH];
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) {
-                    if (c < nc) {
-                        T g = gin[c * a.in_c + off];
-                        if (dem) g *= demod_clamp(dem[c * a.in_c + off]);
-                        SG(c, s, ri) = g;
-                    }
+                for (int c = 0; c < CH; ++c) {
+                    g[c] = c < nc ? gin[c * a.in_c + off] : (T)0;
+                    if (dem && c < nc) g[c] *= demod_clamp(dem[c * a.in_c + off]);
                 }
+#pragma unroll
+                for (int c = 0; c < CH; ++c) SG(c, s, ri) = g[c];
             } else {
+#pragma unroll 4
                 for (int t = 0; t < NW; ++t) SW(t, s, ri) = (T)0;
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) SG(c, s, ri) = (T)0;
+                for (int c = 0; c < CH; ++c) SG(c, s, ri) = (T)0;
             }
             load_image_row(qs + R + s, ri);
         }
         __syncthreads();
 
-        // ------------------------------------------------ B1: logit gradients
-        if (glg && tid < S * TXB) {
+        if (tid < S * TXB) {
             const int s = tid / TXB, xi = tid - s * TXB;
-            const int qy = qs + s, qx = x0 + xi;
-            if (qy >= y0 && qy < y1 && qx < W) {
-                const int ri = xi + R;
-                T gv[kMaxCh];
+            const int qy = qs + s, gx = x0 + xi;
+            const int ri = xi + R;
+            // -------------------------------------------- B1: logit gradients
+            if (glg && qy >= y0 && qy < y1 && gx < W) {
+                T gv[CH];
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) gv[c] = (c < nc) ? SG(c, s, ri) : (T)0;
-                const long long off = (long long)qy * W + qx;
-                TL* gp = glg + off;
-                int cy[2], cx[2];
-                if constexpr (UP) {
-                    cy[0] = min(qy >> 1, a.Hc - 1);
-                    cy[1] = min((qy + 1) >> 1, a.Hc - 1);
-                    cx[0] = min(qx >> 1, a.Wc - 1);
-                    cx[1] = min((qx + 1) >> 1, a.Wc - 1);
-                }
+                for (int c = 0; c < CH; ++c) gv[c] = SG(c, s, ri);
+                const T* lrow[K];
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) lrow[dy + R] = &SLIN(0, qy + dy, ri);
                 auto gw_of = [&](int t) -> T {
                     T acc = (T)0;
                     if (t < NT) {
-                        const int dy = t / K - R, dx = t % K - R;
+                        const int dy = t / K, dx = t % K - R;
 #pragma unroll
-                        for (int c = 0; c < kMaxCh; ++c)
-                            if (c < nc) acc += gv[c] * SLIN(c, qy + dy, ri + dx);
+                        for (int c = 0; c < CH; ++c) acc += gv[c] * lrow[dy][c * LSTR + dx];
                     } else if (t < NT + NUP) {
                         const int i = (t - NT) >> 1, j = (t - NT) & 1;
+                        const int cy = min((qy + i) >> 1, a.Hc - 1), cx = min((gx + j) >> 1, a.Wc - 1);
+                        const T* cp = lhc + (long long)cy * a.Wc + cx;
 #pragma unroll
-                        for (int c = 0; c < kMaxCh; ++c)
-                            if (c < nc) acc += gv[c] * lhc[c * a.c_c + cy[i] * a.Wc + cx[j]];
+                        for (int c = 0; c < CH; ++c)
+                            if (c < nc) acc += gv[c] * cp[c * a.c_c];
                     } else {
                         const int tt = t - NT - NUP;
                         const int dy = tt / K - R, dx = tt % K - R;
 #pragma unroll
-                        for (int c = 0; c < kMaxCh; ++c)
-                            if (c < nc) acc += gv[c] * SPRV(c, qy + dy, ri + dx);
+                        for (int c = 0; c < CH; ++c) acc += gv[c] * SPRV(c, qy + dy, ri + dx);
                     }
                     return acc;
                 };
+                TL* gp = glg + (long long)qy * W + gx;
+                const bool acc_mode = a.accum != 0;
                 if constexpr (SH::REG_GW) {
                     T gw[NW];
 #pragma unroll
@@ -416,13 +434,13 @@ __global__ void __launch_bounds__(BWD_THREADS)
                     T gb = (T)0;
 #pragma unroll
                     for (int t = 0; t < NW; ++t) {
-                        const T g = SW(t, s, ri) * (gw[t] - inner);
+                        const T gz = SW(t, s, ri) * (gw[t] - inner);
                         if (TIED && t >= NT && t < NT + NUP) {
-                            gb += g;
-                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, a.accum);
+                            gb += gz;
+                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, acc_mode);
                         } else {
                             const int ch = t < NT ? t : t - NUP + NLUP;
-                            st_glogit(gp + ch * hw, g, a.accum);
+                            st_glogit(gp + ch * hw, gz, acc_mode);
                         }
                     }
                 } else {
@@ -430,108 +448,114 @@ __global__ void __launch_bounds__(BWD_THREADS)
                     for (int t = 0; t < NW; ++t) inner += SW(t, s, ri) * gw_of(t);
                     T gb = (T)0;
                     for (int t = 0; t < NW; ++t) {
-                        const T g = SW(t, s, ri) * (gw_of(t) - inner);
+                        const T gz = SW(t, s, ri) * (gw_of(t) - inner);
                         if (TIED && t >= NT && t < NT + NUP) {
-                            gb += g;
-                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, a.accum);
+                            gb += gz;
+                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, acc_mode);
                         } else {
                             const int ch = t < NT ? t : t - NUP + NLUP;
-                            st_glogit(gp + ch * hw, g, a.accum);
+                            st_glogit(gp + ch * hw, gz, acc_mode);
                         }
                     }
                 }
             }
-        }
-
-        // ------------------------------------------------ B2: gather transpose
-        for (int i = tid; i < (S + 2 * R) * TXB; i += BWD_THREADS) {
-            const int arow = i / TXB, xi = i - arow * TXB;
-            const int P = qs - R + arow;
-            const int gx = x0 + xi;
-            if (gx >= W) continue;
-            T acc[kMaxCh], pac[kMaxCh];
+            // -------------------------------------------- B2: gather transpose
+            if (qy < H && gx < W) {
+                T h[K][CH], hp[PREV ? K : 1][CH];
 #pragma unroll
-            for (int c = 0; c < kMaxCh; ++c) acc[c] = pac[c] = (T)0;
+                for (int d = 0; d < K; ++d)
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int dy = P - (qs + s);
-                if (dy < -R || dy > R) continue;
-                const int tb = (dy + R) * K;
+                    for (int c = 0; c < CH; ++c) {
+                        h[d][c] = (T)0;
+                        if constexpr (PREV) hp[d][c] = (T)0;
+                    }
 #pragma unroll
                 for (int dx = -R; dx <= R; ++dx) {
-                    const int ri = xi + R - dx;
-                    const T wv = SW(tb + dx + R, s, ri);
+                    const int rj = ri - dx;
+                    T gq[CH];
 #pragma unroll
-                    for (int c = 0; c < kMaxCh; ++c) acc[c] += wv * SG(c, s, ri);
-                    if constexpr (PREV) {
-                        const T pv = SW(NT + NUP + tb + dx + R, s, ri);
+                    for (int c = 0; c < CH; ++c) gq[c] = SG(c, s, rj);
 #pragma unroll
-                        for (int c = 0; c < kMaxCh; ++c) pac[c] += pv * SG(c, s, ri);
+                    for (int d = 0; d < K; ++d) {
+                        const T wv = SW(d * K + dx + R, s, rj);
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) h[d][c] += wv * gq[c];
+                        if constexpr (PREV) {
+                            const T pv = SW(NT + NUP + d * K + dx + R, s, rj);
+#pragma unroll
+                            for (int c = 0; c < CH; ++c) hp[d][c] += pv * gq[c];
+                        }
                     }
                 }
-                // clamp fold along x: logical columns beyond the border land on it
                 if (gx == 0 || gx == W - 1) {
+                    // clamp fold along x: logical columns beyond the border
                     for (int side = 0; side < 2; ++side) {
-                        if (side == 0 && gx != 0) continue;
-                        if (side == 1 && gx != W - 1) continue;
+                        if ((side == 0 && gx != 0) || (side == 1 && gx != W - 1)) continue;
                         for (int e = 1; e <= R; ++e) {
                             const int Pc = side == 0 ? -e : W - 1 + e;
                             for (int dx = -R; dx <= R; ++dx) {
                                 const int qx = Pc - dx;
                                 if (qx < 0 || qx >= W) continue;
-                                const int ri = qx - xr0;
-                                const T wv = SW(tb + dx + R, s, ri);
+                                const int rj = qx - xr0;
+                                for (int d = 0; d < K; ++d) {
+                                    const T wv = SW(d * K + dx + R, s, rj);
 #pragma unroll
-                                for (int c = 0; c < kMaxCh; ++c) acc[c] += wv * SG(c, s, ri);
-                                if constexpr (PREV) {
-                                    const T pv = SW(NT + NUP + tb + dx + R, s, ri);
+                                    for (int c = 0; c < CH; ++c) h[d][c] += wv * SG(c, s, rj);
+                                    if constexpr (PREV) {
+                                        const T pv = SW(NT + NUP + d * K + dx + R, s, rj);
 #pragma unroll
-                                    for (int c = 0; c < kMaxCh; ++c) pac[c] += pv * SG(c, s, ri);
+                                        for (int c = 0; c < CH; ++c) hp[d][c] += pv * SG(c, s, rj);
+                                    }
                                 }
                             }
                         }
                     }
                 }
-            }
 #pragma unroll
-            for (int c = 0; c < kMaxCh; ++c) {
-                SACC(c, P, xi) += acc[c];
-                if constexpr (PREV) SPAC(c, P, xi) += pac[c];
+                for (int d = 0; d < K; ++d) {
+                    const int sl = slot(qy + d - R);
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        SACC(s, sl, c, xi) += h[d][c];
+                        if constexpr (PREV) SPAC(s, sl, c, xi) += hp[d][c];
+                    }
+                }
             }
         }
-
         // ------------------------------------------------ B3: upsample transpose
         if constexpr (UP) {
-            for (int i = tid; i < (S / 2 + 1) * TXC; i += BWD_THREADS) {
-                const int cyo = i / TXC, cxi = i - cyo * TXC;
-                const int Y = (qs >> 1) + cyo, X = (x0 >> 1) + cxi;
-                if (Y >= a.Hc || X >= a.Wc) continue;
-                T acc[kMaxCh];
+            if (tid < S * TXC) {
+                const int s = tid / TXC, cxi = tid - s * TXC;
+                const int qy = qs + s, X = (x0 >> 1) + cxi;
+                if (qy < H && X < a.Wc) {
+                    T v0[CH], v1[CH];
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) acc[c] = (T)0;
+                    for (int c = 0; c < CH; ++c) v0[c] = v1[c] = (T)0;
 #pragma unroll
-                for (int yy = 2 * Y - 1; yy <= 2 * Y + 1; ++yy) {
-                    if (yy < qs || yy >= qs + S || yy >= H) continue;
-                    const int s = yy - qs;
+                    for (int k3 = -1; k3 <= 1; ++k3) {
+                        const int xx = 2 * X + k3;
+                        if (xx < 0 || xx >= W) continue;
+                        const int rj = xx - xr0;
+                        T gq[CH];
 #pragma unroll
-                    for (int ii = 0; ii < 2; ++ii) {
-                        if (min((yy + ii) >> 1, a.Hc - 1) != Y) continue;
+                        for (int c = 0; c < CH; ++c) gq[c] = SG(c, s, rj);
 #pragma unroll
-                        for (int xx = 2 * X - 1; xx <= 2 * X + 1; ++xx) {
-                            if (xx < 0 || xx >= W) continue;
-                            const int ri = xx - xr0;
+                        for (int jj = 0; jj < 2; ++jj) {
+                            if (min((xx + jj) >> 1, a.Wc - 1) != X) continue;
+                            const T w0 = SW(NT + jj, s, rj), w1 = SW(NT + 2 + jj, s, rj);
 #pragma unroll
-                            for (int jj = 0; jj < 2; ++jj) {
-                                if (min((xx + jj) >> 1, a.Wc - 1) != X) continue;
-                                const T wv = SW(NT + ii * 2 + jj, s, ri);
-#pragma unroll
-                                for (int c = 0; c < kMaxCh; ++c) acc[c] += wv * SG(c, s, ri);
+                            for (int c = 0; c < CH; ++c) {
+                                v0[c] += w0 * gq[c];
+                                v1[c] += w1 * gq[c];
                             }
                         }
                     }
-                }
+                    const int Y0 = min(qy >> 1, a.Hc - 1), Y1 = min((qy + 1) >> 1, a.Hc - 1);
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) SCAC(c, Y, cxi) += acc[c];
+                    for (int c = 0; c < CH; ++c) SCAC(s, Y0 & (CR - 1), c, cxi) += v0[c];
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) SCAC(s, Y1 & (CR - 1), c, cxi) += v1[c];
+                }
             }
         }
         __syncthreads();
@@ -542,43 +566,28 @@ __global__ void __launch_bounds__(BWD_THREADS)
         for (int i = tid; i < (pend - next_flush) * TXB; i += BWD_THREADS) {
             const int rr = i / TXB, xi = i - rr * TXB;
             const int P = next_flush + rr, gx = x0 + xi;
-            T v[kMaxCh], pv[kMaxCh];
+            T v[CH], pv[CH];
+            auto take = [&](int row) {
+                const int sl = slot(row);
 #pragma unroll
-            for (int c = 0; c < kMaxCh; ++c) {
-                v[c] = SACC(c, P, xi);
-                SACC(c, P, xi) = (T)0;
-                pv[c] = (T)0;
-                if constexpr (PREV) {
-                    pv[c] = SPAC(c, P, xi);
-                    SPAC(c, P, xi) = (T)0;
-                }
-            }
-            if (P == 0) {  // fold logical rows -R..-1 onto row 0
-                for (int e = 1; e <= R; ++e) {
+                for (int s = 0; s < S; ++s)
 #pragma unroll
-                    for (int c = 0; c < kMaxCh; ++c) {
-                        v[c] += SACC(c, -e, xi);
-                        SACC(c, -e, xi) = (T)0;
+                    for (int c = 0; c < CH; ++c) {
+                        v[c] += SACC(s, sl, c, xi);
+                        SACC(s, sl, c, xi) = (T)0;
                         if constexpr (PREV) {
-                            pv[c] += SPAC(c, -e, xi);
-                            SPAC(c, -e, xi) = (T)0;
+                            pv[c] += SPAC(s, sl, c, xi);
+                            SPAC(s, sl, c, xi) = (T)0;
                         }
                     }
-                }
-            }
-            if (P == H - 1) {  // fold logical rows H..H+R-1 onto the last row
-                for (int e = 1; e <= R; ++e) {
+            };
 #pragma unroll
-                    for (int c = 0; c < kMaxCh; ++c) {
-                        v[c] += SACC(c, H - 1 + e, xi);
-                        SACC(c, H - 1 + e, xi) = (T)0;
-                        if constexpr (PREV) {
-                            pv[c] += SPAC(c, H - 1 + e, xi);
-                            SPAC(c, H - 1 + e, xi) = (T)0;
-                        }
-                    }
-                }
-            }
+            for (int c = 0; c < CH; ++c) v[c] = pv[c] = (T)0;
+            take(P);
+            if (P == 0)
+                for (int e = 1; e <= R; ++e) take(-e);  // fold rows above the image
+            if (P == H - 1)
+                for (int e = 1; e <= R; ++e) take(H - 1 + e);  // and below it
             if (P < y0 || P >= y1 || gx >= W) continue;
             const long long off = (long long)P * W + gx;
             T* glo = (T*)a.gl_out + b * a.in_b;
@@ -588,19 +597,19 @@ __global__ void __launch_bounds__(BWD_THREADS)
                 const T* up = (const T*)a.gin + b * a.in_b;
                 const T* op = a.outp ? (const T*)a.outp + b * a.in_b : nullptr;
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) {
+                for (int c = 0; c < CH; ++c) {
                     if (c >= nc) break;
                     const long long o = c * a.in_c + off;
                     if (dem) {
-                        const T dc = demod_clamp(dem[o]);
-                        glo[o] = v[c] / dc;
+                        const T rd = rcp_dem(demod_clamp(dem[o]));
+                        glo[o] = v[c] * rd;
                         if (gdo) {
                             const T x0v = SLIN(c, P, xi + R);
-                            T gd = up[o] * (op[o] / dc) - v[c] * x0v / dc;
-                            if constexpr (PREV) gd -= pv[c] * SPRV(c, P, xi + R) / dc;
+                            T gd = up[o] * (op[o] * rd) - v[c] * x0v * rd;
+                            if constexpr (PREV) gd -= pv[c] * SPRV(c, P, xi + R) * rd;
                             gdo[o] = gd;
                         }
-                        if constexpr (PREV) gpo[o] = pv[c] / dc;
+                        if constexpr (PREV) gpo[o] = pv[c] * rd;
                     } else {
                         glo[o] = v[c];
                         if constexpr (PREV) gpo[o] = pv[c];
@@ -608,7 +617,7 @@ __global__ void __launch_bounds__(BWD_THREADS)
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c)
+                for (int c = 0; c < CH; ++c)
                     if (c < nc) glo[c * a.in_c + off] = v[c];
             }
         }
@@ -620,16 +629,20 @@ __global__ void __launch_bounds__(BWD_THREADS)
             for (int i = tid; i < (cend - cnext) * TXC; i += BWD_THREADS) {
                 const int rr = i / TXC, cxi = i - rr * TXC;
                 const int Y = cnext + rr, X = (x0 >> 1) + cxi;
-                T v[kMaxCh];
+                T v[CH];
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c) {
-                    v[c] = SCAC(c, Y, cxi);
-                    SCAC(c, Y, cxi) = (T)0;
-                }
+                for (int c = 0; c < CH; ++c) v[c] = (T)0;
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int c = 0; c < CH; ++c) {
+                        v[c] += SCAC(s, Y & (CR - 1), c, cxi);
+                        SCAC(s, Y & (CR - 1), c, cxi) = (T)0;
+                    }
                 if (Y < own0 || Y >= own1 || X >= a.Wc) continue;
                 T* gc = (T*)a.ghat_c + b * a.c_b + (long long)Y * a.Wc + X;
 #pragma unroll
-                for (int c = 0; c < kMaxCh; ++c)
+                for (int c = 0; c < CH; ++c)
                     if (c < nc) gc[c * a.c_c] = v[c];
             }
             cnext = cend;
@@ -660,20 +673,32 @@ __global__ void k_pool2(int nc, int H, int W, const T* __restrict__ in, long lon
     const int yb = 2 * Y, xb = 2 * X;
     const bool hy = yb + 1 < H, hx = xb + 1 < W;
     const T cnt = (T)((hy ? 2 : 1) * (hx ? 2 : 1));
-    for (int c = 0; c < nc; ++c) {
+    const long long o00 = (long long)yb * W + xb;
+    const long long o01 = hx ? o00 + 1 : o00, o10 = hy ? o00 + W : o00, o11 = hy ? o01 + W : o01;
+    T v[kMaxCh][4];
+#pragma unroll
+    for (int c = 0; c < kMaxCh; ++c) {
+        if (c >= nc) break;
         const T* p = in + b * in_b + c * in_c;
-        const T* d = dem ? dem + b * in_b + c * in_c : nullptr;
-        auto val = [&](int y, int x) -> T {
-            T v = p[(long long)y * W + x];
-            if (d) v = v / demod_clamp(d[(long long)y * W + x]);
-            return v;
-        };
-        // pyramid.py:144 sums the 2x2 block (zeros outside) then divides
-        T s00 = val(yb, xb);
-        T s01 = hx ? val(yb, xb + 1) : (T)0;
-        T s10 = hy ? val(yb + 1, xb) : (T)0;
-        T s11 = (hx && hy) ? val(yb + 1, xb + 1) : (T)0;
-        out[b * out_b + c * out_c + (long long)Y * Wc + X] = ((s00 + s01) + (s10 + s11)) / cnt;
+        v[c][0] = p[o00];
+        v[c][1] = p[o01];
+        v[c][2] = p[o10];
+        v[c][3] = p[o11];
+        if (dem) {
+            const T* d = dem + b * in_b + c * in_c;
+            v[c][0] = v[c][0] / demod_clamp(d[o00]);
+            v[c][1] = v[c][1] / demod_clamp(d[o01]);
+            v[c][2] = v[c][2] / demod_clamp(d[o10]);
+            v[c][3] = v[c][3] / demod_clamp(d[o11]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCh; ++c) {
+        if (c >= nc) break;
+        // pyramid.py:144 sums the 2x2 block (zeros outside the image), then divides
+        const T s01 = hx ? v[c][1] : (T)0, s10 = hy ? v[c][2] : (T)0;
+        const T s11 = (hx && hy) ? v[c][3] : (T)0;
+        out[b * out_b + c * out_c + (long long)Y * Wc + X] = ((v[c][0] + s01) + (s10 + s11)) / cnt;
     }
 }
 
@@ -703,38 +728,63 @@ __global__ void k_pyr_final(const FinalArgs a) {
     const int b = blockIdx.z;
     if (x >= a.W || y >= a.H) return;
     const long long off = (long long)y * a.W + x;
-    for (int c = 0; c < a.nc; ++c) {
-        T pb = (T)0;
-        if (a.levels > 1) {
-            const int top = a.levels - 1;
-            const T* gt = (const T*)a.gl[top] + b * a.gl_b[top] + c * a.gl_c[top];
-            T v = gt[(long long)(y >> top) * a.dims_w[top] + (x >> top)];
-            for (int l = top - 1; l >= 0; --l) {
-                // count of the level-(l+1) ancestor's children at level l
-                const int Y = y >> (l + 1), X = x >> (l + 1);
-                const int hy = (2 * Y + 1 < a.dims_h[l]) ? 2 : 1;
-                const int hx = (2 * X + 1 < a.dims_w[l]) ? 2 : 1;
-                v = v / (T)(hy * hx);
-                if (l == 0) break;
-                const T* gl = (const T*)a.gl[l] + b * a.gl_b[l] + c * a.gl_c[l];
-                v = v + gl[(long long)(y >> l) * a.dims_w[l] + (x >> l)];
-            }
-            pb = v;
+    // pool^T chain: identical for every channel except the gL values
+    T pb[kMaxCh];
+#pragma unroll
+    for (int c = 0; c < kMaxCh; ++c) pb[c] = (T)0;
+    if (a.levels > 1) {
+        const int top = a.levels - 1;
+        const long long ot = (long long)(y >> top) * a.dims_w[top] + (x >> top);
+        const T* gt = (const T*)a.gl[top] + b * a.gl_b[top];
+#pragma unroll
+        for (int c = 0; c < kMaxCh; ++c)
+            if (c < a.nc) pb[c] = gt[c * a.gl_c[top] + ot];
+        for (int l = top - 1; l >= 0; --l) {
+            // children count of the level-(l+1) ancestor, at level l
+            const int Y = y >> (l + 1), X = x >> (l + 1);
+            const T cnt = (T)(((2 * Y + 1 < a.dims_h[l]) ? 2 : 1) * ((2 * X + 1 < a.dims_w[l]) ? 2 : 1));
+#pragma unroll
+            for (int c = 0; c < kMaxCh; ++c) pb[c] = pb[c] / cnt;
+            if (l == 0) break;
+            const T* gl = (const T*)a.gl[l] + b * a.gl_b[l];
+            const long long ol = (long long)(y >> l) * a.dims_w[l] + (x >> l);
+#pragma unroll
+            for (int c = 0; c < kMaxCh; ++c)
+                if (c < a.nc) pb[c] = pb[c] + gl[c * a.gl_c[l] + ol];
         }
+    }
+    T* __restrict__ gn = (T*)a.g_noisy;
+    T* __restrict__ gd = (T*)a.g_demod;
+    const T* __restrict__ dm = (const T*)a.demod;
+    const T* __restrict__ nz = (const T*)a.noisy;
+    T vn[kMaxCh], vd[kMaxCh], vdem[kMaxCh], vx[kMaxCh];
+#pragma unroll
+    for (int c = 0; c < kMaxCh; ++c) {
+        if (c >= a.nc) break;
         const long long o = b * a.in_b + c * a.in_c + off;
-        T* gn = (T*)a.g_noisy;
-        if (a.demod) {
-            const T dv = ((const T*)a.demod)[o];
-            const T dc = demod_clamp(dv);
-            gn[o] = gn[o] + pb / dc;
-            if (a.g_demod) {
-                T* gd = (T*)a.g_demod;
-                const T x0 = ((const T*)a.noisy)[o] / dc;
-                const T gdc = gd[o] - pb * x0 / dc;
-                gd[o] = dv > (T)kDemodFloor ? gdc : (T)0;
+        vn[c] = gn[o];
+        if (dm) {
+            vdem[c] = dm[o];
+            if (gd) {
+                vd[c] = gd[o];
+                vx[c] = nz[o];
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCh; ++c) {
+        if (c >= a.nc) break;
+        const long long o = b * a.in_b + c * a.in_c + off;
+        if (dm) {
+            const T dc = demod_clamp(vdem[c]);
+            gn[o] = vn[c] + pb[c] / dc;
+            if (gd) {
+                const T x0 = vx[c] / dc;
+                const T gdc = vd[c] - pb[c] * x0 / dc;
+                gd[o] = vdem[c] > (T)kDemodFloor ? gdc : (T)0;
             }
         } else {
-            gn[o] = gn[o] + pb;
+            gn[o] = vn[c] + pb[c];
         }
     }
 }
