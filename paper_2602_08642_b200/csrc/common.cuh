@@ -41,13 +41,25 @@ __device__ __forceinline__ void st_glogit(__nv_bfloat16* p, float v, bool acc) {
 }
 
 // ---- exponentials ---------------------------------------------------------
-// fp32: MUFU.EX2-based fast exp (arguments are <= 0 after max subtraction, so
-// the relative error is a few ulp where the weight matters); fp64: libdevice.
-__device__ __forceinline__ float sexp(float x) { return __expf(x); }
+// fp32: MUFU.EX2 with flush-to-zero (arguments are <= 0 after the max
+// subtraction; weights below 2^-126 are irrelevant), the max subtraction folded
+// into one FFMA: exp(l - m) = 2^(l*log2e - m*log2e).  fp64: libdevice exp.
+constexpr float kLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// softmax numerator: `mk` is prep_max(m) for the row max m
+__device__ __forceinline__ float prep_max(float m) { return m * kLog2e; }
+__device__ __forceinline__ double prep_max(double m) { return m; }
+__device__ __forceinline__ float softmax_exp(float l, float mk) { return ex2_ftz(fmaf(l, kLog2e, -mk)); }
+__device__ __forceinline__ double softmax_exp(double l, double mk) { return exp(l - mk); }
+__device__ __forceinline__ float sexp(float x) { return ex2_ftz(x * kLog2e); }
 __device__ __forceinline__ double sexp(double x) { return exp(x); }
 
-template <typename T>
-__device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
+__device__ __forceinline__ float tmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
 
 template <typename T>
 __device__ __forceinline__ T demod_clamp(T d) { return d > (T)kDemodFloor ? d : (T)kDemodFloor; }

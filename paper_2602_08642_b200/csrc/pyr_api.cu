@@ -107,6 +107,12 @@ int make_plan(const ssb_pyr_desc* d, PyrPlan* p) {
         p->gl_off[l] = w;
         w += bytes;
     }
+    // kernels address channels of one frame with 32-bit offsets
+    if ((unsigned long long)p->nlog[0] * (unsigned long long)p->H * (unsigned long long)p->W >=
+        (1ull << 32)) {
+        set_error("frame too large: logit channels * H * W must stay below 2^32 per frame");
+        return SSB_EUNSUPPORTED;
+    }
     p->tape_bytes = t;
     p->ws_bytes = w;
     return SSB_OK;

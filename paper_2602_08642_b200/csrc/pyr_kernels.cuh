@@ -57,6 +57,27 @@ struct BwdLevel {
     void* ghat_c;  // coarse ghat^{l+1}
 };
 
+// Load one pixel's logits in weight order (denoise, 4 upsample -- the tied
+// blend logit broadcast --, temporal); `hw` is the per-frame channel stride
+// (32-bit: one uniform multiply + one IMAD.WIDE per load).
+template <typename T, int NT, int NUP, int NLUP, int NTM, typename TL>
+__device__ __forceinline__ void load_softmax_logits(const TL* __restrict__ lp, unsigned hw, T* e) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(lp + t * hw);
+    if constexpr (NUP > 0) {
+        if constexpr (NLUP == 1) {
+            const T v = ld_logit<T>(lp + NT * hw);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[NT + i] = v;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[NT + i] = ld_logit<T>(lp + (NT + i) * hw);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NTM; ++t) e[NT + NUP + t] = ld_logit<T>(lp + (NT + NLUP + t) * hw);
+}
+
 // ===========================================================================
 // Forward level kernel
 // ===========================================================================
@@ -110,31 +131,16 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
     T e[NW];
     T sum = (T)0;
     if (valid) {
-        const long long hw = (long long)H * W, off = (long long)y * W + x;
-        const TL* lg = (const TL*)a.logits + b * a.lg_b + off;
-        T m;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(lg + t * hw);
-        if constexpr (UP) {
-            if constexpr (TIED) {
-                T v = ld_logit<T>(lg + NT * hw);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) e[NT + i] = v;
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) e[NT + i] = ld_logit<T>(lg + (NT + i) * hw);
-            }
-        }
-        if constexpr (PREV) {
-#pragma unroll
-            for (int t = 0; t < NT; ++t) e[NT + NUP + t] = ld_logit<T>(lg + (NT + NLUP + t) * hw);
-        }
-        m = e[0];
+        const unsigned hw = (unsigned)H * (unsigned)W;
+        const TL* lg = (const TL*)a.logits + b * a.lg_b + ((long long)y * W + x);
+        load_softmax_logits<T, NT, NUP, NLUP, NTM>(lg, hw, e);
+        T m = e[0];
 #pragma unroll
         for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
+        const T mk = prep_max(m);
 #pragma unroll
         for (int t = 0; t < NW; ++t) {
-            e[t] = sexp(e[t] - m);
+            e[t] = softmax_exp(e[t], mk);
             sum += e[t];
         }
     }
@@ -215,9 +221,11 @@ struct BwdShape {
     static constexpr int NW = NT + NUP + NTM;
     static constexpr int TXB = BWD_RX - 2 * R;
     static constexpr int TXC = TXB / 2;
-    // accumulator rows live at once: S + 2r, plus the fold rows above row 0
-    // when row 0 is flushed only at the second step (S <= r)
-    static constexpr int ar(int S) { return S + 2 * R + (R + 1 > S ? R + 1 - S : 0); }
+    // accumulator rows live at once: S + 2r, plus -- while row 0 is not yet
+    // flushed (until the first step with qs + S - r > 0) -- the r fold rows
+    // above the image: r + (qs* + S + r) with qs* that first step's start row
+    static constexpr int first_flush_qs(int S) { return R >= S ? S * ((R - S + 1 + S - 1) / S) : 0; }
+    static constexpr int ar(int S) { return S + 2 * R + first_flush_qs(S); }
     static constexpr size_t bytes_for(int S) {
         return sizeof(T) * ((size_t)NW * S * BWD_RX + (size_t)kMaxCh * S * BWD_RX +
                             (size_t)kMaxCh * BWD_LR * BWD_RX * (PREV ? 2 : 1) +
@@ -232,7 +240,7 @@ struct BwdShape {
     static constexpr bool REG_GW = NW <= 56;
 };
 
-__device__ __forceinline__ float rcp_dem(float d) { return __frcp_rn(d); }
+__device__ __forceinline__ float rcp_dem(float d) { return __fdividef(1.0f, d); }
 __device__ __forceinline__ double rcp_dem(double d) { return 1.0 / d; }
 
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
     const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
     const int qstart = max(y0 - RUP, 0);
     const int qend = min(y1 + R, H);
-    const long long hw = (long long)H * W;
+    const unsigned hw32 = (unsigned)H * (unsigned)W;
     auto slot = [](int P) { return (P + 8 * AR) % AR; };
 
     const TL* __restrict__ lg = (const TL*)a.logits + b * a.lg_b;
@@ -322,30 +330,15 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
                 const TL* lp = lg + off;
                 if constexpr (SH::REG_GW) {
                     T e[NW];
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(lp + t * hw);
-                    if constexpr (UP) {
-                        if constexpr (TIED) {
-                            const T v = ld_logit<T>(lp + NT * hw);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) e[NT + i] = v;
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) e[NT + i] = ld_logit<T>(lp + (NT + i) * hw);
-                        }
-                    }
-                    if constexpr (PREV) {
-#pragma unroll
-                        for (int t = 0; t < NT; ++t)
-                            e[NT + NUP + t] = ld_logit<T>(lp + (NT + NLUP + t) * hw);
-                    }
+                    load_softmax_logits<T, NT, NUP, NLUP, SH::NTM>(lp, hw32, e);
                     T m = e[0];
 #pragma unroll
                     for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
+                    const T mk = prep_max(m);
                     T sum = (T)0;
 #pragma unroll
                     for (int t = 0; t < NW; ++t) {
-                        e[t] = sexp(e[t] - m);
+                        e[t] = softmax_exp(e[t], mk);
                         sum += e[t];
                     }
                     const T inv = (T)1 / sum;
@@ -358,13 +351,14 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
                         if (t < NT) ch = t;
                         else if (t < NT + NUP) ch = TIED ? NT : t;
                         else ch = t - NUP + NLUP;
-                        const T v = ld_logit<T>(lp + ch * hw);
+                        const T v = ld_logit<T>(lp + ch * hw32);
                         SW(t, s, ri) = v;
                         m = tmax(m, v);
                     }
+                    const T mk = prep_max(m);
                     T sum = (T)0;
                     for (int t = 0; t < NW; ++t) {
-                        const T ev = sexp(SW(t, s, ri) - m);
+                        const T ev = softmax_exp(SW(t, s, ri), mk);
                         SW(t, s, ri) = ev;
                         sum += ev;
                     }
@@ -431,17 +425,20 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
                     T inner = (T)0;
 #pragma unroll
                     for (int t = 0; t < NW; ++t) inner += SW(t, s, ri) * gw[t];
-                    T gb = (T)0;
 #pragma unroll
-                    for (int t = 0; t < NW; ++t) {
-                        const T gz = SW(t, s, ri) * (gw[t] - inner);
-                        if (TIED && t >= NT && t < NT + NUP) {
-                            gb += gz;
-                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, acc_mode);
-                        } else {
-                            const int ch = t < NT ? t : t - NUP + NLUP;
-                            st_glogit(gp + ch * hw, gz, acc_mode);
-                        }
+                    for (int t = 0; t < NW; ++t) gw[t] = SW(t, s, ri) * (gw[t] - inner);
+                    if constexpr (TIED) gw[NT] = ((gw[NT] + gw[NT + 1]) + gw[NT + 2]) + gw[NT + 3];
+                    // output channel of weight t (the tied blend logit takes the sum)
+                    auto chan = [](int t) { return t < NT ? t : (t < NT + NUP ? NT + (TIED ? 0 : t - NT) : t - NUP + NLUP); };
+                    auto skip = [](int t) { return TIED && t > NT && t < NT + NUP; };
+                    if (acc_mode) {
+#pragma unroll
+                        for (int t = 0; t < NW; ++t)
+                            if (!skip(t)) st_glogit(gp + chan(t) * hw32, gw[t], true);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < NW; ++t)
+                            if (!skip(t)) st_glogit(gp + chan(t) * hw32, gw[t], false);
                     }
                 } else {
                     T inner = (T)0;
@@ -451,10 +448,10 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
                         const T gz = SW(t, s, ri) * (gw_of(t) - inner);
                         if (TIED && t >= NT && t < NT + NUP) {
                             gb += gz;
-                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw, gb, acc_mode);
+                            if (t == NT + NUP - 1) st_glogit(gp + NT * hw32, gb, acc_mode);
                         } else {
                             const int ch = t < NT ? t : t - NUP + NLUP;
-                            st_glogit(gp + ch * hw, gz, acc_mode);
+                            st_glogit(gp + ch * hw32, gz, acc_mode);
                         }
                     }
                 }
