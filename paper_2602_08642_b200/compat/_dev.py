@@ -1,0 +1,66 @@
+"""Host <-> device plumbing for the reference-signature compat layer.
+
+The reference works on HWC float64 numpy arrays; the CUDA kernels take planar
+(B, C, H, W) device tensors.  The compat layer converts once on entry and once
+on exit.  Precision of the device computation:
+
+* ``"f64"`` (default): float64 kernels -- results equal the reference to
+  rounding, so the layer is a true drop-in (the reference's exact-equality
+  assertions hold);
+* ``"f32"``: float32 kernels, the throughput configuration (parity 1e-5).
+
+Set with :func:`set_precision` or the ``SSB_COMPAT_PRECISION`` env var.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+_PRECISION = os.environ.get("SSB_COMPAT_PRECISION", "f64")
+_DEVICE = os.environ.get("SSB_COMPAT_DEVICE", "cuda")
+
+
+def set_precision(p: str) -> None:
+    global _PRECISION
+    if p not in ("f32", "f64"):
+        raise ValueError("precision must be 'f32' or 'f64'")
+    _PRECISION = p
+
+
+def precision() -> str:
+    return _PRECISION
+
+
+def dtype() -> torch.dtype:
+    return torch.float64 if _PRECISION == "f64" else torch.float32
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2602_08642_b200.compat needs a CUDA device (no CPU fallback)")
+    return torch.device(_DEVICE)
+
+
+def to_planar(a, dt=None) -> torch.Tensor:
+    """(H, W, C) array -> (1, C, H, W) device tensor."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 2:
+        a = a[:, :, None]
+    t = torch.from_numpy(np.ascontiguousarray(a.transpose(2, 0, 1))[None])
+    return t.to(device=device(), dtype=dt or dtype()).contiguous()
+
+
+def to_hwc(t: torch.Tensor) -> np.ndarray:
+    """(1, C, H, W) device tensor -> (H, W, C) float64 array."""
+    return t[0].permute(1, 2, 0).to(torch.float64).cpu().numpy()
+
+
+def to_dev(a, dt=torch.float64) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a))).to(device=device(), dtype=dt)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
