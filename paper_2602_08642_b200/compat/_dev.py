@@ -59,7 +59,7 @@ def to_hwc(t: torch.Tensor) -> np.ndarray:
 
 
 def to_dev(a, dt=torch.float64) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(a))).to(device=device(), dtype=dt)
+    return torch.from_numpy(np.array(a, copy=True, order="C")).to(device=device(), dtype=dt)
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
