@@ -49,7 +49,11 @@ WORKLOADS = {
            "c3: 1 x 3840x2160, 4-level 7x7 pyramid, bf16 logits, fp32 radiance/accumulate, fwd+bwd"),
     "c2": (64, 256, 256, 4, 5, "f32",
            "c2: 64 x 256x256 crops, 4-level 5x5 pyramid, fp32, fwd+bwd"),
+    "c4b": (1, 4320, 7680, 4, 7, "f32",
+            "c4b: one 7680x4320 frame, 4-level 7x7 pyramid, fp32, forward only; N>1 splits it into "
+            "row bands with a one-round NVLink halo exchange (bands.py)"),
 }
+FWD_ONLY = {"c4b"}
 CPU_SAMPLE = (540, 960, 3, 5)  # per-worker sample of the c4a workload (H, W, L, k)
 
 
@@ -293,21 +297,54 @@ class Runner:
         self.tape_p = C.c_void_p(self.tape.data_ptr())
         self.ws_p = C.c_void_p(self.ws.data_ptr())
 
+    fwd_only = False
+
     def step(self, stream):
         s = C.c_void_p(stream)
         rc = self.lib.ssb_pyr_forward(C.byref(self.desc), C.byref(self.fio), self.tape_p, s)
         if rc:
             self.check(rc, "ssb_pyr_forward")
+        if self.fwd_only:
+            return
         rc = self.lib.ssb_pyr_backward(C.byref(self.desc), C.byref(self.bio), self.tape_p, self.ws_p, s)
         if rc:
             self.check(rc, "ssb_pyr_backward")
 
 
-def launches_per_step(L):
+class BandRunner:
+    """c4b at N > 1: this rank owns one row band of the frame; every step
+    exchanges the halo rows with its neighbours and runs the forward on the
+    extended crop (bands.forward_distributed)."""
+
+    fwd_only = True
+
+    def __init__(self, dist, rank, world, H, W, L, k, dev):
+        import torch
+
+        from paper_2602_08642_b200 import _lib, bands
+        self.lib = _lib.load()
+        self.dist, self.rank, self.world, self.H, self.k = dist, rank, world, H, k
+        b = bands.plan(H, L, k, world)[rank]
+        g = torch.Generator(device=dev).manual_seed(77 + rank)
+        own = [bands.level_rows(b.own, l, H) for l in range(L)]
+        shapes = level_shapes(H, W, L)
+        self.noisy = torch.rand(1, 3, own[0][1] - own[0][0], W, generator=g, device=dev)
+        self.demod = torch.rand(1, 3, own[0][1] - own[0][0], W, generator=g, device=dev) * 0.95 + 0.05
+        self.logits = [torch.randn(1, logit_channels(l, L, k), o[1] - o[0], shapes[l][1], generator=g,
+                                   device=dev) for l, o in enumerate(own)]
+
+    def step(self, stream):
+        from paper_2602_08642_b200 import bands
+        bands.forward_distributed(self.dist, self.rank, self.world, self.H, self.noisy, self.logits,
+                                  self.demod, ksize=self.k)
+
+
+def launches_per_step(L, fwd_only=False):
     # forward: (L-1) pooling + L level kernels; backward: L level kernels + final sweep
     names = [f"pool{l}->{l + 1}" for l in range(L - 1)]
     names += [f"fwd_l{l}" for l in range(L - 1, -1, -1)]
-    names += [f"bwd_l{l}" for l in range(L)] + ["bwd_final"]
+    if not fwd_only:
+        names += [f"bwd_l{l}" for l in range(L)] + ["bwd_final"]
     return names
 
 
@@ -319,7 +356,7 @@ def time_device(runner, steps, warmup, L, dist, world):
     for _ in range(warmup):
         runner.step(sp)
     torch.cuda.synchronize()
-    names = launches_per_step(L)
+    names = launches_per_step(L, runner.fwd_only)
     per = len(names)
     cap = per * steps
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * cap)]
@@ -439,15 +476,20 @@ def gpu_arm(args, rank, world, local_rank, dist):
     if frames_total % world and frames_total > 1:
         raise SystemExit(f"{frames_total} frames do not split over {world} GPUs")
     B = max(1, frames_total // world)
-    noisy, demod, logits, up = synthetic_inputs(B, H, W, L, k, ldt, dev, seed=1234 + rank)
-    runner = Runner(noisy, demod, logits, up, k)
+    fwd_only = args.workload in FWD_ONLY
+    if fwd_only and world > 1:
+        runner = BandRunner(dist, rank, world, H, W, L, k, dev)
+    else:
+        noisy, demod, logits, up = synthetic_inputs(B, H, W, L, k, ldt, dev, seed=1234 + rank)
+        runner = Runner(noisy, demod, logits, up, k)
+        runner.fwd_only = fwd_only
     sampler = ClockSampler(local_rank)
     sampler.start()
     ms, kern, launches = time_device(runner, args.steps, args.warmup, L, dist, world)
     clocks = sampler.stop()
     sl = 2 if ldt == "bf16" else 4
     fwd_b, bwd_b, dom_b = algorithmic_bytes(H, W, L, k, sl, sl)
-    px_total = B * world * H * W
+    px_total = H * W if fwd_only else B * world * H * W
     value = px_total / (ms * 1e-3) / 1e6
     peaks = {}
     try:
@@ -456,11 +498,17 @@ def gpu_arm(args, rank, world, local_rank, dist):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    dom_ms = kern.get("bwd_l0")
+    if fwd_only:
+        lg0 = logit_channels(0, L, k) * sl
+        dom_name, dom_b = "fwd_l0", H * W * (lg0 + 36) // (world if world > 1 else 1)
+        step_bytes = fwd_b
+    else:
+        dom_name, step_bytes = "bwd_l0", fwd_b + bwd_b
+    dom_ms = kern.get(dom_name)
     dom_gbs = dom_b * B / (dom_ms * 1e-3) / 1e9 if dom_ms else None
-    step_gbs = (fwd_b + bwd_b) * B / (ms * 1e-3) / 1e9
+    step_gbs = step_bytes * B / (ms * 1e-3) / 1e9
     res = {
-        "metric": f"pyramidal filter fwd+bwd throughput ({args.workload})",
+        "metric": f"pyramidal filter {'fwd' if fwd_only else 'fwd+bwd'} throughput ({args.workload})",
         "value": round(value, 3),
         "unit": "Mpix/s",
         "n_gpus": world,
@@ -477,7 +525,8 @@ def gpu_arm(args, rank, world, local_rank, dist):
                    "logit_dtype": ldt, "parallelism": f"frame-sharded x{world}, no collective",
                    "l2": "working set >> 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "bwd_l0 (level-0 backward: softmax recompute, "
-                     "logit grads, gather-transpose, upsample-transpose)",
+                     "logit grads, gather-transpose, upsample-transpose)" if not fwd_only else
+                     "fwd_l0 (level-0 forward: softmax, k x k gather, upsample, remod)",
                      "achieved": round(dom_gbs, 1) if dom_gbs else None, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(dom_gbs / peak, 4) if dom_gbs else None, "traffic": None,
@@ -486,7 +535,7 @@ def gpu_arm(args, rank, world, local_rank, dist):
                      "share_of_step": round(dom_ms / ms, 3) if dom_ms else None},
         "step_roofline": {"achieved": round(step_gbs, 1), "peak": peak, "unit": "GB/s",
                           "frac": round(step_gbs / peak, 4),
-                          "bytes_per_frame": {"fwd": fwd_b, "bwd": bwd_b}},
+                          "bytes_per_frame": {"fwd": fwd_b, "bwd": 0 if fwd_only else bwd_b}},
         "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -544,7 +593,7 @@ def main():
     frames_total, H, W, L, k, ldt, _ = WORKLOADS[args.workload]
 
     # e2e through the host-buffer path
-    if not args.no_e2e:
+    if not args.no_e2e and args.workload not in FWD_ONLY:
         B = max(1, frames_total // world)
         del runner
         import torch
@@ -593,6 +642,18 @@ def also_measurements():
                  "step_frac_of_hbm": round((fwd_b + bwd_b) / (ms * 1e-3) / 1e9 / peak, 4),
                  "bwd_l0_frac_of_hbm": round(dom_b / (kern["bwd_l0"] * 1e-3) / 1e9 / peak, 4),
                  "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
+    del noisy, demod, logits, up, r
+    torch.cuda.empty_cache()
+    frames, H, W, L, k, ldt, desc = WORKLOADS["c4b"]
+    noisy, demod, logits, up = synthetic_inputs(1, H, W, L, k, ldt, torch.device("cuda"), seed=98)
+    r = Runner(noisy, demod, logits, up, k)
+    r.fwd_only = True
+    ms, kern, _ = time_device(r, 20, 3, L, None, 1)
+    fwd_b, _, _ = algorithmic_bytes(H, W, L, k, 4, 4)
+    out["c4b"] = {"workload": desc + " (N=1: full frame)", "mpix_s": round(H * W / (ms * 1e-3) / 1e6, 2),
+                  "ms_per_frame": round(ms, 4),
+                  "fwd_frac_of_hbm": round(fwd_b / (ms * 1e-3) / 1e9 / peak, 4),
+                  "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
     return out
 
 
