@@ -3,6 +3,9 @@
 #include <string>
 
 #include "pyr_launch.cuh"
+#include "tma.cuh"
+
+#include <mutex>
 
 namespace ssb {
 
@@ -38,6 +41,45 @@ void launch_end(cudaStream_t s) {
         cudaEventRecord(g_hook.ev[2 * *g_hook.count + 1], s);
         ++*g_hook.count;
     }
+}
+
+// ---- TMA tensor maps (driver entry point fetched once through the runtime) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+bool make_tma_map_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, int esz,
+                     long long W, long long H, long long C, long long B, int box_w, int box_h,
+                     int box_c) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || !base || ((uintptr_t)base & 15)) return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)C, (cuuint64_t)B};
+    const cuuint64_t strides[3] = {(cuuint64_t)(W * esz), (cuuint64_t)(W * H * esz),
+                                   (cuuint64_t)(W * H * C * esz)};
+    for (int i = 0; i < 3; ++i)
+        if (strides[i] % 16 || strides[i] >= (1ull << 40)) return false;
+    if ((box_w * esz) % 16 || box_w > 256 || box_h > 256 || box_c > 256) return false;
+    const cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)box_h, (cuuint32_t)box_c, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, dtype, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }

@@ -37,6 +37,7 @@ struct FwdLevel {
 
 struct BwdLevel {
     int nc, H, W, Hc, Wc;
+    int c0, ctot, batch, nlog;  // channel group start, total channels, batch, logit channels
     int seg_h;
     int want_params;
     int accum;

@@ -3,6 +3,9 @@
 
 #include <string>
 
+#include <type_traits>
+
+#include "pyr_bwd_tma.cuh"
 #include "pyr_kernels.cuh"
 
 namespace ssb {
@@ -33,8 +36,63 @@ void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
     SSB_LAUNCH(s, k_pyr_fwd<K, TL, T, L0, UP, TIED, PREV><<<grid, block, 0, s>>>(a));
 }
 
+inline int pick_segment(int strips, int H, int B) {
+    // keep >= ~8 CTAs per SM of work, amortise the halo rows
+    int seg = 128;
+    while (seg > 16 && (long long)strips * ((H + seg - 1) / seg) * B < 148 * 8) seg >>= 1;
+    return seg;
+}
+
+// TMA-pipelined level backward (fp32 images and logits, no temporal group,
+// demodulated level 0); returns false if the tensors are not TMA-addressable.
+template <int K, bool L0, bool UP, bool TIED>
+bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
+    using SH = TmaShape<K, L0, UP, TIED>;
+    if (L0 && !a0.demod) return false;
+    if (const char* e = getenv("SSB_NO_TMA")) {
+        if (e[0] == '1') return false;
+    }
+    const long long plane = (long long)a0.H * a0.W;
+    auto base = [&](const void* p, long long pl) {
+        return p ? (const void*)((const float*)p - (long long)a0.c0 * pl) : nullptr;
+    };
+    TmaMaps mp;
+    const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    bool ok = make_tma_map_4d(&mp.lg, a0.logits, f32, 4, a0.W, a0.H, a0.nlog, a0.batch, SH::RX,
+                              SH::S, SH::NLOG) &&
+              make_tma_map_4d(&mp.lin, base(a0.lin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                              SH::RX, SH::S, 3) &&
+              make_tma_map_4d(&mp.up, base(a0.gin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                              SH::RX, SH::S, 3);
+    if (ok && L0)
+        ok = make_tma_map_4d(&mp.dem, base(a0.demod, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                             SH::RX, SH::S, 3) &&
+             (!a0.outp || make_tma_map_4d(&mp.out, base(a0.outp, plane), f32, 4, a0.W, a0.H, a0.ctot,
+                                          a0.batch, SH::RX, SH::S + SH::R, 3));
+    if (ok && UP)
+        ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
+                             a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
+    if (!ok) return false;
+    if (L0 && !a0.outp) mp.out = mp.lin;  // out box unused without the demod gradient
+    auto kern = k_pyr_bwd_tma<K, L0, UP, TIED>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        attr_set = true;
+    }
+    BwdLevel a = a0;
+    const int strips = (a.W + SH::TXB - 1) / SH::TXB;
+    a.seg_h = pick_segment(strips, a.H, a.batch);
+    dim3 grid(strips, (a.H + a.seg_h - 1) / a.seg_h, a.batch);
+    SSB_LAUNCH(s, kern<<<grid, 256, SH::SMEM, s>>>(a, mp));
+    return true;
+}
+
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
 void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
+    if constexpr (std::is_same<T, float>::value && std::is_same<TL, float>::value && !PREV) {
+        if (launch_bwd_tma<K, L0, UP, TIED>(a0, s)) return;
+    }
     using SH = BwdShape<K, UP, PREV, T>;
     auto kern = k_pyr_bwd<K, TL, T, L0, UP, TIED, PREV>;
     static bool attr_set = false;
@@ -44,11 +102,8 @@ void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
     }
     BwdLevel a = a0;
     const int strips = (a.W + SH::TXB - 1) / SH::TXB;
-    // segment height: keep >= ~8 CTAs per SM resident work, amortise the halo
-    int seg = 128;
-    while (seg > 16 && (long long)strips * ((a.H + seg - 1) / seg) * B < 148 * 8) seg >>= 1;
-    a.seg_h = seg;
-    dim3 grid(strips, (a.H + seg - 1) / seg, B);
+    a.seg_h = pick_segment(strips, a.H, B);
+    dim3 grid(strips, (a.H + a.seg_h - 1) / a.seg_h, B);
     SSB_LAUNCH(s, kern<<<grid, BWD_THREADS, SH::SMEM, s>>>(a));
 }
 
@@ -181,6 +236,10 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
             a.nc = nc;
             a.H = p.hl[l];
             a.W = p.wl[l];
+            a.c0 = c0;
+            a.ctot = p.C;
+            a.batch = p.B;
+            a.nlog = p.nlog[l];
             const long long e_l = lvl_elems(p, l);
             a.want_params = want ? 1 : 0;
             a.accum = accum;

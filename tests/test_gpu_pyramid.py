@@ -295,3 +295,54 @@ def test_primitives_match_reference(ops):
     np.testing.assert_allclose(planar_to_hwc(ops.softmax_channels(z)), d["nk_wt0"], rtol=1e-13)
     np.testing.assert_allclose(planar_to_hwc(ops.softmax_channels(z, active=29)), d["nk_wf0"],
                                rtol=1e-13, atol=0)
+
+
+TMA_CASES = [  # TMA-eligible shapes (fp32, W % 4 == 0 at every level) incl. edge sizes
+    (8, 16, 2, 5, 3), (1, 32, 2, 5, 3), (3, 8, 2, 3, 3), (70, 64, 3, 5, 3), (130, 128, 4, 7, 3),
+    (64, 96, 3, 5, 6), (37, 256, 3, 5, 3), (96, 64, 3, 3, 5),
+]
+
+
+@pytest.mark.parametrize("h,w,L,k,C", TMA_CASES)
+@pytest.mark.parametrize("want", [True, False])
+def test_tma_path_vs_oracle(ops, h, w, L, k, C, want):
+    """The TMA-pipelined backward (fp32, demod) against the oracle, incl.
+    image smaller than the kernel, single-row frames, two channel groups."""
+    rng = np.random.default_rng(h * 7 + w + C)
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    logits = [f32(z) for z in op.random_logits(h, w, L, k, rng, temporal=False)]
+    noisy = f32(rng.lognormal(-1.0, 1.5, (h, w, C)))
+    dm = f32(rng.uniform(0.0005, 1.0, (h, w, C)))
+    up = f32(rng.normal(size=(h, w, C)))
+    out_r, tape = op.forward(noisy, logits, None, dm, k=k)
+    g_r = op.backward(tape, up, want_param_grads=want)
+    out, t = ops.pyramid_forward(hwc_to_planar(noisy, torch.float32),
+                                 [hwc_to_planar(z, torch.float32) for z in logits],
+                                 hwc_to_planar(dm, torch.float32), ksize=k)
+    g = ops.pyramid_backward(t, hwc_to_planar(up, torch.float32), want_param_grads=want)
+    assert_close(planar_to_hwc(out), out_r, 1e-5)
+    assert_close(planar_to_hwc(g.input), g_r.input, 1e-5)
+    if want:
+        assert_close(planar_to_hwc(g.demod), g_r.demod, 1e-5)
+        floor = 1e-5 * gscale(g_r.logits)
+        for l in range(L):
+            np.testing.assert_allclose(planar_to_hwc(g.logits[l]), g_r.logits[l], rtol=1e-5, atol=floor)
+
+
+def test_tma_and_generic_paths_agree(ops, monkeypatch):
+    """SSB_NO_TMA=1 forces the generic strip walker: both backward kernels
+    agree to fp32 rounding on a 1080p-shaped batch."""
+    torch.manual_seed(3)
+    H, W, L, k = 270, 480, 3, 5
+    noisy = torch.rand(2, 3, H, W, device="cuda")
+    dm = torch.rand(2, 3, H, W, device="cuda") * 0.9 + 0.05
+    lg = [torch.randn(2, ops.logit_channels(l, L, k), h, w, device="cuda")
+          for l, (h, w) in enumerate(ops.level_shapes(H, W, L))]
+    up = torch.randn(2, 3, H, W, device="cuda")
+    _, t = ops.pyramid_forward(noisy, lg, dm, ksize=k)
+    g1 = ops.pyramid_backward(t, up)
+    monkeypatch.setenv("SSB_NO_TMA", "1")
+    g2 = ops.pyramid_backward(t, up)
+    for a_, b_ in [(g1.input, g2.input), (g1.demod, g2.demod)] + list(zip(g1.logits, g2.logits)):
+        scale = b_.abs().max().item()
+        assert (a_ - b_).abs().max().item() <= 2e-5 * scale
