@@ -69,12 +69,14 @@ __device__ __forceinline__ T demod_clamp(T d) { return d > (T)kDemodFloor ? d : 
 // time individual kernels with CUDA events on their own stream.
 void launch_begin(cudaStream_t s);
 void launch_end(cudaStream_t s);
+void launch_debug_check(cudaStream_t s, const char* what);
 
 }  // namespace ssb
 
-#define SSB_LAUNCH(stream, ...)          \
-    do {                                 \
-        ::ssb::launch_begin(stream);     \
-        __VA_ARGS__;                     \
-        ::ssb::launch_end(stream);       \
+#define SSB_LAUNCH(stream, ...)                    \
+    do {                                           \
+        ::ssb::launch_begin(stream);               \
+        __VA_ARGS__;                               \
+        ::ssb::launch_end(stream);                 \
+        ::ssb::launch_debug_check(stream, #__VA_ARGS__); \
     } while (0)

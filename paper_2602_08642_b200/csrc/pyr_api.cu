@@ -1,5 +1,7 @@
 // C ABI of the pyramid filter + the reference's surface primitives.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "pyr_launch.cuh"
@@ -80,6 +82,22 @@ bool make_tma_map_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dty
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// SSB_DEBUG_SYNC=1: synchronise after every launch and report the first
+// failing kernel by name (debugging aid; never set in measurements)
+void launch_debug_check(cudaStream_t s, const char* what) {
+    static const bool on = [] {
+        const char* e = getenv("SSB_DEBUG_SYNC");
+        return e && e[0] == '1';
+    }();
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[ssb] kernel failed: %s\n  -> %s\n", what, cudaGetErrorString(e));
+        fflush(stderr);
+    }
 }
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }

@@ -34,19 +34,26 @@ template <int K, bool L0, bool UP, bool TIED>
 struct TmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
-    static constexpr int S = 4, RX = 64, TXB = RX - 2 * R, TXC = TXB / 2;
+    // TMA boxes must start 16-B aligned in x: smem column 0 is global x0 - RA
+    // (RA = 4), rows are RX = TXB + 8 floats wide, TXB a multiple of 4.
+    static constexpr int RA = 4, S = 4;
+    static constexpr int TXB = ((64 - 2 * R) / 4) * 4, RX = TXB + 2 * RA, RW = TXB + 2 * R;
+    static constexpr int TXC = TXB / 2;
     static constexpr int NPRO = (2 * R + S - 1) / S;  // image-ring blocks above step 0
     static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
     static constexpr int NBU = 3;                      // upstream-ring blocks
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
     static constexpr int FFQ = R >= S ? S * ((R - S + 1 + S - 1) / S) : 0;
     static constexpr int AR = S + 2 * R + FFQ;         // accumulator ring rows
-    static constexpr int CR = 4, CB = 32, CROWS = S / 2 + 1;
-    static constexpr int LGF = NLOG * S * RX;          // floats per logits buffer
-    static constexpr int BLKF = NI * 3 * S * RX;       // floats per image-ring block
-    static constexpr int UPF = 3 * S * RX;
-    static constexpr int OUTF = L0 ? 3 * (S + R) * RX : 0;
-    static constexpr int LHF = UP ? 3 * CROWS * CB : 0;
+    static constexpr int CR = 4, CB = 36, CROWS = S / 2 + 1;  // coarse box: aligned start, TXC + 1 + 2 cols
+    // every TMA destination starts 128-B aligned (sizes rounded up to 32 floats)
+    static constexpr int al32(int n) { return (n + 31) & ~31; }
+    static constexpr int LGF = al32(NLOG * S * RX);    // floats per logits buffer
+    static constexpr int DEMOFF = al32(3 * S * RX);    // demod plane offset inside a ring block
+    static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
+    static constexpr int UPF = al32(3 * S * RX);
+    static constexpr int OUTF = L0 ? al32(3 * (S + R) * RX) : 0;
+    static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
     static constexpr size_t FLOATS = (size_t)2 * LGF + NBL * BLKF + NBU * UPF + OUTF + 2 * LHF +
                                      3 * S * RX + S * RX + AR * 3 * TXB + (UP ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
@@ -57,9 +64,10 @@ __global__ void __launch_bounds__(256, 2)
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
     using SH = TmaShape<K, L0, UP, TIED>;
     constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
+    constexpr int RA = SH::RA, RW = SH::RW;
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
     constexpr int NI = SH::NI, AR = SH::AR, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
-    constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF;
+    constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF;
     constexpr int PL = S * RX;  // floats per image plane in a block
     constexpr int RUP = (R + 1) & ~1;
 
@@ -78,7 +86,8 @@ __global__ void __launch_bounds__(256, 2)
     const int tid = threadIdx.x;
     const int b = blockIdx.z;
     const int nc = a.nc, H = a.H, W = a.W, c0 = a.c0;
-    const int x0 = blockIdx.x * TXB, xr0 = x0 - R;
+    const int x0 = blockIdx.x * TXB, xs0 = x0 - RA;   // xs0: global x of smem column 0
+    const int cxs = (x0 >> 1) & ~3, cxo = (x0 >> 1) - cxs;  // coarse box start (aligned), offset
     const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
     const int qstart = max(y0 - RUP, 0);
     const int qend = min(y1 + R, H);
@@ -90,7 +99,7 @@ __global__ void __launch_bounds__(256, 2)
     // image-ring row r (absolute) -> pointer to plane `which` (0: x0/L, 1: demod), channel 0
     auto lin_row = [&](int r, int which) {
         const int rel = r - qstart - R + NPRO * S;
-        return lin_block(rel / S - NPRO) + (which * 3 * S + (rel % S)) * RX;
+        return lin_block(rel / S - NPRO) + which * DEMOFF + (rel % S) * RX;
     };
     auto up_row = [&](int r) {  // q row r -> upstream ring, channel 0
         const int rel = r - qstart + S;
@@ -103,28 +112,29 @@ __global__ void __launch_bounds__(256, 2)
         const int qs = qstart + j * S;
         uint32_t bytes = (LGF + BLKF + UPF + SH::LHF) * 4;
         mbar_expect_tx(bar, bytes);
-        tma_load_4d(s_lg + (j & 1) * LGF, &mp.lg, xr0, qs, 0, b, bar);
-        tma_load_4d(lin_block(j), &mp.lin, xr0, qs + R, c0, b, bar);
-        if constexpr (L0) tma_load_4d(lin_block(j) + 3 * PL, &mp.dem, xr0, qs + R, c0, b, bar);
-        tma_load_4d(up_block(j), &mp.up, xr0, qs, c0, b, bar);
-        if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, x0 >> 1, qs >> 1, c0, b, bar);
+        tma_load_4d(s_lg + (j & 1) * LGF, &mp.lg, xs0, qs, 0, b, bar);
+        tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
+        if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
+        tma_load_4d(up_block(j), &mp.up, xs0, qs, c0, b, bar);
+        if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
     };
     auto issue_out = [&](int j) {
         if constexpr (L0) {
             mbar_expect_tx(&bars[2], SH::OUTF * 4);
-            tma_load_4d(s_out, &mp.out, xr0, qstart + j * S - R, c0, b, &bars[2]);
+            tma_load_4d(s_out, &mp.out, xs0, qstart + j * S - R, c0, b, &bars[2]);
         }
     };
 
     // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion)
-    const bool col_border = xr0 < 0 || xr0 + RX > W;
+    const bool col_border = xs0 < 0 || xs0 + RX > W;
     auto patch_rows = [&](int r0, int r1) {
         if (col_border) {
             for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
                 const int ri = i % RX, rest = i / RX;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
-                const int src = clampi(xr0 + ri, 0, W - 1) - xr0;
-                if (src != ri) lin_row(r, 0)[pc * PL + ri] = lin_row(r, 0)[pc * PL + src];
+                const int src = clampi(xs0 + ri, 0, W - 1) - xs0;
+                float* row = lin_row(r, pc / 3) + (pc % 3) * PL;
+                if (src != ri) row[ri] = row[src];
             }
             __syncthreads();
         }
@@ -133,7 +143,7 @@ __global__ void __launch_bounds__(256, 2)
                 const int ri = i % RX, rest = i / RX;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
                 const int src = clampi(r, 0, H - 1);
-                if (src != r) lin_row(r, 0)[pc * PL + ri] = lin_row(src, 0)[pc * PL + ri];
+                if (src != r) lin_row(r, pc / 3)[(pc % 3) * PL + ri] = lin_row(src, pc / 3)[(pc % 3) * PL + ri];
             }
             __syncthreads();
         }
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(256, 2)
             float* blk = lin_block(j);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float d = blk[3 * PL + c * PL + s * RX + ri];
+                const float d = blk[DEMOFF + c * PL + s * RX + ri];
                 blk[c * PL + s * RX + ri] *= rcp_dem(demod_clamp(d));
             }
         }
@@ -162,8 +172,8 @@ __global__ void __launch_bounds__(256, 2)
     if (tid == 0) {
         mbar_expect_tx(&bars[3], NPRO * BLKF * 4);
         for (int j = -NPRO; j < 0; ++j) {
-            tma_load_4d(lin_block(j), &mp.lin, xr0, qstart + R + j * S, c0, b, &bars[3]);
-            if constexpr (L0) tma_load_4d(lin_block(j) + 3 * PL, &mp.dem, xr0, qstart + R + j * S, c0, b, &bars[3]);
+            tma_load_4d(lin_block(j), &mp.lin, xs0, qstart + R + j * S, c0, b, &bars[3]);
+            if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qstart + R + j * S, c0, b, &bars[3]);
         }
         if (nsteps > 0) issue_step(0);
         issue_out(0);
@@ -178,7 +188,9 @@ __global__ void __launch_bounds__(256, 2)
 
     int next_flush = max(qstart - R, 0);
     int cnext = qstart >> 1;
-    const int s_a = tid >> 6, ri_a = tid & 63;  // phase A mapping (S x RX = 256)
+    const int s_a = tid >> 6, rw_a = tid & 63;  // phase A: S rows x 64 threads, RW <= 64 used
+    const int ri_a = RA - R + rw_a;               // smem column of this thread's region pixel
+    const bool act_a = rw_a < RW;
 
     for (int i = 0; i < nsteps; ++i) {
         const int qs = qstart + i * S;
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(256, 2)
         mbar_wait(&bars[i & 1], (i >> 1) & 1);
 
         // ------------------------------------------------ A: softmax, G', x0
-        {
+        if (act_a) {
             float e[NLOG];
 #pragma unroll
             for (int t = 0; t < NLOG; ++t) e[t] = lgb[t * PL + s_a * RX + ri_a];
@@ -228,7 +240,7 @@ __global__ void __launch_bounds__(256, 2)
         // ------------------------------------------------ B1: logit gradients
         if (a.want_params && tid < S * TXB) {
             const int s = tid / TXB, xi = tid - s * TXB;
-            const int qy = qs + s, gx = x0 + xi, ri = xi + R;
+            const int qy = qs + s, gx = x0 + xi, ri = xi + RA;
             if (qy >= y0 && qy < y1 && gx < W) {
                 float gq[3];
 #pragma unroll
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(256, 2)
                 }
                 if constexpr (UP) {
                     const float* lh = s_lhc + (i & 1) * SH::LHF;
-                    const int cyb = qs >> 1, cxb = x0 >> 1;
+                    const int cyb = qs >> 1, cxb = cxs;
 #pragma unroll
                     for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(256, 2)
         // ------------------------------------------------ B2: gather transpose
         if (tid < 3 * TXB) {
             const int c = tid / TXB, xi = tid - c * TXB;
-            const int gx = x0 + xi, ri = xi + R;
+            const int gx = x0 + xi, ri = xi + RA;
             if (gx < W) {
                 float acc[S + 2 * R];
 #pragma unroll
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__(256, 2)
                             for (int dx = -R; dx <= R; ++dx) {
                                 const int qx = Pc - dx;
                                 if (qx < 0 || qx >= W) continue;
-                                const int rj = qx - xr0;
+                                const int rj = qx - xs0;
 #pragma unroll
                                 for (int s = 0; s < S; ++s) {
                                     const float g = s_g[c * PL + s * RX + rj];
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(256, 2)
                         for (int k3 = -1; k3 <= 1; ++k3) {
                             const int xx = 2 * X + k3;
                             if (xx < 0 || xx >= W) continue;
-                            const int rj = xx - xr0;
+                            const int rj = xx - xs0;
                             const float g = s_g[c * PL + s * RX + rj];
 #pragma unroll
                             for (int jj = 0; jj < 2; ++jj) {
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(256, 2)
             float* glo = (float*)a.gl_out + (long long)b * a.in_b;
             if constexpr (L0) {
                 float* gdo = a.gdc_out ? (float*)a.gdc_out + (long long)b * a.in_b : nullptr;
-                const int ri = xi + R;
+                const int ri = xi + RA;
                 const float* xr = lin_row(P, 0) + ri;
                 const float* dr = lin_row(P, 1) + ri;
                 const float* ur = up_row(P) + ri;
