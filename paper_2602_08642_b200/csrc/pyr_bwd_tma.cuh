@@ -54,6 +54,11 @@ struct TmaShape {
     static constexpr int UPF = al32(3 * S * RX);
     static constexpr int OUTF = L0 ? al32(3 * (S + R) * RX) : 0;
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
+    // transaction bytes (exact box sizes, not the padded buffer sizes)
+    static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
+    static constexpr uint32_t TX_STEP = NLOG * S * RX * 4 + (NI + 1) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
+    static constexpr uint32_t TX_OUT = 3 * (S + R) * RX * 4;
+    static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr size_t FLOATS = (size_t)2 * LGF + NBL * BLKF + NBU * UPF + OUTF + 2 * LHF +
                                      3 * S * RX + S * RX + AR * 3 * TXB + (UP ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
@@ -110,8 +115,7 @@ __global__ void __launch_bounds__(256, 2)
     auto issue_step = [&](int j) {
         uint64_t* bar = &bars[j & 1];
         const int qs = qstart + j * S;
-        uint32_t bytes = (LGF + BLKF + UPF + SH::LHF) * 4;
-        mbar_expect_tx(bar, bytes);
+        mbar_expect_tx(bar, SH::TX_STEP);
         tma_load_4d(s_lg + (j & 1) * LGF, &mp.lg, xs0, qs, 0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(256, 2)
     };
     auto issue_out = [&](int j) {
         if constexpr (L0) {
-            mbar_expect_tx(&bars[2], SH::OUTF * 4);
+            mbar_expect_tx(&bars[2], SH::TX_OUT);
             tma_load_4d(s_out, &mp.out, xs0, qstart + j * S - R, c0, b, &bars[2]);
         }
     };
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncthreads();
     if (tid == 0) {
-        mbar_expect_tx(&bars[3], NPRO * BLKF * 4);
+        mbar_expect_tx(&bars[3], SH::TX_PRO);
         for (int j = -NPRO; j < 0; ++j) {
             tma_load_4d(lin_block(j), &mp.lin, xs0, qstart + R + j * S, c0, b, &bars[3]);
             if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qstart + R + j * S, c0, b, &bars[3]);
