@@ -100,6 +100,15 @@ __global__ void __launch_bounds__(256, 2)
     const unsigned hw32 = (unsigned)H * (unsigned)W;
     auto slot = [](int P) { return (P + 8 * AR) % AR; };
     auto lin_block = [&](int j) { return s_lin + ((j + 64 * NBL) % NBL) * BLKF; };
+    int sl_i = 0;  // ring slot of the current step's image block (i mod NBL), kept incrementally
+    // image-ring row r for rows of the current step's window [qs - NPRO*S + R, qs + 2S + R)
+    auto lin_row_step = [&](int qs, int r, int which) {
+        const int rel = r - qs - R + NPRO * S;      // >= 0
+        int slt = sl_i - NPRO + (rel >> 2);         // S == 4
+        slt += slt < 0 ? NBL : 0;
+        slt -= slt >= NBL ? NBL : 0;
+        return s_lin + slt * BLKF + which * DEMOFF + (rel & 3) * RX;
+    };
     auto up_block = [&](int j) { return s_up + ((j + 64 * NBU) % NBU) * UPF; };
     // image-ring row r (absolute) -> pointer to plane `which` (0: x0/L, 1: demod), channel 0
     auto lin_row = [&](int r, int which) {
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(256, 2)
     const int ri_a = RA - R + rw_a;               // smem column of this thread's region pixel
     const bool act_a = rw_a < RW;
 
-    for (int i = 0; i < nsteps; ++i) {
+    for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = qstart + i * S;
         float* lgb = s_lg + (i & 1) * LGF;
         if (tid == 0) {
@@ -227,11 +236,11 @@ __global__ void __launch_bounds__(256, 2)
             for (int t = 0; t < NLOG; ++t) lgb[t * PL + s_a * RX + ri_a] = e[t];
             const float inv = __fdividef(1.f, sum);
             s_inv[s_a * RX + ri_a] = inv;
-            convert_block(i, s_a, ri_a);
+            convert_block(i, s_a, ri_a);  // (block i = slot sl_i)
             const float* ub = up_block(i) + s_a * RX + ri_a;
             float dq[3] = {1.f, 1.f, 1.f};
             if constexpr (L0) {
-                const float* dr = lin_row(qs + s_a, 1) + ri_a;
+                const float* dr = lin_row_step(qs, qs + s_a, 1) + ri_a;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dq[c] = demod_clamp(dr[c * PL]);
             }
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(256, 2)
                 float gw[NW];
 #pragma unroll
                 for (int dy = -R; dy <= R; ++dy) {
-                    const float* lr = lin_row(qy + dy, 0) + ri;
+                    const float* lr = lin_row_step(qs, qy + dy, 0) + ri;
 #pragma unroll
                     for (int dx = -R; dx <= R; ++dx) {
                         float acc = 0.f;
@@ -285,7 +294,8 @@ __global__ void __launch_bounds__(256, 2)
                     dot = fmaf(ep[slot_t * PL], gw[t], dot);
                 }
                 const float inner = dot * inv;
-                float* gp = (float*)a.glogits + (long long)b * a.lg_b + ((long long)qy * W + gx);
+                float* const gfb = (float*)a.glogits + (long long)b * a.lg_b;  // uniform per CTA
+                const unsigned po = (unsigned)qy * (unsigned)W + (unsigned)gx;
                 const bool acc_mode = a.accum != 0;
                 float gz[NLOG];
 #pragma unroll
@@ -300,17 +310,18 @@ __global__ void __launch_bounds__(256, 2)
                 }
                 if (acc_mode) {
 #pragma unroll
-                    for (int t = 0; t < NLOG; ++t) gp[t * hw32] += gz[t];
+                    for (int t = 0; t < NLOG; ++t) gfb[po + t * hw32] += gz[t];
                 } else {
 #pragma unroll
-                    for (int t = 0; t < NLOG; ++t) __stcs(gp + t * hw32, gz[t]);
+                    for (int t = 0; t < NLOG; ++t) __stcs(gfb + (po + t * hw32), gz[t]);
                 }
             }
         }
 
         // ------------------------------------------------ B2: gather transpose
-        if (tid < 3 * TXB) {
-            const int c = tid / TXB, xi = tid - c * TXB;
+        if (tid >= 256 - 3 * TXB) {
+            const int u2 = tid - (256 - 3 * TXB);
+            const int c = u2 / TXB, xi = u2 - c * TXB;
             const int gx = x0 + xi, ri = xi + RA;
             if (gx < W) {
                 float acc[S + 2 * R];
@@ -354,20 +365,24 @@ __global__ void __launch_bounds__(256, 2)
         }
         // ------------------------------------------------ B3: upsample transpose
         if constexpr (UP) {
-            if (tid >= 256 - 3 * TXC) {
-                const int u = tid - (256 - 3 * TXC);
+            // B3 items on the threads not running B2 first, then wrap onto the top threads
+            const int nb3 = 256 - 3 * TXB;
+            const int u = tid < nb3 ? tid : (tid >= 256 - (3 * TXC - nb3) ? nb3 + tid - (256 - (3 * TXC - nb3)) : -1);
+            if (u >= 0 && u < 3 * TXC) {
                 const int c = u / TXC, cxi = u - c * TXC;
                 const int X = (x0 >> 1) + cxi;
                 if (X < a.Wc) {
                     float cv[CROWS];
 #pragma unroll
                     for (int k2 = 0; k2 < CROWS; ++k2) cv[k2] = 0.f;
-                    const int cyb = qs >> 1;
+                    const int cyb = qs >> 1;  // qs is even
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
                         const int qy = qs + s;
                         if (qy >= H) break;
-                        const int Y0 = min(qy >> 1, a.Hc - 1) - cyb, Y1 = min((qy + 1) >> 1, a.Hc - 1) - cyb;
+                        // parents: row s/2 (tap i = 0) and (s+1)/2 (tap i = 1), the latter
+                        // clamped onto the last coarse row when it falls off the image
+                        const bool clamp1 = ((qy + 1) >> 1) > a.Hc - 1;
 #pragma unroll
                         for (int k3 = -1; k3 <= 1; ++k3) {
                             const int xx = 2 * X + k3;
@@ -379,8 +394,9 @@ __global__ void __launch_bounds__(256, 2)
                                 if (min((xx + jj) >> 1, a.Wc - 1) != X) continue;
                                 const float w0 = lgb[(TIED ? NT : NT + jj) * PL + s * RX + rj];
                                 const float w1 = lgb[(TIED ? NT : NT + 2 + jj) * PL + s * RX + rj];
-                                cv[Y0] = fmaf(w0, g, cv[Y0]);
-                                cv[Y1] = fmaf(w1, g, cv[Y1]);
+                                cv[s >> 1] = fmaf(w0, g, cv[s >> 1]);
+                                if (clamp1) cv[(s + 1) >> 1 == 0 ? 0 : ((s + 1) >> 1) - 1] = fmaf(w1, g, cv[(s + 1) >> 1 == 0 ? 0 : ((s + 1) >> 1) - 1]);
+                                else cv[(s + 1) >> 1] = fmaf(w1, g, cv[(s + 1) >> 1]);
                             }
                         }
                     }
@@ -428,8 +444,8 @@ __global__ void __launch_bounds__(256, 2)
             if constexpr (L0) {
                 float* gdo = a.gdc_out ? (float*)a.gdc_out + (long long)b * a.in_b : nullptr;
                 const int ri = xi + RA;
-                const float* xr = lin_row(P, 0) + ri;
-                const float* dr = lin_row(P, 1) + ri;
+                const float* xr = lin_row_step(qs, P, 0) + ri;
+                const float* dr = lin_row_step(qs, P, 1) + ri;
                 const float* ur = up_row(P) + ri;
                 const float* orow = s_out + (P - (qs - R)) * RX + ri;
 #pragma unroll
