@@ -58,6 +58,13 @@ __device__ __forceinline__ double softmax_exp(double l, double mk) { return exp(
 __device__ __forceinline__ float sexp(float x) { return ex2_ftz(x * kLog2e); }
 __device__ __forceinline__ double sexp(double x) { return exp(x); }
 
+// fp32 hot paths divide by reciprocal-multiply (MUFU.RCP, <= 2 ulp; exact for
+// the power-of-two pooling counts); fp64 (the parity mode) keeps IEEE division
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
+__device__ __forceinline__ float frcp(float b) { return __fdividef(1.0f, b); }
+__device__ __forceinline__ double frcp(double b) { return 1.0 / b; }
+
 __device__ __forceinline__ float tmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
 

@@ -79,6 +79,25 @@ __device__ __forceinline__ void load_softmax_logits(const TL* __restrict__ lp, u
     for (int t = 0; t < NTM; ++t) e[NT + NUP + t] = ld_logit<T>(lp + (NT + NLUP + t) * hw);
 }
 
+template <typename T, int NT, int NUP, int NLUP, int NTM, typename TL>
+__device__ __forceinline__ void load_softmax_logits_off(const TL* __restrict__ fb, unsigned po,
+                                                        unsigned hw, T* e) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) e[t] = ld_logit<T>(fb + (po + t * hw));
+    if constexpr (NUP > 0) {
+        if constexpr (NLUP == 1) {
+            const T v = ld_logit<T>(fb + (po + NT * hw));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[NT + i] = v;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) e[NT + i] = ld_logit<T>(fb + (po + (NT + i) * hw));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NTM; ++t) e[NT + NUP + t] = ld_logit<T>(fb + (po + (NT + NLUP + t) * hw));
+}
+
 // ===========================================================================
 // Forward level kernel
 // ===========================================================================
@@ -112,15 +131,15 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
         for (int c = 0; c < kMaxCh; ++c) {
             if (c < nc) {
                 T v = lin[c * a.in_c + off];
-                T dc = (T)1;
+                T rd = (T)1;
                 if (dem) {
-                    dc = demod_clamp(dem[c * a.in_c + off]);
-                    v = v / dc;
+                    rd = frcp(demod_clamp(dem[c * a.in_c + off]));
+                    v = v * rd;
                 }
                 s_in[c][ry][rx] = v;
                 if constexpr (PREV) {
                     T p = prv[c * a.in_c + off];
-                    if (dem) p = p / dc;
+                    if (dem) p = p * rd;
                     s_pv[c][ry][rx] = p;
                 }
             }
@@ -133,8 +152,8 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
     T sum = (T)0;
     if (valid) {
         const unsigned hw = (unsigned)H * (unsigned)W;
-        const TL* lg = (const TL*)a.logits + b * a.lg_b + ((long long)y * W + x);
-        load_softmax_logits<T, NT, NUP, NLUP, NTM>(lg, hw, e);
+        const TL* lfb = (const TL*)a.logits + b * a.lg_b;  // uniform per CTA
+        load_softmax_logits_off<T, NT, NUP, NLUP, NTM>(lfb, (unsigned)y * (unsigned)W + (unsigned)x, hw, e);
         T m = e[0];
 #pragma unroll
         for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
@@ -148,7 +167,7 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
     __syncthreads();
     if (!valid) return;
 
-    const T inv = (T)1 / sum;
+    const T inv = frcp(sum);
     const long long off = (long long)y * W + x;
     T* outp = (T*)a.out + b * a.in_b;
     const T* lhc = UP ? (const T*)a.lhat_c + b * a.c_b : nullptr;
@@ -342,7 +361,7 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
                         e[t] = softmax_exp(e[t], mk);
                         sum += e[t];
                     }
-                    const T inv = (T)1 / sum;
+                    const T inv = frcp(sum);
 #pragma unroll
                     for (int t = 0; t < NW; ++t) SW(t, s, ri) = e[t] * inv;
                 } else {
@@ -363,7 +382,7 @@ __global__ void __launch_bounds__(BWD_THREADS, (BwdShape<K, UP, PREV, T>::MINB))
                         SW(t, s, ri) = ev;
                         sum += ev;
                     }
-                    const T inv = (T)1 / sum;
+                    const T inv = frcp(sum);
                     for (int t = 0; t < NW; ++t) SW(t, s, ri) *= inv;
                 }
                 T g[CH];
@@ -670,7 +689,7 @@ __global__ void k_pool2(int nc, int H, int W, const T* __restrict__ in, long lon
     if (X >= Wc || Y >= Hc) return;
     const int yb = 2 * Y, xb = 2 * X;
     const bool hy = yb + 1 < H, hx = xb + 1 < W;
-    const T cnt = (T)((hy ? 2 : 1) * (hx ? 2 : 1));
+    const T rcnt = (hy && hx) ? (T)0.25 : ((hy || hx) ? (T)0.5 : (T)1);  // exact 1/count
     const long long o00 = (long long)yb * W + xb;
     const long long o01 = hx ? o00 + 1 : o00, o10 = hy ? o00 + W : o00, o11 = hy ? o01 + W : o01;
     T v[kMaxCh][4];
@@ -684,10 +703,10 @@ __global__ void k_pool2(int nc, int H, int W, const T* __restrict__ in, long lon
         v[c][3] = p[o11];
         if (dem) {
             const T* d = dem + b * in_b + c * in_c;
-            v[c][0] = v[c][0] / demod_clamp(d[o00]);
-            v[c][1] = v[c][1] / demod_clamp(d[o01]);
-            v[c][2] = v[c][2] / demod_clamp(d[o10]);
-            v[c][3] = v[c][3] / demod_clamp(d[o11]);
+            v[c][0] = fdiv(v[c][0], demod_clamp(d[o00]));
+            v[c][1] = fdiv(v[c][1], demod_clamp(d[o01]));
+            v[c][2] = fdiv(v[c][2], demod_clamp(d[o10]));
+            v[c][3] = fdiv(v[c][3], demod_clamp(d[o11]));
         }
     }
 #pragma unroll
@@ -696,7 +715,7 @@ __global__ void k_pool2(int nc, int H, int W, const T* __restrict__ in, long lon
         // pyramid.py:144 sums the 2x2 block (zeros outside the image), then divides
         const T s01 = hx ? v[c][1] : (T)0, s10 = hy ? v[c][2] : (T)0;
         const T s11 = (hx && hy) ? v[c][3] : (T)0;
-        out[b * out_b + c * out_c + (long long)Y * Wc + X] = ((v[c][0] + s01) + (s10 + s11)) / cnt;
+        out[b * out_b + c * out_c + (long long)Y * Wc + X] = ((v[c][0] + s01) + (s10 + s11)) * rcnt;
     }
 }
 
@@ -740,9 +759,10 @@ __global__ void k_pyr_final(const FinalArgs a) {
         for (int l = top - 1; l >= 0; --l) {
             // children count of the level-(l+1) ancestor, at level l
             const int Y = y >> (l + 1), X = x >> (l + 1);
-            const T cnt = (T)(((2 * Y + 1 < a.dims_h[l]) ? 2 : 1) * ((2 * X + 1 < a.dims_w[l]) ? 2 : 1));
+            const bool hy = 2 * Y + 1 < a.dims_h[l], hx = 2 * X + 1 < a.dims_w[l];
+            const T rcnt = (hy && hx) ? (T)0.25 : ((hy || hx) ? (T)0.5 : (T)1);
 #pragma unroll
-            for (int c = 0; c < kMaxCh; ++c) pb[c] = pb[c] / cnt;
+            for (int c = 0; c < kMaxCh; ++c) pb[c] = pb[c] * rcnt;  // power-of-two count: exact
             if (l == 0) break;
             const T* gl = (const T*)a.gl[l] + b * a.gl_b[l];
             const long long ol = (long long)(y >> l) * a.dims_w[l] + (x >> l);
@@ -774,11 +794,11 @@ __global__ void k_pyr_final(const FinalArgs a) {
         if (c >= a.nc) break;
         const long long o = b * a.in_b + c * a.in_c + off;
         if (dm) {
-            const T dc = demod_clamp(vdem[c]);
-            gn[o] = vn[c] + pb[c] / dc;
+            const T rd = frcp(demod_clamp(vdem[c]));
+            gn[o] = vn[c] + pb[c] * rd;
             if (gd) {
-                const T x0 = vx[c] / dc;
-                const T gdc = vd[c] - pb[c] * x0 / dc;
+                const T x0 = vx[c] * rd;
+                const T gdc = vd[c] - pb[c] * x0 * rd;
                 gd[o] = vdem[c] > (T)kDemodFloor ? gdc : (T)0;
             }
         } else {
