@@ -120,6 +120,15 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * FWD_TX + tx;
     const int nc = a.nc, H = a.H, W = a.W;
 
+    const int x = x0 + tx, y = y0 + ty;
+    const bool valid = (x < W) && (y < H);
+    T e[NW];
+    T sum = (T)0;
+    if (valid) {  // logit loads first: they overlap the image staging below
+        const unsigned hw = (unsigned)H * (unsigned)W;
+        const TL* lfb = (const TL*)a.logits + b * a.lg_b;  // uniform per CTA
+        load_softmax_logits_off<T, NT, NUP, NLUP, NTM>(lfb, (unsigned)y * (unsigned)W + (unsigned)x, hw, e);
+    }
     const T* lin = (const T*)a.lin + b * a.in_b;
     const T* dem = (L0 && a.demod) ? (const T*)a.demod + b * a.in_b : nullptr;
     const T* prv = PREV ? (const T*)a.prev + b * a.in_b : nullptr;
@@ -146,14 +155,7 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
         }
     }
 
-    const int x = x0 + tx, y = y0 + ty;
-    const bool valid = (x < W) && (y < H);
-    T e[NW];
-    T sum = (T)0;
     if (valid) {
-        const unsigned hw = (unsigned)H * (unsigned)W;
-        const TL* lfb = (const TL*)a.logits + b * a.lg_b;  // uniform per CTA
-        load_softmax_logits_off<T, NT, NUP, NLUP, NTM>(lfb, (unsigned)y * (unsigned)W + (unsigned)x, hw, e);
         T m = e[0];
 #pragma unroll
         for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
