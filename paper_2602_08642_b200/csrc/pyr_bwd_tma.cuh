@@ -208,13 +208,6 @@ __global__ void __launch_bounds__(256, 2)
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = qstart + i * S;
         float* lgb = s_lg + (i & 1) * LGF;
-        if (tid == 0) {
-            if (i + 1 < nsteps) {
-                fence_proxy_async();
-                issue_step(i + 1);
-            }
-            if (i > 0) issue_out(i);
-        }
         mbar_wait(&bars[i & 1], (i >> 1) & 1);
 
         // ------------------------------------------------ A: softmax, G', x0
@@ -248,6 +241,15 @@ __global__ void __launch_bounds__(256, 2)
             for (int c = 0; c < 3; ++c) s_g[c * PL + s_a * RX + ri_a] = ub[c * PL] * dq[c] * inv;
         }
         __syncthreads();
+        // every thread has finished the previous step's flush and this step's
+        // phase A: the buffers of step i+1 (and this step's out box) are free
+        if (tid == 0) {
+            if (i + 1 < nsteps) {
+                fence_proxy_async();
+                issue_step(i + 1);
+            }
+            if (i > 0) issue_out(i);
+        }
         if (col_border || qs + R + S > H) patch_rows(qs + R, qs + R + S);
 
         // ------------------------------------------------ B1: logit gradients
@@ -489,7 +491,8 @@ __global__ void __launch_bounds__(256, 2)
             }
             cnext = cend;
         }
-        __syncthreads();
+        // no barrier here: the next phase A touches none of the buffers this
+        // flush reads; the next prefetch is issued after the next phase-A barrier
     }
 }
 

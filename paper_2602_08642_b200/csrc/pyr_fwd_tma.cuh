@@ -1,0 +1,226 @@
+// Level forward, TMA-pipelined row walker (fp32 images + fp32 logits, no
+// temporal group; other configurations use k_pyr_fwd).
+//
+// CTA = column strip of TXF = 64 own columns x one segment of rows, walked in
+// steps of S = 4 rows (256 threads, one own pixel each).  Per step one thread
+// issues, one step ahead, TMA boxes for: the step's logits (TXF x S x C_l),
+// the image rows R ahead of it (x0 = noisy / max(d, 1e-3) at level 0, or the
+// pooled level, landing in a block ring that also keeps the R rows above) and
+// the coarse Lhat rows of the upsample taps.  Then: softmax from smem into
+// registers, in-place demodulation of the new image rows, one barrier, k x k
+// gather + 4 upsample taps, remodulation, store.  One __syncthreads per step.
+#pragma once
+
+#include "pyr_kernels.cuh"
+#include "tma.cuh"
+
+namespace ssb {
+
+struct FwdTmaMaps {
+    CUtensorMap lg;   // logits (W, H, NLOG, B), box (TXF, S, NLOG)
+    CUtensorMap lin;  // noisy (level 0) or L^l, box (RX, S, 3)
+    CUtensorMap dem;  // demod (level 0), box (RX, S, 3)
+    CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
+};
+
+template <int K, bool L0, bool UP, bool TIED>
+struct FwdTmaShape {
+    static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
+    static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
+    static constexpr int S = 4, TXF = 64, RA = 4, RX = TXF + 2 * RA;
+    static constexpr int NPRO = (2 * R + S - 1) / S, NBL = NPRO + 2;
+    static constexpr int NI = L0 ? 2 : 1;
+    static constexpr int CB = 36, CROWS = S / 2 + 1;
+    static constexpr int al32(int n) { return (n + 31) & ~31; }
+    static constexpr int LGF = al32(NLOG * S * TXF);
+    static constexpr int DEMOFF = al32(3 * S * RX);
+    static constexpr int BLKF = NI * DEMOFF;
+    static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
+    static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
+    static constexpr uint32_t TX_STEP = NLOG * S * TXF * 4 + NI * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
+    static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
+    static constexpr size_t FLOATS = (size_t)LGF + NBL * BLKF + 2 * LHF;
+    static constexpr size_t SMEM = FLOATS * 4 + 32;
+    static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
+    static constexpr int MINB = MINB_SMEM > 4 ? 4 : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
+};
+
+template <int K, bool L0, bool UP, bool TIED>
+__global__ void __launch_bounds__(256, (FwdTmaShape<K, L0, UP, TIED>::MINB))
+    k_pyr_fwd_tma(const FwdLevel a, const __grid_constant__ FwdTmaMaps mp) {
+    using SH = FwdTmaShape<K, L0, UP, TIED>;
+    constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S;
+    constexpr int TXF = SH::TXF, RA = SH::RA, RX = SH::RX, NPRO = SH::NPRO, NBL = SH::NBL;
+    constexpr int NI = SH::NI, CB = SH::CB, CROWS = SH::CROWS, LGF = SH::LGF, BLKF = SH::BLKF;
+    constexpr int DEMOFF = SH::DEMOFF, PL = S * RX, LPL = S * TXF;
+
+    extern __shared__ __align__(128) unsigned char smem_ftma[];
+    float* s_lg = reinterpret_cast<float*>(smem_ftma);  // [NLOG][S][TXF]
+    float* s_lin = s_lg + LGF;                           // [NBL][NI][3][S][RX]
+    float* s_lhc = s_lin + NBL * BLKF;                   // [2][3][CROWS][CB]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_ftma + SH::FLOATS * 4);
+
+    const int tid = threadIdx.x;
+    const int b = blockIdx.z;
+    const int H = a.H, W = a.W, c0 = a.c0, nc = a.nc;
+    const int x0 = blockIdx.x * TXF, xs0 = x0 - RA;
+    const int cxs = (x0 >> 1) & ~3;
+    const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
+    const int nsteps = (y1 - y0 + S - 1) / S;
+    const int s_t = tid >> 6, xi = tid & 63;  // own pixel of this thread in a step
+
+    auto lin_block = [&](int j) { return s_lin + ((j + 64 * NBL) % NBL) * BLKF; };
+    int sl_i = 0;  // slot of the current step's image block
+    auto lin_row_step = [&](int qs, int r, int which) {
+        const int rel = r - qs - R + NPRO * S;  // >= 0, S == 4
+        int slt = sl_i - NPRO + (rel >> 2);
+        slt += slt < 0 ? NBL : 0;
+        slt -= slt >= NBL ? NBL : 0;
+        return s_lin + slt * BLKF + which * DEMOFF + (rel & 3) * RX;
+    };
+    auto issue_step = [&](int j) {
+        uint64_t* bar = &bars[0];
+        const int qs = y0 + j * S;
+        mbar_expect_tx(bar, SH::TX_STEP);
+        tma_load_4d(s_lg, &mp.lg, x0, qs, 0, b, bar);
+        tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
+        if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
+        if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
+    };
+    const bool col_border = xs0 < 0 || xs0 + RX > W;
+    // clamp-to-edge patch of image rows [r0, r1) of the ring (after conversion)
+    auto patch_rows = [&](int qs, int r0, int r1) {
+        if (col_border) {
+            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
+                const int ri = i % RX, rest = i / RX;
+                const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
+                const int src = clampi(xs0 + ri, 0, W - 1) - xs0;
+                float* row = lin_row_step(qs, r, pc / 3) + (pc % 3) * PL;
+                if (src != ri) row[ri] = row[src];
+            }
+            __syncthreads();
+        }
+        if (r0 < 0 || r1 > H) {
+            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
+                const int ri = i % RX, rest = i / RX;
+                const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
+                const int src = clampi(r, 0, H - 1);
+                if (src != r)
+                    lin_row_step(qs, r, pc / 3)[(pc % 3) * PL + ri] = lin_row_step(qs, src, pc / 3)[(pc % 3) * PL + ri];
+            }
+            __syncthreads();
+        }
+    };
+    auto convert_rows = [&](float* blk) {  // x0 = noisy / max(d, floor), in place
+        if constexpr (L0) {
+            for (int i = tid; i < S * RX; i += 256) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    blk[c * PL + i] *= frcp(demod_clamp(blk[DEMOFF + c * PL + i]));
+            }
+        }
+    };
+
+    // ---- prologue: image rows [y0 - NPRO*S + R, y0 + R) and step 0
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&bars[1], SH::TX_PRO);
+        for (int j = -NPRO; j < 0; ++j) {
+            tma_load_4d(lin_block(j), &mp.lin, xs0, y0 + R + j * S, c0, b, &bars[1]);
+            if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, y0 + R + j * S, c0, b, &bars[1]);
+        }
+        issue_step(0);
+    }
+    mbar_wait(&bars[1], 0);
+    for (int j = -NPRO; j < 0; ++j) convert_rows(lin_block(j));
+    __syncthreads();
+    sl_i = 0;
+    patch_rows(y0, y0 + R - NPRO * S, y0 + R);
+
+    float* const ofb = (float*)a.out + (long long)b * a.in_b;
+    const unsigned hw32 = (unsigned)H * (unsigned)W;
+
+    for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
+        const int qs = y0 + i * S;
+        mbar_wait(&bars[0], i & 1);
+        // softmax of this thread's own pixel, from smem into registers
+        float e[NW];
+        {
+            float z[NLOG];
+#pragma unroll
+            for (int t = 0; t < NLOG; ++t) z[t] = s_lg[t * LPL + s_t * TXF + xi];
+            float m = z[0];
+#pragma unroll
+            for (int t = 1; t < NLOG; ++t) m = fmaxf(m, z[t]);
+            const float mk = m * kLog2e;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) e[t] = ex2_ftz(fmaf(z[t], kLog2e, -mk));
+            if constexpr (UP) {
+                if constexpr (TIED) {
+                    const float eb = ex2_ftz(fmaf(z[NT], kLog2e, -mk));
+#pragma unroll
+                    for (int t = NT; t < NW; ++t) e[t] = eb;
+                } else {
+#pragma unroll
+                    for (int t = NT; t < NW; ++t) e[t] = ex2_ftz(fmaf(z[t], kLog2e, -mk));
+                }
+            }
+        }
+        convert_rows(lin_block(i));
+        __syncthreads();  // logits consumed, new image rows converted
+        if (tid == 0 && i + 1 < nsteps) {
+            fence_proxy_async();
+            issue_step(i + 1);
+        }
+        if (col_border || qs + R + S > H) patch_rows(qs, qs + R, qs + R + S);
+
+        const int qy = qs + s_t, gx = x0 + xi;
+        if (qy < y1 && gx < W) {
+            float sum = 0.f;
+#pragma unroll
+            for (int t = 0; t < NW; ++t) sum += e[t];
+            const float inv = frcp(sum);
+            float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int dy = -R; dy <= R; ++dy) {
+                const float* lr = lin_row_step(qs, qy + dy, 0) + xi + RA;
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) {
+                    const float wv = e[(dy + R) * K + dx + R];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[c] = fmaf(wv, lr[c * PL + dx], acc[c]);
+                }
+            }
+            if constexpr (UP) {
+                const float* lh = s_lhc + (i & 1) * SH::LHF;
+                const int cyb = qs >> 1;
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const int cy = min((qy + ii) >> 1, a.Hc - 1) - cyb;
+                        const int cx = min((gx + jj) >> 1, a.Wc - 1) - cxs;
+                        const float wv = e[NT + 2 * ii + jj];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) acc[c] = fmaf(wv, lh[(c * CROWS + cy) * CB + cx], acc[c]);
+                    }
+            }
+            const unsigned po = (unsigned)qy * (unsigned)W + (unsigned)gx;
+            const float* dr = L0 ? lin_row_step(qs, qy, 1) + xi + RA : nullptr;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (c >= nc) break;
+                float v = acc[c] * inv;
+                if constexpr (L0) v *= demod_clamp(dr[c * PL]);
+                ofb[po + c * hw32] = v;
+            }
+        }
+    }
+}
+
+}  // namespace ssb

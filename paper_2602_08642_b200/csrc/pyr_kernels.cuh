@@ -24,6 +24,7 @@ constexpr int kMaxCh = 3;  // channels per launch; larger C is split by the host
 
 struct FwdLevel {
     int nc, H, W, Hc, Wc;
+    int c0, ctot, batch, nlog, seg_h;  // channel group start, total channels, batch, logit channels
     const void* logits;
     long long lg_b;  // batch stride of logits (elements)
     const void* lin;  // L^l (l > 0) or noisy (l == 0)

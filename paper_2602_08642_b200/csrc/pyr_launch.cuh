@@ -6,6 +6,7 @@
 #include <type_traits>
 
 #include "pyr_bwd_tma.cuh"
+#include "pyr_fwd_tma.cuh"
 #include "pyr_kernels.cuh"
 
 namespace ssb {
@@ -29,8 +30,53 @@ int make_plan(const ssb_pyr_desc* d, PyrPlan* p);
 
 inline long long lvl_elems(const PyrPlan& p, int l) { return (long long)p.hl[l] * p.wl[l]; }
 
+inline int pick_segment(int strips, int H, int B);
+
+// TMA-pipelined level forward (fp32 images and logits, no temporal group,
+// demodulated level 0); returns false if the tensors are not TMA-addressable.
+template <int K, bool L0, bool UP, bool TIED>
+bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
+    using SH = FwdTmaShape<K, L0, UP, TIED>;
+    if (L0 && !a0.demod) return false;
+    if (const char* e = getenv("SSB_NO_TMA")) {
+        if (e[0] == '1') return false;
+    }
+    const long long plane = (long long)a0.H * a0.W;
+    auto base = [&](const void* p, long long pl) {
+        return p ? (const void*)((const float*)p - (long long)a0.c0 * pl) : nullptr;
+    };
+    FwdTmaMaps mp;
+    const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    bool ok = make_tma_map_4d(&mp.lg, a0.logits, f32, 4, a0.W, a0.H, a0.nlog, a0.batch, SH::TXF,
+                              SH::S, SH::NLOG) &&
+              make_tma_map_4d(&mp.lin, base(a0.lin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                              SH::RX, SH::S, 3);
+    if (ok && L0)
+        ok = make_tma_map_4d(&mp.dem, base(a0.demod, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                             SH::RX, SH::S, 3);
+    if (ok && UP)
+        ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
+                             a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
+    if (!ok) return false;
+    auto kern = k_pyr_fwd_tma<K, L0, UP, TIED>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        attr_set = true;
+    }
+    FwdLevel a = a0;
+    const int strips = (a.W + SH::TXF - 1) / SH::TXF;
+    a.seg_h = pick_segment(strips, a.H, a.batch);
+    dim3 grid(strips, (a.H + a.seg_h - 1) / a.seg_h, a.batch);
+    SSB_LAUNCH(s, kern<<<grid, 256, SH::SMEM, s>>>(a, mp));
+    return true;
+}
+
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
 void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
+    if constexpr (std::is_same<T, float>::value && std::is_same<TL, float>::value && !PREV) {
+        if (launch_fwd_tma<K, L0, UP, TIED>(a, s)) return;
+    }
     dim3 block(FWD_TX, FWD_TY);
     dim3 grid((a.W + FWD_TX - 1) / FWD_TX, (a.H + FWD_TY - 1) / FWD_TY, B);
     SSB_LAUNCH(s, k_pyr_fwd<K, TL, T, L0, UP, TIED, PREV><<<grid, block, 0, s>>>(a));
@@ -191,6 +237,10 @@ int run_forward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_fwd_io* i
             a.nc = nc;
             a.H = p.hl[l];
             a.W = p.wl[l];
+            a.c0 = c0;
+            a.ctot = p.C;
+            a.batch = p.B;
+            a.nlog = p.nlog[l];
             const long long e_l = lvl_elems(p, l);
             a.logits = io->logits[l];
             a.lg_b = (long long)p.nlog[l] * e_l;
