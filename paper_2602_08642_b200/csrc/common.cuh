@@ -40,6 +40,19 @@ __device__ __forceinline__ void st_glogit(__nv_bfloat16* p, float v, bool acc) {
     *p = __float2bfloat16_rn(v);
 }
 
+// ---- shared-memory logit staging (TMA boxes keep the storage type)
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+// gradient of one logit into the storage type, streaming (written once)
+__device__ __forceinline__ void st_gz(float* p, float v, bool acc) {
+    if (acc) *p += v;
+    else __stcs(p, v);
+}
+__device__ __forceinline__ void st_gz(__nv_bfloat16* p, float v, bool acc) {
+    if (acc) v += __bfloat162float(*p);
+    __stcs(reinterpret_cast<unsigned short*>(p), __bfloat16_as_ushort(__float2bfloat16_rn(v)));
+}
+
 // ---- exponentials ---------------------------------------------------------
 // fp32: MUFU.EX2 with flush-to-zero (arguments are <= 0 after the max
 // subtraction; weights below 2^-126 are irrelevant), the max subtraction folded

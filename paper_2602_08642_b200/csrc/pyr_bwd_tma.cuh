@@ -1,5 +1,6 @@
-// Level backward, TMA-pipelined strip walker (fp32 images + fp32 logits, no
-// temporal group; other configurations use k_pyr_bwd in pyr_kernels.cuh).
+// Level backward, TMA-pipelined strip walker (fp32 images, fp32 or bf16
+// logits, no temporal group; other configurations use k_pyr_bwd in
+// pyr_kernels.cuh).
 //
 // Same column-strip / S-row-step structure and the same arithmetic as
 // k_pyr_bwd, with the data movement rebuilt for sm_100a:
@@ -30,14 +31,17 @@ struct TmaMaps {
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
 };
 
-template <int K, bool L0, bool UP, bool TIED>
+template <int K, typename TL, bool L0, bool UP, bool TIED>
 struct TmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
     // TMA boxes must start 16-B aligned in x: smem column 0 is global x0 - RA
-    // (RA = 4), rows are RX = TXB + 8 floats wide, TXB a multiple of 4.
-    static constexpr int RA = 4, S = 4;
-    static constexpr int TXB = ((64 - 2 * R) / 4) * 4, RX = TXB + 2 * RA, RW = TXB + 2 * R;
+    // with RA = 16 B of logits (4 fp32 / 8 bf16), rows are RX = TXB + 2 RA
+    // wide, TXB a multiple of RA.
+    static constexpr int LGE = (int)sizeof(TL);  // logit element size
+    static constexpr bool SEP = LGE != 4;        // bf16: staging box + separate fp32 exponentials
+    static constexpr int RA = 16 / LGE, S = 4;
+    static constexpr int TXB = ((64 - 2 * R) / RA) * RA, RX = TXB + 2 * RA, RW = TXB + 2 * R;
     static constexpr int TXC = TXB / 2;
     static constexpr int NPRO = (2 * R + S - 1) / S;  // image-ring blocks above step 0
     static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
@@ -48,7 +52,11 @@ struct TmaShape {
     static constexpr int CR = 4, CB = 36, CROWS = S / 2 + 1;  // coarse box: aligned start, TXC + 1 + 2 cols
     // every TMA destination starts 128-B aligned (sizes rounded up to 32 floats)
     static constexpr int al32(int n) { return (n + 31) & ~31; }
-    static constexpr int LGF = al32(NLOG * S * RX);    // floats per logits buffer
+    static constexpr int LGF = al32(NLOG * S * RX);    // floats per exponentials buffer
+    // logits staging (storage type): fp32 = the two exponential buffers
+    // themselves (in place); bf16 = one staging box + one fp32 buffer
+    static constexpr int LGS = SEP ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
+    static constexpr int LGBUF = SEP ? LGF + LGS : 2 * LGF;
     static constexpr int DEMOFF = al32(3 * S * RX);    // demod plane offset inside a ring block
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
     static constexpr int UPF = al32(3 * S * RX);
@@ -56,18 +64,19 @@ struct TmaShape {
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
-    static constexpr uint32_t TX_STEP = NLOG * S * RX * 4 + (NI + 1) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
+    static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 1) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
     static constexpr uint32_t TX_OUT = 3 * (S + R) * RX * 4;
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
-    static constexpr size_t FLOATS = (size_t)2 * LGF + NBL * BLKF + NBU * UPF + OUTF + 2 * LHF +
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + NBU * UPF + OUTF + 2 * LHF +
                                      3 * S * RX + S * RX + AR * 3 * TXB + (UP ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
 };
 
-template <int K, bool L0, bool UP, bool TIED>
+template <int K, typename TL, bool L0, bool UP, bool TIED>
 __global__ void __launch_bounds__(256, 2)
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
-    using SH = TmaShape<K, L0, UP, TIED>;
+    using SH = TmaShape<K, TL, L0, UP, TIED>;
+    constexpr bool SEP = SH::SEP;
     constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
     constexpr int RA = SH::RA, RW = SH::RW;
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
@@ -77,8 +86,8 @@ __global__ void __launch_bounds__(256, 2)
     constexpr int RUP = (R + 1) & ~1;
 
     extern __shared__ __align__(128) unsigned char smem_tma[];
-    float* s_lg = reinterpret_cast<float*>(smem_tma);  // [2][NLOG][S][RX]
-    float* s_lin = s_lg + 2 * LGF;                     // [NBL][NI][3][S][RX]
+    float* s_lg = reinterpret_cast<float*>(smem_tma);  // [2][NLOG][S][RX] | [NLOG][S][RX] + staging
+    float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RX]
     float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]
     float* s_out = s_up + NBU * UPF;                   // [3][S+R][RX]
     float* s_lhc = s_out + SH::OUTF;                   // [2][3][CROWS][CB]
@@ -125,7 +134,7 @@ __global__ void __launch_bounds__(256, 2)
         uint64_t* bar = &bars[j & 1];
         const int qs = qstart + j * S;
         mbar_expect_tx(bar, SH::TX_STEP);
-        tma_load_4d(s_lg + (j & 1) * LGF, &mp.lg, xs0, qs, 0, b, bar);
+        tma_load_4d(SEP ? s_lg + LGF : s_lg + (j & 1) * LGF, &mp.lg, xs0, qs, 0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
         tma_load_4d(up_block(j), &mp.up, xs0, qs, c0, b, bar);
@@ -207,14 +216,15 @@ __global__ void __launch_bounds__(256, 2)
 
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = qstart + i * S;
-        float* lgb = s_lg + (i & 1) * LGF;
+        float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
+        const TL* lgs = reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb);  // staged logits
         mbar_wait(&bars[i & 1], (i >> 1) & 1);
 
         // ------------------------------------------------ A: softmax, G', x0
         if (act_a) {
             float e[NLOG];
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) e[t] = lgb[t * PL + s_a * RX + ri_a];
+            for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PL + s_a * RX + ri_a]);
             float m = e[0];
 #pragma unroll
             for (int t = 1; t < NLOG; ++t) m = fmaxf(m, e[t]);
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(256, 2)
                     dot = fmaf(ep[slot_t * PL], gw[t], dot);
                 }
                 const float inner = dot * inv;
-                float* const gfb = (float*)a.glogits + (long long)b * a.lg_b;  // uniform per CTA
+                TL* const gfb = (TL*)a.glogits + (long long)b * a.lg_b;  // uniform per CTA
                 const unsigned po = (unsigned)qy * (unsigned)W + (unsigned)gx;
                 const bool acc_mode = a.accum != 0;
                 float gz[NLOG];
@@ -310,13 +320,8 @@ __global__ void __launch_bounds__(256, 2)
                         for (int t = NT; t < NW; ++t) gz[t] = ep[t * PL] * (gw[t] - inner);
                     }
                 }
-                if (acc_mode) {
 #pragma unroll
-                    for (int t = 0; t < NLOG; ++t) gfb[po + t * hw32] += gz[t];
-                } else {
-#pragma unroll
-                    for (int t = 0; t < NLOG; ++t) __stcs(gfb + (po + t * hw32), gz[t]);
-                }
+                for (int t = 0; t < NLOG; ++t) st_gz(gfb + (po + t * hw32), gz[t], acc_mode);
             }
         }
 

@@ -1,5 +1,5 @@
-// Level forward, TMA-pipelined row walker (fp32 images + fp32 logits, no
-// temporal group; other configurations use k_pyr_fwd).
+// Level forward, TMA-pipelined row walker (fp32 images, fp32 or bf16 logits,
+// no temporal group; other configurations use k_pyr_fwd).
 //
 // CTA = column strip of TXF = 64 own columns x one segment of rows, walked in
 // steps of S = 4 rows (256 threads, one own pixel each).  Per step one thread
@@ -23,7 +23,7 @@ struct FwdTmaMaps {
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
 };
 
-template <int K, bool L0, bool UP, bool TIED>
+template <int K, typename TL, bool L0, bool UP, bool TIED>
 struct FwdTmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
@@ -32,12 +32,13 @@ struct FwdTmaShape {
     static constexpr int NI = L0 ? 2 : 1;
     static constexpr int CB = 36, CROWS = S / 2 + 1;
     static constexpr int al32(int n) { return (n + 31) & ~31; }
-    static constexpr int LGF = al32(NLOG * S * TXF);
+    static constexpr int LGE = (int)sizeof(TL);          // logit element size (4 or 2)
+    static constexpr int LGF = al32((NLOG * S * TXF * LGE + 3) / 4);  // floats per logits buffer
     static constexpr int DEMOFF = al32(3 * S * RX);
     static constexpr int BLKF = NI * DEMOFF;
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
-    static constexpr uint32_t TX_STEP = NLOG * S * TXF * 4 + NI * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
+    static constexpr uint32_t TX_STEP = NLOG * S * TXF * LGE + NI * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr size_t FLOATS = (size_t)LGF + NBL * BLKF + 2 * LHF;
     static constexpr size_t SMEM = FLOATS * 4 + 32;
@@ -45,18 +46,18 @@ struct FwdTmaShape {
     static constexpr int MINB = MINB_SMEM > 4 ? 4 : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
 };
 
-template <int K, bool L0, bool UP, bool TIED>
-__global__ void __launch_bounds__(256, (FwdTmaShape<K, L0, UP, TIED>::MINB))
+template <int K, typename TL, bool L0, bool UP, bool TIED>
+__global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
     k_pyr_fwd_tma(const FwdLevel a, const __grid_constant__ FwdTmaMaps mp) {
-    using SH = FwdTmaShape<K, L0, UP, TIED>;
+    using SH = FwdTmaShape<K, TL, L0, UP, TIED>;
     constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S;
     constexpr int TXF = SH::TXF, RA = SH::RA, RX = SH::RX, NPRO = SH::NPRO, NBL = SH::NBL;
     constexpr int NI = SH::NI, CB = SH::CB, CROWS = SH::CROWS, LGF = SH::LGF, BLKF = SH::BLKF;
     constexpr int DEMOFF = SH::DEMOFF, PL = S * RX, LPL = S * TXF;
 
     extern __shared__ __align__(128) unsigned char smem_ftma[];
-    float* s_lg = reinterpret_cast<float*>(smem_ftma);  // [NLOG][S][TXF]
-    float* s_lin = s_lg + LGF;                           // [NBL][NI][3][S][RX]
+    const TL* s_lg = reinterpret_cast<const TL*>(smem_ftma);  // [NLOG][S][TXF]
+    float* s_lin = reinterpret_cast<float*>(smem_ftma) + LGF;                          // [NBL][NI][3][S][RX]
     float* s_lhc = s_lin + NBL * BLKF;                   // [2][3][CROWS][CB]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_ftma + SH::FLOATS * 4);
 
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, L0, UP, TIED>::MINB))
         uint64_t* bar = &bars[0];
         const int qs = y0 + j * S;
         mbar_expect_tx(bar, SH::TX_STEP);
-        tma_load_4d(s_lg, &mp.lg, x0, qs, 0, b, bar);
+        tma_load_4d((void*)s_lg, &mp.lg, x0, qs, 0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
         if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, L0, UP, TIED>::MINB))
         {
             float z[NLOG];
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) z[t] = s_lg[t * LPL + s_t * TXF + xi];
+            for (int t = 0; t < NLOG; ++t) z[t] = to_f32(s_lg[t * LPL + s_t * TXF + xi]);
             float m = z[0];
 #pragma unroll
             for (int t = 1; t < NLOG; ++t) m = fmaxf(m, z[t]);

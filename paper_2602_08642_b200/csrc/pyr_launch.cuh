@@ -32,11 +32,17 @@ inline long long lvl_elems(const PyrPlan& p, int l) { return (long long)p.hl[l] 
 
 inline int pick_segment(int strips, int H, int B);
 
-// TMA-pipelined level forward (fp32 images and logits, no temporal group,
-// demodulated level 0); returns false if the tensors are not TMA-addressable.
-template <int K, bool L0, bool UP, bool TIED>
+template <typename TL>
+constexpr CUtensorMapDataType tma_dtype() {
+    return sizeof(TL) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+}
+
+// TMA-pipelined level forward (fp32 images, fp32/bf16 logits, no temporal
+// group, demodulated level 0); returns false if the tensors are not
+// TMA-addressable.
+template <int K, typename TL, bool L0, bool UP, bool TIED>
 bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
-    using SH = FwdTmaShape<K, L0, UP, TIED>;
+    using SH = FwdTmaShape<K, TL, L0, UP, TIED>;
     if (L0 && !a0.demod) return false;
     if (const char* e = getenv("SSB_NO_TMA")) {
         if (e[0] == '1') return false;
@@ -47,8 +53,8 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
     };
     FwdTmaMaps mp;
     const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    bool ok = make_tma_map_4d(&mp.lg, a0.logits, f32, 4, a0.W, a0.H, a0.nlog, a0.batch, SH::TXF,
-                              SH::S, SH::NLOG) &&
+    bool ok = make_tma_map_4d(&mp.lg, a0.logits, tma_dtype<TL>(), sizeof(TL), a0.W, a0.H, a0.nlog,
+                              a0.batch, SH::TXF, SH::S, SH::NLOG) &&
               make_tma_map_4d(&mp.lin, base(a0.lin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
                               SH::RX, SH::S, 3);
     if (ok && L0)
@@ -58,7 +64,7 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
         ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
     if (!ok) return false;
-    auto kern = k_pyr_fwd_tma<K, L0, UP, TIED>;
+    auto kern = k_pyr_fwd_tma<K, TL, L0, UP, TIED>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
@@ -74,8 +80,8 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
 
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
 void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
-    if constexpr (std::is_same<T, float>::value && std::is_same<TL, float>::value && !PREV) {
-        if (launch_fwd_tma<K, L0, UP, TIED>(a, s)) return;
+    if constexpr (std::is_same<T, float>::value && !std::is_same<TL, double>::value && !PREV) {
+        if (launch_fwd_tma<K, TL, L0, UP, TIED>(a, s)) return;
     }
     dim3 block(FWD_TX, FWD_TY);
     dim3 grid((a.W + FWD_TX - 1) / FWD_TX, (a.H + FWD_TY - 1) / FWD_TY, B);
@@ -89,11 +95,12 @@ inline int pick_segment(int strips, int H, int B) {
     return seg;
 }
 
-// TMA-pipelined level backward (fp32 images and logits, no temporal group,
-// demodulated level 0); returns false if the tensors are not TMA-addressable.
-template <int K, bool L0, bool UP, bool TIED>
+// TMA-pipelined level backward (fp32 images, fp32/bf16 logits, no temporal
+// group, demodulated level 0); returns false if the tensors are not
+// TMA-addressable.
+template <int K, typename TL, bool L0, bool UP, bool TIED>
 bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
-    using SH = TmaShape<K, L0, UP, TIED>;
+    using SH = TmaShape<K, TL, L0, UP, TIED>;
     if (L0 && !a0.demod) return false;
     if (const char* e = getenv("SSB_NO_TMA")) {
         if (e[0] == '1') return false;
@@ -104,8 +111,8 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
     };
     TmaMaps mp;
     const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    bool ok = make_tma_map_4d(&mp.lg, a0.logits, f32, 4, a0.W, a0.H, a0.nlog, a0.batch, SH::RX,
-                              SH::S, SH::NLOG) &&
+    bool ok = make_tma_map_4d(&mp.lg, a0.logits, tma_dtype<TL>(), sizeof(TL), a0.W, a0.H, a0.nlog,
+                              a0.batch, SH::RX, SH::S, SH::NLOG) &&
               make_tma_map_4d(&mp.lin, base(a0.lin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
                               SH::RX, SH::S, 3) &&
               make_tma_map_4d(&mp.up, base(a0.gin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
@@ -120,7 +127,7 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
     if (!ok) return false;
     if (L0 && !a0.outp) mp.out = mp.lin;  // out box unused without the demod gradient
-    auto kern = k_pyr_bwd_tma<K, L0, UP, TIED>;
+    auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
@@ -136,8 +143,8 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
 
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
 void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
-    if constexpr (std::is_same<T, float>::value && std::is_same<TL, float>::value && !PREV) {
-        if (launch_bwd_tma<K, L0, UP, TIED>(a0, s)) return;
+    if constexpr (std::is_same<T, float>::value && !std::is_same<TL, double>::value && !PREV) {
+        if (launch_bwd_tma<K, TL, L0, UP, TIED>(a0, s)) return;
     }
     using SH = BwdShape<K, UP, PREV, T>;
     auto kern = k_pyr_bwd<K, TL, T, L0, UP, TIED, PREV>;
