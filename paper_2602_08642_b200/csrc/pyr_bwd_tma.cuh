@@ -1,21 +1,34 @@
 // Level backward, TMA-pipelined strip walker (fp32 images, fp32 or bf16
 // logits, no temporal group; other configurations use k_pyr_bwd in
-// pyr_kernels.cuh).
+// pyr_kernels.cuh).  Reference: reconstruct_backward (pyramid.py:362-455).
 //
-// Same column-strip / S-row-step structure and the same arithmetic as
-// k_pyr_bwd, with the data movement rebuilt for sm_100a:
-//  * every global input of a step arrives by cp.async.bulk.tensor (TMA) into
-//    shared memory, issued by one thread one step ahead (double-buffered
-//    logits, block rings for the image rows), completion on mbarriers --
-//    no per-thread address math, no load latency on the critical path,
-//    out-of-image texels arrive as zeros (clamp-to-edge is patched in smem);
-//  * the softmax is not normalised per weight: s_g holds G * (1/sum) and the
-//    softmax backward is rewritten in terms of the exponentials;
-//  * the gather-transpose (B2) and upsample-transpose (B3) run one thread per
-//    (column, channel) over the S rows with register accumulators, so one
-//    accumulator ring suffices.
-// ~104 KB shared memory at k = 5 -> 2 CTAs (16 warps) per SM.
+// CTA = column strip of TXB own columns (+R halo columns each side) x one
+// segment of rows, walked in steps of S = 4 rows.  Data movement: every
+// global input of a step (logits, image rows R ahead, upstream, forward
+// output, coarse Lhat rows) arrives by cp.async.bulk.tensor into shared
+// memory, issued by one thread one step ahead, completion on mbarriers;
+// out-of-image texels arrive as zeros (clamp-to-edge is patched in smem).
+//
+// Per step, with w = e * inv the softmax of the pixel's logits:
+//  A  (all warps) exponentials e, G = gout * inv, and the softmax backward's
+//     inner product from the level output the tape already holds:
+//        sum_t w_t gw_t = sum_c gout_c * y_c(q)   (y = the level output),
+//     inner' = inv * sum_c gin_c out_c (level 0: gin = upstream, out = the
+//     remodulated output; level l: gin = ghat^l, out = Lhat^l).  So every
+//     tap's logit gradient is final as soon as its gw is known:
+//        g_logit_t = e_t * (sum_c G_c x_c(q + o_t) - inner').
+//  Then the warps split by role (one loop each, CTA barriers in step):
+//  B1 (warps 0-3) logit gradients, one thread per horizontal pixel PAIR
+//     (float2 shared loads, FFMA2 over tap pairs, paired streaming stores),
+//     and the upsample transpose (B3) separably per coarse column.
+//  B2 (warps 4-7) gather-transpose, one thread per (column, group of tap
+//     columns) with a register window of the S + 2R output rows the step
+//     touches; finished rows are reduced across the groups with warp
+//     shuffles and written directly (level 0: partial g_noisy and g_demod) --
+//     no accumulator ring in shared memory, no atomics, deterministic.
 #pragma once
+
+#include <type_traits>
 
 #include "pyr_kernels.cuh"
 #include "tma.cuh"
@@ -27,7 +40,7 @@ struct TmaMaps {
     CUtensorMap lin;  // noisy (level 0) or L^l, box (RX, S, 3)
     CUtensorMap dem;  // demod (level 0), box (RX, S, 3)
     CUtensorMap up;   // upstream (level 0) or ghat^l, box (RX, S, 3)
-    CUtensorMap out;  // forward output (level 0), box (RX, S + R, 3)
+    CUtensorMap out;  // forward output (level 0) or Lhat^l, box (RX, S, 3)
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
 };
 
@@ -37,18 +50,27 @@ struct TmaShape {
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
     // TMA boxes must start 16-B aligned in x: smem column 0 is global x0 - RA
     // with RA = 16 B of logits (4 fp32 / 8 bf16), rows are RX = TXB + 2 RA
-    // wide, TXB a multiple of RA.
+    // wide, TXB a multiple of RA.  k = 7 uses narrower strips (shared memory).
     static constexpr int LGE = (int)sizeof(TL);  // logit element size
     static constexpr bool SEP = LGE != 4;        // bf16: staging box + separate fp32 exponentials
     static constexpr int RA = 16 / LGE, S = 4;
-    static constexpr int TXB = ((64 - 2 * R) / RA) * RA, RX = TXB + 2 * RA, RW = TXB + 2 * R;
-    static constexpr int TXC = TXB / 2;
+    static constexpr int TXW = ((64 - 2 * R) / RA) * RA;
+    static constexpr int TXB = K >= 7 ? 32 : TXW, RX = TXB + 2 * RA, RW = TXB + 2 * R;
+    static constexpr int TXC = TXB / 2, NPAIR = TXB / 2;
     static constexpr int NPRO = (2 * R + S - 1) / S;  // image-ring blocks above step 0
     static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
-    static constexpr int NBU = 3;                      // upstream-ring blocks
+    // upstream ring (level 0: the flush needs u * out, R rows behind); other
+    // levels and the forward output / Lhat^l: one block (read in phase A only)
+    static constexpr int NBU = L0 ? (R + S - 1) / S + 2 : 1;
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
-    static constexpr int FFQ = R >= S ? S * ((R - S + 1 + S - 1) / S) : 0;
-    static constexpr int AR = S + 2 * R + FFQ;         // accumulator ring rows
+    // B1: S * NPAIR pixel pairs on warps 0-3; tap rows split in B1SPL warp-uniform parts
+    static constexpr int NB1 = S * NPAIR;
+    static constexpr int B1SPL = NB1 <= 64 ? 2 : 1;
+    static constexpr int B1ITEMS = 128 / B1SPL;
+    static constexpr int DYS = (K + B1SPL - 1) / B1SPL;  // tap rows per part
+    // B2: TXB columns x B2SPL tap-column groups on warps 4-7 (adjacent lanes)
+    static constexpr int B2SPL = TXB * 4 <= 128 ? 4 : (TXB * 2 <= 128 ? 2 : 1);
+    static constexpr int AW = S + 2 * R, NPW = (AW + 1) / 2;  // output-row window (float2 pairs)
     static constexpr int CR = 4, CB = 36, CROWS = S / 2 + 1;  // coarse box: aligned start, TXC + 1 + 2 cols
     // every TMA destination starts 128-B aligned (sizes rounded up to 32 floats)
     static constexpr int al32(int n) { return (n + 31) & ~31; }
@@ -59,55 +81,88 @@ struct TmaShape {
     static constexpr int LGBUF = SEP ? LGF + LGS : 2 * LGF;
     static constexpr int DEMOFF = al32(3 * S * RX);    // demod plane offset inside a ring block
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
-    static constexpr int UPF = al32(3 * S * RX);
-    static constexpr int OUTF = L0 ? al32(3 * (S + R) * RX) : 0;
+    static constexpr int UPF = al32(3 * S * RX);       // floats per upstream / output block
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
-    static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 1) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
-    static constexpr uint32_t TX_OUT = 3 * (S + R) * RX * 4;
+    static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + NBU * UPF + OUTF + 2 * LHF +
-                                     3 * S * RX + S * RX + AR * 3 * TXB + (UP ? CR * 3 * TXC : 0);
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + 1) * UPF + 2 * LHF +
+                                     3 * S * RX + S * RX + (UP ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
+    static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
+    static_assert(TXB * B2SPL <= 128 && TXC <= 128, "B2/B3 items exceed their warps");
+    static_assert(S * RW <= 256 && RW <= 64, "phase A items exceed the CTA");
+    static_assert(S == 4 && (32 % B2SPL) == 0, "step geometry");
 };
+
+// paired gradient store (two horizontally adjacent pixels, 8-B / 4-B aligned)
+template <bool ACC>
+__device__ __forceinline__ void st_gz2(float* p, float a, float b) {
+    float2* q = reinterpret_cast<float2*>(p);
+    if constexpr (ACC) {
+        float2 o = *q;
+        o.x += a;
+        o.y += b;
+        *q = o;
+    } else {
+        __stcs(q, make_float2(a, b));
+    }
+}
+template <bool ACC>
+__device__ __forceinline__ void st_gz2(__nv_bfloat16* p, float a, float b) {
+    __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(p);
+    if constexpr (ACC) {
+        const float2 o = __bfloat1622float2(*q);
+        a += o.x;
+        b += o.y;
+    }
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    __stcs(reinterpret_cast<unsigned*>(q), *reinterpret_cast<const unsigned*>(&v));
+}
+
+__device__ __forceinline__ float rcp_fast(float x) {  // MUFU.RCP (x >= 1e-3 here)
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0, 256;" ::: "memory"); }
 
 template <int K, typename TL, bool L0, bool UP, bool TIED>
 __global__ void __launch_bounds__(256, 2)
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
     using SH = TmaShape<K, TL, L0, UP, TIED>;
     constexpr bool SEP = SH::SEP;
-    constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
-    constexpr int RA = SH::RA, RW = SH::RW;
+    constexpr int R = SH::R, NT = SH::NT, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
+    constexpr int RA = SH::RA, RW = SH::RW, NPAIR = SH::NPAIR;
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
-    constexpr int NI = SH::NI, AR = SH::AR, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
+    constexpr int NI = SH::NI, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
     constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF;
+    constexpr int B1SPL = SH::B1SPL, B2SPL = SH::B2SPL, AW = SH::AW, NPW = SH::NPW;
     constexpr int PL = S * RX;  // floats per image plane in a block
     constexpr int RUP = (R + 1) & ~1;
 
     extern __shared__ __align__(128) unsigned char smem_tma[];
     float* s_lg = reinterpret_cast<float*>(smem_tma);  // [2][NLOG][S][RX] | [NLOG][S][RX] + staging
     float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RX]
-    float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]
-    float* s_out = s_up + NBU * UPF;                   // [3][S+R][RX]
-    float* s_lhc = s_out + SH::OUTF;                   // [2][3][CROWS][CB]
-    float* s_g = s_lhc + 2 * SH::LHF;                  // [3][S][RX]  G * (1/sum)
-    float* s_inv = s_g + 3 * PL;                       // [S][RX]
-    float* s_acc = s_inv + PL;                         // [AR][3][TXB]
-    float* s_cac = s_acc + AR * 3 * TXB;               // [CR][3][TXC]
+    float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]  (level 0: u * out after A)
+    float* s_ob = s_up + NBU * UPF;                    // [3][S][RX]  forward output / Lhat^l
+    float* s_lhc = s_ob + UPF;                         // [2][3][CROWS][CB]
+    float* s_g = s_lhc + 2 * SH::LHF;                  // [3][S][RX]  G = gout / sum
+    float* s_inn = s_g + 3 * PL;                       // [S][RX]     inner' = sum_c gin_c out_c / sum
+    float* s_cac = s_inn + PL;                         // [CR][3][TXC] coarse ghat accumulators
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
 
     const int tid = threadIdx.x;
     const int b = blockIdx.z;
     const int nc = a.nc, H = a.H, W = a.W, c0 = a.c0;
     const int x0 = blockIdx.x * TXB, xs0 = x0 - RA;   // xs0: global x of smem column 0
-    const int cxs = (x0 >> 1) & ~3, cxo = (x0 >> 1) - cxs;  // coarse box start (aligned), offset
+    const int cxs = (x0 >> 1) & ~3;                   // coarse box start (16-B aligned)
     const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
     const int qstart = max(y0 - RUP, 0);
     const int qend = min(y1 + R, H);
     const int nsteps = (qend - qstart + S - 1) / S;
     const unsigned hw32 = (unsigned)H * (unsigned)W;
-    auto slot = [](int P) { return (P + 8 * AR) % AR; };
     auto lin_block = [&](int j) { return s_lin + ((j + 64 * NBL) % NBL) * BLKF; };
     int sl_i = 0;  // ring slot of the current step's image block (i mod NBL), kept incrementally
     // image-ring row r for rows of the current step's window [qs - NPRO*S + R, qs + 2S + R)
@@ -118,15 +173,15 @@ __global__ void __launch_bounds__(256, 2)
         slt -= slt >= NBL ? NBL : 0;
         return s_lin + slt * BLKF + which * DEMOFF + (rel & 3) * RX;
     };
-    auto up_block = [&](int j) { return s_up + ((j + 64 * NBU) % NBU) * UPF; };
+    auto ring_block = [&](float* base, int j) { return base + ((j + 64 * NBU) % NBU) * UPF; };
     // image-ring row r (absolute) -> pointer to plane `which` (0: x0/L, 1: demod), channel 0
     auto lin_row = [&](int r, int which) {
         const int rel = r - qstart - R + NPRO * S;
         return lin_block(rel / S - NPRO) + which * DEMOFF + (rel % S) * RX;
     };
-    auto up_row = [&](int r) {  // q row r -> upstream ring, channel 0
+    auto ring_row = [&](float* base, int r) {  // q row r -> upstream ring, channel 0
         const int rel = r - qstart + S;
-        return up_block(rel / S - 1) + (rel % S) * RX;
+        return ring_block(base, rel / S - 1) + (rel % S) * RX;
     };
 
     // ---- TMA issue (thread 0)
@@ -137,17 +192,13 @@ __global__ void __launch_bounds__(256, 2)
         tma_load_4d(SEP ? s_lg + LGF : s_lg + (j & 1) * LGF, &mp.lg, xs0, qs, 0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
-        tma_load_4d(up_block(j), &mp.up, xs0, qs, c0, b, bar);
+        tma_load_4d(ring_block(s_up, j), &mp.up, xs0, qs, c0, b, bar);
+        tma_load_4d(s_ob, &mp.out, xs0, qs, c0, b, bar);
         if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
     };
-    auto issue_out = [&](int j) {
-        if constexpr (L0) {
-            mbar_expect_tx(&bars[2], SH::TX_OUT);
-            tma_load_4d(s_out, &mp.out, xs0, qstart + j * S - R, c0, b, &bars[2]);
-        }
-    };
 
-    // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion)
+    // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion);
+    // called by all 256 threads with uniform arguments
     const bool col_border = xs0 < 0 || xs0 + RX > W;
     auto patch_rows = [&](int r0, int r1) {
         if (col_border) {
@@ -158,7 +209,7 @@ __global__ void __launch_bounds__(256, 2)
                 float* row = lin_row(r, pc / 3) + (pc % 3) * PL;
                 if (src != ri) row[ri] = row[src];
             }
-            __syncthreads();
+            cta_sync();
         }
         if (r0 < 0 || r1 > H) {
             for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
@@ -167,7 +218,7 @@ __global__ void __launch_bounds__(256, 2)
                 const int src = clampi(r, 0, H - 1);
                 if (src != r) lin_row(r, pc / 3)[(pc % 3) * PL + ri] = lin_row(src, pc / 3)[(pc % 3) * PL + ri];
             }
-            __syncthreads();
+            cta_sync();
         }
     };
     // x0 = noisy / max(d, floor) in place (level 0), for ring rows of block j
@@ -177,13 +228,12 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 const float d = blk[DEMOFF + c * PL + s * RX + ri];
-                blk[c * PL + s * RX + ri] *= rcp_dem(demod_clamp(d));
+                blk[c * PL + s * RX + ri] *= rcp_fast(fmaxf(d, (float)kDemodFloor));
             }
         }
     };
 
     // ---- prologue
-    for (int i = tid; i < AR * 3 * TXB; i += 256) s_acc[i] = 0.f;
     if constexpr (UP)
         for (int i = tid; i < CR * 3 * TXC; i += 256) s_cac[i] = 0.f;
     if (tid == 0) {
@@ -198,7 +248,6 @@ __global__ void __launch_bounds__(256, 2)
             if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qstart + R + j * S, c0, b, &bars[3]);
         }
         if (nsteps > 0) issue_step(0);
-        issue_out(0);
     }
     mbar_wait(&bars[3], 0);
     for (int i = tid; i < NPRO * S * RX; i += 256) {
@@ -208,19 +257,15 @@ __global__ void __launch_bounds__(256, 2)
     __syncthreads();
     patch_rows(qstart + R - NPRO * S, qstart + R);
 
-    int next_flush = max(qstart - R, 0);
-    int cnext = qstart >> 1;
     const int s_a = tid >> 6, rw_a = tid & 63;  // phase A: S rows x 64 threads, RW <= 64 used
     const int ri_a = RA - R + rw_a;               // smem column of this thread's region pixel
     const bool act_a = rw_a < RW;
 
-    for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
-        const int qs = qstart + i * S;
-        float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
-        const TL* lgs = reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb);  // staged logits
+    // ------------------------------------------------ A: softmax, G, inner'
+    // (every thread; ends with the CTA barrier, the next prefetch and the
+    // clamp patch of the image rows that arrived with this step)
+    auto phase_a = [&](int i, int qs, float* lgb, const TL* lgs) {
         mbar_wait(&bars[i & 1], (i >> 1) & 1);
-
-        // ------------------------------------------------ A: softmax, G', x0
         if (act_a) {
             float e[NLOG];
 #pragma unroll
@@ -228,276 +273,455 @@ __global__ void __launch_bounds__(256, 2)
             float m = e[0];
 #pragma unroll
             for (int t = 1; t < NLOG; ++t) m = fmaxf(m, e[t]);
-            const float mk = m * kLog2e;
-            float sum = 0.f;
+            const float2 mk2 = bcast2(-m * kLog2e);
+            float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) {
-                e[t] = ex2_ftz(fmaf(e[t], kLog2e, -mk));
-                sum += (TIED && t == NT) ? 4.f * e[t] : e[t];
+            for (int t = 0; t + 1 < NLOG; t += 2) {
+                const float2 z2 = ffma2(make_float2(e[t], e[t + 1]), bcast2(kLog2e), mk2);
+                e[t] = ex2_ftz(z2.x);
+                e[t + 1] = ex2_ftz(z2.y);
+                sum2 = fadd2(sum2, make_float2((TIED && t == NT) ? 4.f * e[t] : e[t],
+                                               (TIED && t + 1 == NT) ? 4.f * e[t + 1] : e[t + 1]));
+            }
+            float sum = sum2.x + sum2.y;
+            if constexpr (NLOG & 1) {
+                e[NLOG - 1] = ex2_ftz(fmaf(e[NLOG - 1], kLog2e, mk2.x));
+                sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];
             }
 #pragma unroll
             for (int t = 0; t < NLOG; ++t) lgb[t * PL + s_a * RX + ri_a] = e[t];
-            const float inv = __fdividef(1.f, sum);
-            s_inv[s_a * RX + ri_a] = inv;
+            const float inv = rcp_fast(sum);
             convert_block(i, s_a, ri_a);  // (block i = slot sl_i)
-            const float* ub = up_block(i) + s_a * RX + ri_a;
+            float* ub = ring_block(s_up, i) + s_a * RX + ri_a;
+            const float* ob = s_ob + s_a * RX + ri_a;
             float dq[3] = {1.f, 1.f, 1.f};
             if constexpr (L0) {
                 const float* dr = lin_row_step(qs, qs + s_a, 1) + ri_a;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) dq[c] = demod_clamp(dr[c * PL]);
+                for (int c = 0; c < 3; ++c) dq[c] = fmaxf(dr[c * PL], (float)kDemodFloor);
             }
+            float inner = 0.f;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) s_g[c * PL + s_a * RX + ri_a] = ub[c * PL] * dq[c] * inv;
-        }
-        __syncthreads();
-        // every thread has finished the previous step's flush and this step's
-        // phase A: the buffers of step i+1 (and this step's out box) are free
-        if (tid == 0) {
-            if (i + 1 < nsteps) {
-                fence_proxy_async();
-                issue_step(i + 1);
+            for (int c = 0; c < 3; ++c) {
+                const float u = ub[c * PL], uo = u * ob[c * PL];
+                inner += uo;
+                s_g[c * PL + s_a * RX + ri_a] = u * dq[c] * inv;
+                if constexpr (L0) ub[c * PL] = uo;  // the flush's demod gradient needs u * out
             }
-            if (i > 0) issue_out(i);
+            s_inn[s_a * RX + ri_a] = inner * inv;
+        }
+        cta_sync();
+        // every thread has finished the previous step and this step's phase A:
+        // the buffers of step i+1 are free
+        if (tid == 0 && i + 1 < nsteps) {
+            fence_proxy_async();
+            issue_step(i + 1);
         }
         if (col_border || qs + R + S > H) patch_rows(qs + R, qs + R + S);
+    };
 
-        // ------------------------------------------------ B1: logit gradients
-        if (a.want_params && tid < S * TXB) {
-            const int s = tid / TXB, xi = tid - s * TXB;
-            const int qy = qs + s, gx = x0 + xi, ri = xi + RA;
-            if (qy >= y0 && qy < y1 && gx < W) {
-                float gq[3];
+    const bool want = a.want_params != 0;
+    const bool acc_mode = a.accum != 0;
+
+    if (tid < 128) {
+        // ==================================================== B1 + B3 warps
+        int cnext = qstart >> 1;
+        const int part = B1SPL == 1 ? 0 : tid / SH::B1ITEMS;
+        const int item = tid - part * SH::B1ITEMS;
+        const int s = item / NPAIR, xi = 2 * (item - s * NPAIR), ri = xi + RA;
+        for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
+            const int qs = qstart + i * S;
+            float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
+            phase_a(i, qs, lgb, reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb));
+
+            // -------------------------------------------- B1: logit gradients
+            const int qy = qs + s, gx = x0 + xi;
+            // W is a multiple of 4 on this path: the pair (gx, gx + 1) is in
+            // the image and 8-B aligned in every gradient plane
+            if (want && item < SH::NB1 && qy >= y0 && qy < y1 && gx < W) {
+                float g0[3], g1[3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) gq[c] = s_g[c * PL + s * RX + ri];
-                const float inv = s_inv[s * RX + ri];
-                float gw[NW];
-#pragma unroll
-                for (int dy = -R; dy <= R; ++dy) {
-                    const float* lr = lin_row_step(qs, qy + dy, 0) + ri;
-#pragma unroll
-                    for (int dx = -R; dx <= R; ++dx) {
-                        float acc = 0.f;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) acc = fmaf(gq[c], lr[c * PL + dx], acc);
-                        gw[(dy + R) * K + dx + R] = acc;
-                    }
+                for (int c = 0; c < 3; ++c) {
+                    const float2 gg = *reinterpret_cast<const float2*>(s_g + c * PL + s * RX + ri);
+                    g0[c] = gg.x;
+                    g1[c] = gg.y;
                 }
-                if constexpr (UP) {
-                    const float* lh = s_lhc + (i & 1) * SH::LHF;
-                    const int cyb = qs >> 1, cxb = cxs;
-#pragma unroll
-                    for (int ii = 0; ii < 2; ++ii)
-#pragma unroll
-                        for (int jj = 0; jj < 2; ++jj) {
-                            const int cy = min((qy + ii) >> 1, a.Hc - 1) - cyb;
-                            const int cx = min((gx + jj) >> 1, a.Wc - 1) - cxb;
-                            float acc = 0.f;
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) acc = fmaf(gq[c], lh[(c * CROWS + cy) * CB + cx], acc);
-                            gw[NT + 2 * ii + jj] = acc;
-                        }
-                }
+                const float2 inn = *reinterpret_cast<const float2*>(s_inn + s * RX + ri);
                 const float* ep = lgb + s * RX + ri;
-                float dot = 0.f;
+                auto body = [&](auto acc_t) {
+                    constexpr bool ACC = decltype(acc_t)::value;
+                    constexpr int PA = R & 1;        // odd R: window starts one column early (8-B aligned)
+                    constexpr int NV2 = R + 1 + PA;  // float2 window loads per row and channel
+                    const int t_first = part == 0 ? 0 : SH::DYS * K;
+                    TL* gp = (TL*)a.glogits + (long long)b * a.lg_b + ((unsigned)qy * (unsigned)W + (unsigned)gx) +
+                             (size_t)t_first * hw32;
+                    auto tap_row = [&](int dy) {
+                        const float* xr = lin_row_step(qs, qy + dy, 0) + ri - R - PA;
+                        // accumulators start at -inner': g_logit_t = e_t * (gw_t - inner')
+                        float gw0[K], gw1[K];
 #pragma unroll
-                for (int t = 0; t < NW; ++t) {
-                    const int slot_t = (TIED && t >= NT) ? NT : t;
-                    dot = fmaf(ep[slot_t * PL], gw[t], dot);
-                }
-                const float inner = dot * inv;
-                TL* const gfb = (TL*)a.glogits + (long long)b * a.lg_b;  // uniform per CTA
-                const unsigned po = (unsigned)qy * (unsigned)W + (unsigned)gx;
-                const bool acc_mode = a.accum != 0;
-                float gz[NLOG];
+                        for (int d = 0; d < K; ++d) {
+                            gw0[d] = -inn.x;
+                            gw1[d] = -inn.y;
+                        }
 #pragma unroll
-                for (int t = 0; t < NT; ++t) gz[t] = ep[t * PL] * (gw[t] - inner);
-                if constexpr (UP) {
-                    if constexpr (TIED) {
-                        gz[NT] = ep[NT * PL] * (((gw[NT] + gw[NT + 1]) + (gw[NT + 2] + gw[NT + 3])) - 4.f * inner);
+                        for (int c = 0; c < 3; ++c) {
+                            float2 vv[NV2];
+#pragma unroll
+                            for (int k2 = 0; k2 < NV2; ++k2)
+                                vv[k2] = *reinterpret_cast<const float2*>(xr + c * PL + 2 * k2);
+                            auto V = [&](int k) { return (k & 1) ? vv[k >> 1].y : vv[k >> 1].x; };
+                            // pixel p reads window value PA + p + d for tap d; taps whose
+                            // value starts an aligned pair go two at a time (FFMA2)
+#pragma unroll
+                            for (int d = 0; d < K; ++d) {
+                                if (((PA + d) & 1) == 0 && d + 1 < K) {
+                                    const float2 r = ffma2(bcast2(g0[c]), vv[(PA + d) >> 1], make_float2(gw0[d], gw0[d + 1]));
+                                    gw0[d] = r.x;
+                                    gw0[d + 1] = r.y;
+                                } else if (!(d >= 1 && ((PA + d - 1) & 1) == 0)) {
+                                    gw0[d] = fmaf(g0[c], V(PA + d), gw0[d]);
+                                }
+                                if (((PA + 1 + d) & 1) == 0 && d + 1 < K) {
+                                    const float2 r = ffma2(bcast2(g1[c]), vv[(PA + 1 + d) >> 1], make_float2(gw1[d], gw1[d + 1]));
+                                    gw1[d] = r.x;
+                                    gw1[d + 1] = r.y;
+                                } else if (!(d >= 1 && ((PA + d) & 1) == 0)) {
+                                    gw1[d] = fmaf(g1[c], V(PA + 1 + d), gw1[d]);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int d = 0; d < K; ++d) {
+                            const int t = (dy + R) * K + d;
+                            const float2 e2 = *reinterpret_cast<const float2*>(ep + t * PL);
+                            st_gz2<ACC>(gp, e2.x * gw0[d], e2.y * gw1[d]);
+                            gp += hw32;
+                        }
+                    };
+                    if (part == 0) {
+#pragma unroll
+                        for (int dy = -R; dy < -R + SH::DYS; ++dy) tap_row(dy);
                     } else {
 #pragma unroll
-                        for (int t = NT; t < NW; ++t) gz[t] = ep[t * PL] * (gw[t] - inner);
+                        for (int dy = -R + SH::DYS; dy <= R; ++dy) tap_row(dy);
                     }
-                }
+                    if constexpr (UP) {
+                        if (part == B1SPL - 1) {
+                            // parents: columns gx/2 (both pixels, jj = 0; pixel 0 jj = 1) and
+                            // gx/2 + 1 clamped (pixel 1, jj = 1); rows per ii
+                            const float* lh = s_lhc + (i & 1) * SH::LHF;
+                            const int cyb = qs >> 1;
+                            const int X0 = min(gx >> 1, a.Wc - 1) - cxs;
+                            const int X1 = min((gx >> 1) + 1, a.Wc - 1) - cxs;
+                            float gu0[4], gu1[4];
 #pragma unroll
-                for (int t = 0; t < NLOG; ++t) st_gz(gfb + (po + t * hw32), gz[t], acc_mode);
-            }
-        }
-
-        // ------------------------------------------------ B2: gather transpose
-        if (tid >= 256 - 3 * TXB) {
-            const int u2 = tid - (256 - 3 * TXB);
-            const int c = u2 / TXB, xi = u2 - c * TXB;
-            const int gx = x0 + xi, ri = xi + RA;
-            if (gx < W) {
-                float acc[S + 2 * R];
+                            for (int ii = 0; ii < 2; ++ii) {
+                                const int cy = min((qy + ii) >> 1, a.Hc - 1) - cyb;
+                                float s00 = -inn.x, s10 = -inn.y, s11 = -inn.y;
 #pragma unroll
-                for (int k2 = 0; k2 < S + 2 * R; ++k2) acc[k2] = 0.f;
+                                for (int c = 0; c < 3; ++c) {
+                                    const float l0 = lh[(c * CROWS + cy) * CB + X0];
+                                    const float l1 = lh[(c * CROWS + cy) * CB + X1];
+                                    s00 = fmaf(g0[c], l0, s00);
+                                    s10 = fmaf(g1[c], l0, s10);
+                                    s11 = fmaf(g1[c], l1, s11);
+                                }
+                                gu0[2 * ii] = s00;
+                                gu0[2 * ii + 1] = s00;
+                                gu1[2 * ii] = s10;
+                                gu1[2 * ii + 1] = s11;
+                            }
+                            if constexpr (TIED) {
+                                const float2 e2 = *reinterpret_cast<const float2*>(ep + NT * PL);
+                                const float a0 = (gu0[0] + gu0[1]) + (gu0[2] + gu0[3]);
+                                const float a1 = (gu1[0] + gu1[1]) + (gu1[2] + gu1[3]);
+                                st_gz2<ACC>(gp, e2.x * a0, e2.y * a1);
+                            } else {
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-#pragma unroll
-                    for (int dx = -R; dx <= R; ++dx) {
-                        const int rj = ri - dx;
-                        const float g = s_g[c * PL + s * RX + rj];
-#pragma unroll
-                        for (int d = 0; d < K; ++d)
-                            acc[s + d] = fmaf(lgb[(d * K + dx + R) * PL + s * RX + rj], g, acc[s + d]);
-                    }
-                }
-                if (gx == 0 || gx == W - 1) {
-                    // clamp fold along x: logical columns beyond the border land on it
-                    for (int side = 0; side < 2; ++side) {
-                        if ((side == 0 && gx != 0) || (side == 1 && gx != W - 1)) continue;
-                        for (int e = 1; e <= R; ++e) {
-                            const int Pc = side == 0 ? -e : W - 1 + e;
-                            for (int dx = -R; dx <= R; ++dx) {
-                                const int qx = Pc - dx;
-                                if (qx < 0 || qx >= W) continue;
-                                const int rj = qx - xs0;
-#pragma unroll
-                                for (int s = 0; s < S; ++s) {
-                                    const float g = s_g[c * PL + s * RX + rj];
-#pragma unroll
-                                    for (int d = 0; d < K; ++d)
-                                        acc[s + d] = fmaf(lgb[(d * K + dx + R) * PL + s * RX + rj], g, acc[s + d]);
+                                for (int t4 = 0; t4 < 4; ++t4) {
+                                    const float2 e2 = *reinterpret_cast<const float2*>(ep + (NT + t4) * PL);
+                                    st_gz2<ACC>(gp, e2.x * gu0[t4], e2.y * gu1[t4]);
+                                    gp += hw32;
                                 }
                             }
                         }
                     }
-                }
-#pragma unroll
-                for (int k2 = 0; k2 < S + 2 * R; ++k2) s_acc[(slot(qs - R + k2) * 3 + c) * TXB + xi] += acc[k2];
+                };
+                if (acc_mode) body(std::true_type{});
+                else body(std::false_type{});
             }
-        }
-        // ------------------------------------------------ B3: upsample transpose
-        if constexpr (UP) {
-            // B3 items on the threads not running B2 first, then wrap onto the top threads
-            const int nb3 = 256 - 3 * TXB;
-            const int u = tid < nb3 ? tid : (tid >= 256 - (3 * TXC - nb3) ? nb3 + tid - (256 - (3 * TXC - nb3)) : -1);
-            if (u >= 0 && u < 3 * TXC) {
-                const int c = u / TXC, cxi = u - c * TXC;
+
+            // -------------------------------------------- B3: upsample transpose
+            // coarse column X receives fine columns 2X-1 (tap j=1), 2X (j=0,1),
+            // 2X+1 (j=0; and j=1 at the last coarse column, W even); coarse row
+            // min((y+i)/2, Hc-1) per fine row y and tap row i
+            if constexpr (UP) {
+                const int cxi = (tid & 31) * 4 + (tid >> 5);  // items spread over the 4 warps
                 const int X = (x0 >> 1) + cxi;
-                if (X < a.Wc) {
-                    float cv[CROWS];
+                if (cxi < TXC && X < a.Wc) {
+                    const int rj = 2 * cxi + RA;  // smem column of fine x = 2X
+                    const bool lastX = X == a.Wc - 1;
+                    float cv[CROWS][3];
 #pragma unroll
-                    for (int k2 = 0; k2 < CROWS; ++k2) cv[k2] = 0.f;
+                    for (int k2 = 0; k2 < CROWS; ++k2)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) cv[k2][c] = 0.f;
                     const int cyb = qs >> 1;  // qs is even
 #pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const int qy = qs + s;
-                        if (qy >= H) break;
-                        // parents: row s/2 (tap i = 0) and (s+1)/2 (tap i = 1), the latter
-                        // clamped onto the last coarse row when it falls off the image
-                        const bool clamp1 = ((qy + 1) >> 1) > a.Hc - 1;
+                    for (int ss = 0; ss < S; ++ss) {
+                        const int qy = qs + ss;
+                        if (qy < H) {
+                            float gm[3], g0[3], gq[3];
 #pragma unroll
-                        for (int k3 = -1; k3 <= 1; ++k3) {
-                            const int xx = 2 * X + k3;
-                            if (xx < 0 || xx >= W) continue;
-                            const int rj = xx - xs0;
-                            const float g = s_g[c * PL + s * RX + rj];
+                            for (int c = 0; c < 3; ++c) {
+                                const float* gr = s_g + c * PL + ss * RX + rj;
+                                gm[c] = gr[-1];
+                                g0[c] = gr[0];
+                                gq[c] = gr[1];
+                            }
 #pragma unroll
-                            for (int jj = 0; jj < 2; ++jj) {
-                                if (min((xx + jj) >> 1, a.Wc - 1) != X) continue;
-                                const float w0 = lgb[(TIED ? NT : NT + jj) * PL + s * RX + rj];
-                                const float w1 = lgb[(TIED ? NT : NT + 2 + jj) * PL + s * RX + rj];
-                                cv[s >> 1] = fmaf(w0, g, cv[s >> 1]);
-                                if (clamp1) cv[(s + 1) >> 1 == 0 ? 0 : ((s + 1) >> 1) - 1] = fmaf(w1, g, cv[(s + 1) >> 1 == 0 ? 0 : ((s + 1) >> 1) - 1]);
-                                else cv[(s + 1) >> 1] = fmaf(w1, g, cv[(s + 1) >> 1]);
+                            for (int ii = 0; ii < 2; ++ii) {
+                                const float* w0 = lgb + (TIED ? NT : NT + 2 * ii) * PL + ss * RX + rj;
+                                const float* w1 = lgb + (TIED ? NT : NT + 2 * ii + 1) * PL + ss * RX + rj;
+                                const float am = w1[-1], a0 = w0[0] + w1[0];
+                                const float aq = lastX ? w0[1] + w1[1] : w0[1];
+                                const int yl = min((qy + ii) >> 1, a.Hc - 1) - cyb;  // 0..2
+#pragma unroll
+                                for (int yy = 0; yy < CROWS; ++yy) {
+                                    if (yy != yl) continue;
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c)
+                                        cv[yy][c] = fmaf(am, gm[c], fmaf(a0, g0[c], fmaf(aq, gq[c], cv[yy][c])));
+                                }
                             }
                         }
                     }
 #pragma unroll
                     for (int k2 = 0; k2 < CROWS; ++k2)
-                        s_cac[(((cyb + k2) & (CR - 1)) * 3 + c) * TXC + cxi] += cv[k2];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) s_cac[(((cyb + k2) & (CR - 1)) * 3 + c) * TXC + cxi] += cv[k2][c];
                 }
             }
-        }
-        __syncthreads();
+            cta_sync();  // end of step: B2 warps flushed their rows, B3 accumulations done
 
-        // ------------------------------------------------ flush finished rows
-        const bool bottom = qs + S >= H;
-        const int pend = max(bottom ? H : qs + S - R, next_flush);
-        if constexpr (L0) mbar_wait(&bars[2], i & 1);
-        for (int k2 = tid; k2 < (pend - next_flush) * TXB; k2 += 256) {
-            const int rr = k2 / TXB, xi = k2 - rr * TXB;
-            const int P = next_flush + rr, gx = x0 + xi;
-            float v[3];
+            if constexpr (UP) {
+                // coarse ghat rows finished by this step (all B3 items are in)
+                const bool bottom = qs + S >= H;
+                const int cend = bottom ? a.Hc : (qs + S) >> 1;
+                const int own0 = y0 >> 1, own1 = (y1 + 1) >> 1;
+                for (int k2 = tid; k2 < (cend - cnext) * TXC; k2 += 128) {
+                    const int rr = k2 / TXC, cxi = k2 - rr * TXC;
+                    const int Y = cnext + rr, X = (x0 >> 1) + cxi;
+                    float v[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                float* p = &s_acc[(slot(P) * 3 + c) * TXB + xi];
-                v[c] = *p;
-                *p = 0.f;
+                    for (int c = 0; c < 3; ++c) {
+                        float* p = &s_cac[((Y & (CR - 1)) * 3 + c) * TXC + cxi];
+                        v[c] = *p;
+                        *p = 0.f;
+                    }
+                    if (Y < own0 || Y >= own1 || X >= a.Wc) continue;
+                    float* gc = (float*)a.ghat_c + (long long)b * a.c_b + (long long)Y * a.Wc + X;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        if (c < nc) gc[c * a.c_c] = v[c];
+                }
+                cnext = cend;
             }
-            if (P == 0)
-                for (int e = 1; e <= R; ++e)
+        }
+    } else {
+        // ==================================================== B2 warps
+        const int b2 = tid - 128;
+        const int col = b2 / B2SPL, part = b2 - col * B2SPL;
+        const int gx = x0 + col, ri = col + RA;
+        const bool act2 = col < TXB && gx < W;
+        // the lanes of a column split the tap columns dx (window rows stay compile-time)
+        constexpr int DXN = (K + B2SPL - 1) / B2SPL;
+        const int dx0 = -R + part * DXN, ndx = min(DXN, R + 1 - dx0);
+        float* const glo = (float*)a.gl_out + (long long)b * a.in_b;
+        float* const gdo = (L0 && a.gdc_out) ? (float*)a.gdc_out + (long long)b * a.in_b : nullptr;
+        // output rows qs - R + k, k in [0, AW), packed in pairs (2p, 2p+1) so
+        // taps d, d+1 landing on one pair go as one FFMA2
+        float2 win[NPW][3];
+#pragma unroll
+        for (int p = 0; p < NPW; ++p)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) win[p][c] = make_float2(0.f, 0.f);
+        auto wget = [&](int k, int c) { return (k & 1) ? win[k >> 1][c].y : win[k >> 1][c].x; };
+        auto wadd = [&](int k, int c, float v) {
+            if (k & 1) win[k >> 1][c].y += v;
+            else win[k >> 1][c].x += v;
+        };
+        for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
+            const int qs = qstart + i * S;
+            float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;
+            phase_a(i, qs, lgb, reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb));
+
+            // taps of tap column dx for every source row of the step: window row
+            // k = s + d (compile-time), smem column rj = ri - dx (runtime)
+            auto gather_dx = [&](int rj, int dx) {
+#pragma unroll
+                for (int ss = 0; ss < S; ++ss) {
+                    float g[3], w[K];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) g[c] = s_g[c * PL + ss * RX + rj];
+#pragma unroll
+                    for (int d = 0; d < K; ++d) w[d] = lgb[(d * K + dx + R) * PL + ss * RX + rj];
+#pragma unroll
+                    for (int d = 0; d < K; ++d) {
+                        const int k = ss + d;
+                        if ((k & 1) == 0 && d + 1 < K) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c)
+                                win[k >> 1][c] = ffma2(make_float2(w[d], w[d + 1]), bcast2(g[c]), win[k >> 1][c]);
+                        } else if (!(d >= 1 && ((k - 1) & 1) == 0)) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) wadd(k, c, w[d] * g[c]);
+                        }
+                    }
+                }
+            };
+            if (act2) {
+                // this lane's tap columns: [dx0, dx0 + ndx)
+#pragma unroll
+                for (int j = 0; j < DXN; ++j)
+                    if (j < ndx) gather_dx(ri - (dx0 + j), dx0 + j);
+                if (part == 0 && (gx == 0 || gx == W - 1)) {
+                    // clamp fold along x: taps of in-image sources that land beyond
+                    // the border column are gathered onto it (border columns only)
+#pragma unroll 1
+                    for (int e = 1; e <= R; ++e) {
+                        const int Pc = gx == 0 ? -e : W - 1 + e;
+#pragma unroll 1
+                        for (int dx = -R; dx <= R; ++dx) {
+                            const int qx = Pc - dx;
+                            if (qx >= 0 && qx < W) gather_dx(qx - xs0, dx);
+                        }
+                    }
+                }
+            }
+
+            // ---- finished output rows: image-border row folds, reduce over the
+            // row groups (adjacent lanes), write
+            const bool bottom = qs + S >= H;
+            if (qs == 0) {
+                // rows above the image fold onto row 0 (window row R)
+#pragma unroll
+                for (int k = 0; k < R; ++k)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        float* p = &s_acc[(slot(-e) * 3 + c) * TXB + xi];
-                        v[c] += *p;
-                        *p = 0.f;
+                        wadd(R, c, wget(k, c));
+                        if (k & 1) win[k >> 1][c].y = 0.f;
+                        else win[k >> 1][c].x = 0.f;
                     }
-            if (P == H - 1)
-                for (int e = 1; e <= R; ++e)
+            }
+            const int klast = H - 1 - (qs - R);  // window row of the image's last row
+            if (bottom) {
+                // rows below the image fold onto row H-1
+#pragma unroll
+                for (int k = 1; k < AW; ++k)
+#pragma unroll
+                    for (int kl = 0; kl < k; ++kl)
+                        if (kl == klast)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) wadd(kl, c, wget(k, c));
+            }
+            // block of S window rows starting at compile-time kb: reduce-scatter
+            // across the B2SPL lanes of the column, each lane writes S/B2SPL rows
+            auto flush_block = [&](auto kb_t) {
+                constexpr int KB = decltype(kb_t)::value;
+                constexpr int PB = KB / 2;  // first pair (KB even)
+                float2 keep[3];             // rows of this lane (pair or one component)
+                int krow;                   // first window row this lane writes
+                int nrow;                   // rows this lane writes (1 or 2 or 4)
+                float vout[4][3];
+                if constexpr (B2SPL == 1) {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) vout[r][c] = wget(KB + r, c);
+                    krow = KB;
+                    nrow = 4;
+                } else {
+                    // round 1: halves (pairs PB, PB+1) between lanes part ^ (B2SPL/2)
+                    const int hm = B2SPL / 2;
+                    const bool upper = (part & hm) != 0;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        float* p = &s_acc[(slot(H - 1 + e) * 3 + c) * TXB + xi];
-                        v[c] += *p;
-                        *p = 0.f;
+                        const float2 lo = PB < NPW ? win[PB][c] : make_float2(0.f, 0.f);
+                        const float2 hi = PB + 1 < NPW ? win[PB + 1][c] : make_float2(0.f, 0.f);
+                        const float2 send = upper ? lo : hi;
+                        float2 recv;
+                        recv.x = __shfl_xor_sync(0xffffffffu, send.x, hm);
+                        recv.y = __shfl_xor_sync(0xffffffffu, send.y, hm);
+                        keep[c] = fadd2(upper ? hi : lo, recv);
                     }
-            if (P < y0 || P >= y1 || gx >= W) continue;
-            const long long off = (long long)P * W + gx;
-            float* glo = (float*)a.gl_out + (long long)b * a.in_b;
-            if constexpr (L0) {
-                float* gdo = a.gdc_out ? (float*)a.gdc_out + (long long)b * a.in_b : nullptr;
-                const int ri = xi + RA;
-                const float* xr = lin_row_step(qs, P, 0) + ri;
-                const float* dr = lin_row_step(qs, P, 1) + ri;
-                const float* ur = up_row(P) + ri;
-                const float* orow = s_out + (P - (qs - R)) * RX + ri;
+                    if constexpr (B2SPL == 2) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    if (c >= nc) break;
-                    const long long o = c * a.in_c + off;
-                    if (a.demod) {
-                        const float rd = rcp_dem(demod_clamp(dr[c * PL]));
-                        glo[o] = v[c] * rd;
-                        if (gdo) gdo[o] = ur[c * PL] * (orow[c * (S + R) * RX] * rd) - v[c] * xr[c * PL] * rd;
+                        for (int c = 0; c < 3; ++c) {
+                            vout[0][c] = keep[c].x;
+                            vout[1][c] = keep[c].y;
+                        }
+                        krow = KB + (upper ? 2 : 0);
+                        nrow = 2;
                     } else {
-                        glo[o] = v[c];
+                        // round 2: components between lanes part ^ 1
+                        const bool odd = (part & 1) != 0;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const float send = odd ? keep[c].x : keep[c].y;
+                            const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+                            vout[0][c] = (odd ? keep[c].y : keep[c].x) + recv;
+                        }
+                        krow = KB + (upper ? 2 : 0) + (odd ? 1 : 0);
+                        nrow = 1;
                     }
                 }
-            } else {
+                if (!act2) return;
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    if (c < nc) glo[c * a.in_c + off] = v[c];
-            }
-        }
-        next_flush = pend;
-
-        if constexpr (UP) {
-            const int cend = bottom ? a.Hc : (qs + S) >> 1;
-            const int own0 = y0 >> 1, own1 = (y1 + 1) >> 1;
-            for (int k2 = tid; k2 < (cend - cnext) * TXC; k2 += 256) {
-                const int rr = k2 / TXC, cxi = k2 - rr * TXC;
-                const int Y = cnext + rr, X = (x0 >> 1) + cxi;
-                float v[3];
+                for (int r = 0; r < 4; ++r) {
+                    if (r >= nrow) break;
+                    const int P = qs - R + krow + r;
+                    if (P < y0 || P >= y1 || P > H - 1) continue;
+                    const unsigned off = (unsigned)P * (unsigned)W + (unsigned)gx;
+                    if constexpr (L0) {
+                        const float* xr = lin_row_step(qs, P, 0) + ri;
+                        const float* dr = lin_row_step(qs, P, 1) + ri;
+                        const float* uor = ring_row(s_up, P) + ri;  // u * out
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    float* p = &s_cac[((Y & (CR - 1)) * 3 + c) * TXC + cxi];
-                    v[c] = *p;
-                    *p = 0.f;
+                        for (int c = 0; c < 3; ++c) {
+                            if (c >= nc) break;
+                            const unsigned o = c * hw32 + off;
+                            if (a.demod) {
+                                const float rd = rcp_fast(fmaxf(dr[c * PL], (float)kDemodFloor));
+                                const float v = vout[r][c];
+                                __stcs(glo + o, v * rd);
+                                if (gdo) __stcs(gdo + o, (uor[c * PL] - v * xr[c * PL]) * rd);
+                            } else {
+                                __stcs(glo + o, vout[r][c]);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            if (c < nc) glo[c * hw32 + off] = vout[r][c];
+                    }
                 }
-                if (Y < own0 || Y >= own1 || X >= a.Wc) continue;
-                float* gc = (float*)a.ghat_c + (long long)b * a.c_b + (long long)Y * a.Wc + X;
+            };
+            flush_block(std::integral_constant<int, 0>{});
+            if (bottom) {
+                // the image's last rows: the whole window is final
+                if constexpr (AW > S) flush_block(std::integral_constant<int, (AW > S ? S : 0)>{});
+                if constexpr (AW > 2 * S) flush_block(std::integral_constant<int, (AW > 2 * S ? 2 * S : 0)>{});
+            }
+            // slide the window by S rows
+#pragma unroll
+            for (int p = 0; p < NPW; ++p)
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
-                    if (c < nc) gc[c * a.c_c] = v[c];
-            }
-            cnext = cend;
+                    win[p][c] = p + S / 2 < NPW ? win[p + S / 2][c] : make_float2(0.f, 0.f);
+            cta_sync();  // end of step
         }
-        // no barrier here: the next phase A touches none of the buffers this
-        // flush reads; the next prefetch is issued after the next phase-A barrier
     }
 }
 

@@ -101,7 +101,8 @@ inline int pick_segment(int strips, int H, int B) {
 template <int K, typename TL, bool L0, bool UP, bool TIED>
 bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
     using SH = TmaShape<K, TL, L0, UP, TIED>;
-    if (L0 && !a0.demod) return false;
+    // needs the forward output (level 0) / Lhat^l for the softmax-backward inner product
+    if ((L0 && !a0.demod) || !a0.outp) return false;
     if (const char* e = getenv("SSB_NO_TMA")) {
         if (e[0] == '1') return false;
     }
@@ -117,16 +118,16 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
                               SH::RX, SH::S, 3) &&
               make_tma_map_4d(&mp.up, base(a0.gin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
                               SH::RX, SH::S, 3);
+    if (ok)
+        ok = make_tma_map_4d(&mp.out, base(a0.outp, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                             SH::RX, SH::S, 3);
     if (ok && L0)
         ok = make_tma_map_4d(&mp.dem, base(a0.demod, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
-                             SH::RX, SH::S, 3) &&
-             (!a0.outp || make_tma_map_4d(&mp.out, base(a0.outp, plane), f32, 4, a0.W, a0.H, a0.ctot,
-                                          a0.batch, SH::RX, SH::S + SH::R, 3));
+                             SH::RX, SH::S, 3);
     if (ok && UP)
         ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
     if (!ok) return false;
-    if (L0 && !a0.outp) mp.out = mp.lin;  // out box unused without the demod gradient
     auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -316,6 +317,7 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
                 a.gprev_out = io->g_prev ? (T*)io->g_prev + coff0 : nullptr;
             } else {
                 a.lin = (const T*)(tp + p.pool_off[l]) + (long long)c0 * e_l;
+                a.outp = (const T*)(tp + p.lhat_off[l]) + (long long)c0 * e_l;  // Lhat^l
                 a.gin = (const T*)(wp + p.ghat_off[l]) + (long long)c0 * e_l;
                 a.gl_out = (T*)(wp + p.gl_off[l]) + (long long)c0 * e_l;
             }
