@@ -18,9 +18,9 @@
 //     tap's logit gradient is final as soon as its gw is known:
 //        g_logit_t = e_t * (sum_c G_c x_c(q + o_t) - inner').
 //  Then the warps split by role (one loop each, CTA barriers in step):
-//  B1 (warps 0-3) logit gradients, one thread per horizontal pixel PAIR
-//     (float2 shared loads, FFMA2 over tap pairs, paired streaming stores),
-//     and the upsample transpose (B3) separably per coarse column.
+//  B1 (warps 0-3) logit gradients, one thread per horizontal pixel QUAD
+//     (float4 shared loads, FFMA2 over tap pairs, 16-B streaming stores),
+//     and the upsample transpose (B3) separably per (coarse column, channel).
 //  B2 (warps 4-7) gather-transpose, one thread per (column, group of tap
 //     columns) with a register window of the S + 2R output rows the step
 //     touches; finished rows are reduced across the groups with warp
@@ -56,16 +56,16 @@ struct TmaShape {
     static constexpr int RA = 16 / LGE, S = 4;
     static constexpr int TXW = ((64 - 2 * R) / RA) * RA;
     static constexpr int TXB = K >= 7 ? 32 : TXW, RX = TXB + 2 * RA, RW = TXB + 2 * R;
-    static constexpr int TXC = TXB / 2, NPAIR = TXB / 2;
+    static constexpr int TXC = TXB / 2, NQUAD = TXB / 4;
     static constexpr int NPRO = (2 * R + S - 1) / S;  // image-ring blocks above step 0
     static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
     // upstream ring (level 0: the flush needs u * out, R rows behind); other
     // levels and the forward output / Lhat^l: one block (read in phase A only)
     static constexpr int NBU = L0 ? (R + S - 1) / S + 2 : 1;
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
-    // B1: S * NPAIR pixel pairs on warps 0-3; tap rows split in B1SPL warp-uniform parts
-    static constexpr int NB1 = S * NPAIR;
-    static constexpr int B1SPL = NB1 <= 64 ? 2 : 1;
+    // B1: S * NQUAD pixel quads on warps 0-3; tap rows split in B1SPL warp-uniform parts
+    static constexpr int NB1 = S * NQUAD;
+    static constexpr int B1SPL = NB1 <= 32 ? 4 : (NB1 <= 64 ? 2 : 1);
     static constexpr int B1ITEMS = 128 / B1SPL;
     static constexpr int DYS = (K + B1SPL - 1) / B1SPL;  // tap rows per part
     // B2: TXB columns x B2SPL tap-column groups on warps 4-7 (adjacent lanes)
@@ -91,7 +91,7 @@ struct TmaShape {
                                      3 * S * RX + S * RX + (UP ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
-    static_assert(TXB * B2SPL <= 128 && TXC <= 128, "B2/B3 items exceed their warps");
+    static_assert(TXB * B2SPL <= 128 && 3 * TXC <= 128 && TXB % 4 == 0, "B2/B3 items exceed their warps");
     static_assert(S * RW <= 256 && RW <= 64, "phase A items exceed the CTA");
     static_assert(S == 4 && (32 % B2SPL) == 0, "step geometry");
 };
@@ -121,6 +121,37 @@ __device__ __forceinline__ void st_gz2(__nv_bfloat16* p, float a, float b) {
     __stcs(reinterpret_cast<unsigned*>(q), *reinterpret_cast<const unsigned*>(&v));
 }
 
+// quad gradient store (four horizontally adjacent pixels, 16-B / 8-B aligned)
+template <bool ACC>
+__device__ __forceinline__ void st_gz4(float* p, float a, float b, float c, float d) {
+    float4* q = reinterpret_cast<float4*>(p);
+    if constexpr (ACC) {
+        float4 o = *q;
+        o.x += a;
+        o.y += b;
+        o.z += c;
+        o.w += d;
+        *q = o;
+    } else {
+        __stcs(q, make_float4(a, b, c, d));
+    }
+}
+template <bool ACC>
+__device__ __forceinline__ void st_gz4(__nv_bfloat16* p, float a, float b, float c, float d) {
+    uint2* q = reinterpret_cast<uint2*>(p);
+    if constexpr (ACC) {
+        const uint2 o = *q;
+        const float2 o0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.x));
+        const float2 o1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.y));
+        a += o0.x;
+        b += o0.y;
+        c += o1.x;
+        d += o1.y;
+    }
+    const __nv_bfloat162 v0 = __floats2bfloat162_rn(a, b), v1 = __floats2bfloat162_rn(c, d);
+    __stcs(q, make_uint2(*reinterpret_cast<const unsigned*>(&v0), *reinterpret_cast<const unsigned*>(&v1)));
+}
+
 __device__ __forceinline__ float rcp_fast(float x) {  // MUFU.RCP (x >= 1e-3 here)
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -134,7 +165,7 @@ __global__ void __launch_bounds__(256, 2)
     using SH = TmaShape<K, TL, L0, UP, TIED>;
     constexpr bool SEP = SH::SEP;
     constexpr int R = SH::R, NT = SH::NT, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
-    constexpr int RA = SH::RA, RW = SH::RW, NPAIR = SH::NPAIR;
+    constexpr int RA = SH::RA, RW = SH::RW, NQUAD = SH::NQUAD;
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
     constexpr int NI = SH::NI, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
     constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF;
@@ -202,12 +233,14 @@ __global__ void __launch_bounds__(256, 2)
     const bool col_border = xs0 < 0 || xs0 + RX > W;
     auto patch_rows = [&](int r0, int r1) {
         if (col_border) {
-            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
-                const int ri = i % RX, rest = i / RX;
+            // only the columns outside the image: [0, lo) and [hi, RX)
+            const int lo = max(0, -xs0), hi = min(RX, W - xs0), nb = lo + (RX - hi);
+            for (int i = tid; i < (r1 - r0) * NI * 3 * nb; i += 256) {
+                const int k = i % nb, rest = i / nb;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
-                const int src = clampi(xs0 + ri, 0, W - 1) - xs0;
+                const int ri = k < lo ? k : hi + (k - lo), src = k < lo ? lo : hi - 1;
                 float* row = lin_row(r, pc / 3) + (pc % 3) * PL;
-                if (src != ri) row[ri] = row[src];
+                row[ri] = row[src];
             }
             cta_sync();
         }
@@ -328,7 +361,7 @@ __global__ void __launch_bounds__(256, 2)
         int cnext = qstart >> 1;
         const int part = B1SPL == 1 ? 0 : tid / SH::B1ITEMS;
         const int item = tid - part * SH::B1ITEMS;
-        const int s = item / NPAIR, xi = 2 * (item - s * NPAIR), ri = xi + RA;
+        const int s = item / NQUAD, xi = 4 * (item - s * NQUAD), ri = xi + RA;
         for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
             const int qs = qstart + i * S;
             float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
@@ -336,112 +369,123 @@ __global__ void __launch_bounds__(256, 2)
 
             // -------------------------------------------- B1: logit gradients
             const int qy = qs + s, gx = x0 + xi;
-            // W is a multiple of 4 on this path: the pair (gx, gx + 1) is in
-            // the image and 8-B aligned in every gradient plane
+            // W is a multiple of 4 on this path: the quad (gx .. gx + 3) is in
+            // the image and 16-B aligned in every gradient plane
             if (want && item < SH::NB1 && qy >= y0 && qy < y1 && gx < W) {
-                float g0[3], g1[3];
+                float g[4][3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const float2 gg = *reinterpret_cast<const float2*>(s_g + c * PL + s * RX + ri);
-                    g0[c] = gg.x;
-                    g1[c] = gg.y;
+                    const float4 gg = *reinterpret_cast<const float4*>(s_g + c * PL + s * RX + ri);
+                    g[0][c] = gg.x;
+                    g[1][c] = gg.y;
+                    g[2][c] = gg.z;
+                    g[3][c] = gg.w;
                 }
-                const float2 inn = *reinterpret_cast<const float2*>(s_inn + s * RX + ri);
+                const float4 inn4 = *reinterpret_cast<const float4*>(s_inn + s * RX + ri);
+                const float inn[4] = {inn4.x, inn4.y, inn4.z, inn4.w};
                 const float* ep = lgb + s * RX + ri;
                 auto body = [&](auto acc_t) {
                     constexpr bool ACC = decltype(acc_t)::value;
-                    constexpr int PA = R & 1;        // odd R: window starts one column early (8-B aligned)
-                    constexpr int NV2 = R + 1 + PA;  // float2 window loads per row and channel
-                    const int t_first = part == 0 ? 0 : SH::DYS * K;
+                    constexpr int OFF = 4 - R;  // window value m = x(ri - 4 + m); pixel p, tap d -> m = p + d + OFF
+                    const int t_first = part * SH::DYS * K;
                     TL* gp = (TL*)a.glogits + (long long)b * a.lg_b + ((unsigned)qy * (unsigned)W + (unsigned)gx) +
                              (size_t)t_first * hw32;
                     auto tap_row = [&](int dy) {
-                        const float* xr = lin_row_step(qs, qy + dy, 0) + ri - R - PA;
+                        const float* xr = lin_row_step(qs, qy + dy, 0) + ri - 4;
                         // accumulators start at -inner': g_logit_t = e_t * (gw_t - inner')
-                        float gw0[K], gw1[K];
+                        float gw[4][K];
 #pragma unroll
-                        for (int d = 0; d < K; ++d) {
-                            gw0[d] = -inn.x;
-                            gw1[d] = -inn.y;
-                        }
+                        for (int p = 0; p < 4; ++p)
+#pragma unroll
+                            for (int d = 0; d < K; ++d) gw[p][d] = -inn[p];
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
-                            float2 vv[NV2];
+                            float2 vv[6];
 #pragma unroll
-                            for (int k2 = 0; k2 < NV2; ++k2)
-                                vv[k2] = *reinterpret_cast<const float2*>(xr + c * PL + 2 * k2);
-                            auto V = [&](int k) { return (k & 1) ? vv[k >> 1].y : vv[k >> 1].x; };
-                            // pixel p reads window value PA + p + d for tap d; taps whose
-                            // value starts an aligned pair go two at a time (FFMA2)
-#pragma unroll
-                            for (int d = 0; d < K; ++d) {
-                                if (((PA + d) & 1) == 0 && d + 1 < K) {
-                                    const float2 r = ffma2(bcast2(g0[c]), vv[(PA + d) >> 1], make_float2(gw0[d], gw0[d + 1]));
-                                    gw0[d] = r.x;
-                                    gw0[d + 1] = r.y;
-                                } else if (!(d >= 1 && ((PA + d - 1) & 1) == 0)) {
-                                    gw0[d] = fmaf(g0[c], V(PA + d), gw0[d]);
-                                }
-                                if (((PA + 1 + d) & 1) == 0 && d + 1 < K) {
-                                    const float2 r = ffma2(bcast2(g1[c]), vv[(PA + 1 + d) >> 1], make_float2(gw1[d], gw1[d + 1]));
-                                    gw1[d] = r.x;
-                                    gw1[d + 1] = r.y;
-                                } else if (!(d >= 1 && ((PA + d) & 1) == 0)) {
-                                    gw1[d] = fmaf(g1[c], V(PA + 1 + d), gw1[d]);
-                                }
+                            for (int k2 = 0; k2 < 3; ++k2) {
+                                const float4 t4 = *reinterpret_cast<const float4*>(xr + c * PL + 4 * k2);
+                                vv[2 * k2] = make_float2(t4.x, t4.y);
+                                vv[2 * k2 + 1] = make_float2(t4.z, t4.w);
                             }
+                            auto V = [&](int m) { return (m & 1) ? vv[m >> 1].y : vv[m >> 1].x; };
+                            // taps whose window value starts an aligned pair go two at a time
+#pragma unroll
+                            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                                for (int d = 0; d < K; ++d) {
+                                    const int m = p + d + OFF;
+                                    if ((m & 1) == 0 && d + 1 < K) {
+                                        const float2 r = ffma2(bcast2(g[p][c]), vv[m >> 1], make_float2(gw[p][d], gw[p][d + 1]));
+                                        gw[p][d] = r.x;
+                                        gw[p][d + 1] = r.y;
+                                    } else if (!(d >= 1 && ((m - 1) & 1) == 0)) {
+                                        gw[p][d] = fmaf(g[p][c], V(m), gw[p][d]);
+                                    }
+                                }
                         }
 #pragma unroll
                         for (int d = 0; d < K; ++d) {
                             const int t = (dy + R) * K + d;
-                            const float2 e2 = *reinterpret_cast<const float2*>(ep + t * PL);
-                            st_gz2<ACC>(gp, e2.x * gw0[d], e2.y * gw1[d]);
+                            const float4 e4 = *reinterpret_cast<const float4*>(ep + t * PL);
+                            st_gz4<ACC>(gp, e4.x * gw[0][d], e4.y * gw[1][d], e4.z * gw[2][d], e4.w * gw[3][d]);
                             gp += hw32;
                         }
                     };
-                    if (part == 0) {
 #pragma unroll
-                        for (int dy = -R; dy < -R + SH::DYS; ++dy) tap_row(dy);
-                    } else {
+                    for (int pp = 0; pp < B1SPL; ++pp) {
+                        if (part == pp) {
 #pragma unroll
-                        for (int dy = -R + SH::DYS; dy <= R; ++dy) tap_row(dy);
+                            for (int dy = -R + pp * SH::DYS; dy < -R + (pp + 1) * SH::DYS && dy <= R; ++dy) tap_row(dy);
+                        }
                     }
                     if constexpr (UP) {
                         if (part == B1SPL - 1) {
-                            // parents: columns gx/2 (both pixels, jj = 0; pixel 0 jj = 1) and
-                            // gx/2 + 1 clamped (pixel 1, jj = 1); rows per ii
+                            // parents: pixel p takes column (gx + p + jj) / 2 (clamped): the
+                            // quad reads coarse columns gx/2, gx/2 + 1, gx/2 + 2 (clamped)
                             const float* lh = s_lhc + (i & 1) * SH::LHF;
                             const int cyb = qs >> 1;
-                            const int X0 = min(gx >> 1, a.Wc - 1) - cxs;
-                            const int X1 = min((gx >> 1) + 1, a.Wc - 1) - cxs;
-                            float gu0[4], gu1[4];
+                            int Xc[3];
+#pragma unroll
+                            for (int k2 = 0; k2 < 3; ++k2) Xc[k2] = min((gx >> 1) + k2, a.Wc - 1) - cxs;
+                            float gu[4][4];  // [pixel][tap 2ii + jj]
 #pragma unroll
                             for (int ii = 0; ii < 2; ++ii) {
                                 const int cy = min((qy + ii) >> 1, a.Hc - 1) - cyb;
-                                float s00 = -inn.x, s10 = -inn.y, s11 = -inn.y;
+                                float dotc[4][3];  // [pixel][parent column offset 0..2]
+#pragma unroll
+                                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                                    for (int k2 = 0; k2 < 3; ++k2) dotc[p][k2] = -inn[p];
 #pragma unroll
                                 for (int c = 0; c < 3; ++c) {
-                                    const float l0 = lh[(c * CROWS + cy) * CB + X0];
-                                    const float l1 = lh[(c * CROWS + cy) * CB + X1];
-                                    s00 = fmaf(g0[c], l0, s00);
-                                    s10 = fmaf(g1[c], l0, s10);
-                                    s11 = fmaf(g1[c], l1, s11);
+                                    float lv[3];
+#pragma unroll
+                                    for (int k2 = 0; k2 < 3; ++k2) lv[k2] = lh[(c * CROWS + cy) * CB + Xc[k2]];
+#pragma unroll
+                                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                                        for (int jj = 0; jj < 2; ++jj) {
+                                            const int k2 = (p + jj) >> 1;  // parent offset of (pixel p, tap jj)
+                                            if (jj == 1 && ((p + 1) >> 1) == (p >> 1)) continue;  // same parent as jj = 0
+                                            dotc[p][k2] = fmaf(g[p][c], lv[k2], dotc[p][k2]);
+                                        }
                                 }
-                                gu0[2 * ii] = s00;
-                                gu0[2 * ii + 1] = s00;
-                                gu1[2 * ii] = s10;
-                                gu1[2 * ii + 1] = s11;
+#pragma unroll
+                                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                                    for (int jj = 0; jj < 2; ++jj) gu[p][2 * ii + jj] = dotc[p][(p + jj) >> 1];
                             }
                             if constexpr (TIED) {
-                                const float2 e2 = *reinterpret_cast<const float2*>(ep + NT * PL);
-                                const float a0 = (gu0[0] + gu0[1]) + (gu0[2] + gu0[3]);
-                                const float a1 = (gu1[0] + gu1[1]) + (gu1[2] + gu1[3]);
-                                st_gz2<ACC>(gp, e2.x * a0, e2.y * a1);
+                                const float4 e4 = *reinterpret_cast<const float4*>(ep + NT * PL);
+                                float z[4];
+#pragma unroll
+                                for (int p = 0; p < 4; ++p) z[p] = (gu[p][0] + gu[p][1]) + (gu[p][2] + gu[p][3]);
+                                st_gz4<ACC>(gp, e4.x * z[0], e4.y * z[1], e4.z * z[2], e4.w * z[3]);
                             } else {
 #pragma unroll
                                 for (int t4 = 0; t4 < 4; ++t4) {
-                                    const float2 e2 = *reinterpret_cast<const float2*>(ep + (NT + t4) * PL);
-                                    st_gz2<ACC>(gp, e2.x * gu0[t4], e2.y * gu1[t4]);
+                                    const float4 e4 = *reinterpret_cast<const float4*>(ep + (NT + t4) * PL);
+                                    st_gz4<ACC>(gp, e4.x * gu[0][t4], e4.y * gu[1][t4], e4.z * gu[2][t4], e4.w * gu[3][t4]);
                                     gp += hw32;
                                 }
                             }
@@ -453,56 +497,51 @@ __global__ void __launch_bounds__(256, 2)
             }
 
             // -------------------------------------------- B3: upsample transpose
-            // coarse column X receives fine columns 2X-1 (tap j=1), 2X (j=0,1),
-            // 2X+1 (j=0; and j=1 at the last coarse column, W even); coarse row
-            // min((y+i)/2, Hc-1) per fine row y and tap row i
+            // item (coarse column X, channel c).  Coarse X receives fine columns
+            // 2X-1 (tap j=1), 2X (j=0,1), 2X+1 (j=0; and j=1 at the last coarse
+            // column, W even); coarse row (y+i)/2 per fine row y and tap row i,
+            // clamped onto Hc-1 at the image bottom (fixed up below)
             if constexpr (UP) {
-                const int cxi = (tid & 31) * 4 + (tid >> 5);  // items spread over the 4 warps
-                const int X = (x0 >> 1) + cxi;
-                if (cxi < TXC && X < a.Wc) {
-                    const int rj = 2 * cxi + RA;  // smem column of fine x = 2X
-                    const bool lastX = X == a.Wc - 1;
-                    float cv[CROWS][3];
+                if (tid < 3 * TXC) {
+                    const int c = tid / TXC, cxi = tid - c * TXC;
+                    const int X = (x0 >> 1) + cxi;
+                    if (X < a.Wc) {
+                        const int rj = 2 * cxi + RA;  // smem column of fine x = 2X
+                        const bool lastX = X == a.Wc - 1;
+                        float cv[CROWS + 1];
 #pragma unroll
-                    for (int k2 = 0; k2 < CROWS; ++k2)
+                        for (int k2 = 0; k2 <= CROWS; ++k2) cv[k2] = 0.f;
+                        const int cyb = qs >> 1;  // qs is even
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) cv[k2][c] = 0.f;
-                    const int cyb = qs >> 1;  // qs is even
-#pragma unroll
-                    for (int ss = 0; ss < S; ++ss) {
-                        const int qy = qs + ss;
-                        if (qy < H) {
-                            float gm[3], g0[3], gq[3];
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                                const float* gr = s_g + c * PL + ss * RX + rj;
-                                gm[c] = gr[-1];
-                                g0[c] = gr[0];
-                                gq[c] = gr[1];
-                            }
+                        for (int ss = 0; ss < S; ++ss) {
+                            const float* gr = s_g + c * PL + ss * RX + rj;
+                            const float gm = gr[-1], g0 = gr[0], gq = gr[1];
 #pragma unroll
                             for (int ii = 0; ii < 2; ++ii) {
                                 const float* w0 = lgb + (TIED ? NT : NT + 2 * ii) * PL + ss * RX + rj;
                                 const float* w1 = lgb + (TIED ? NT : NT + 2 * ii + 1) * PL + ss * RX + rj;
                                 const float am = w1[-1], a0 = w0[0] + w1[0];
                                 const float aq = lastX ? w0[1] + w1[1] : w0[1];
-                                const int yl = min((qy + ii) >> 1, a.Hc - 1) - cyb;  // 0..2
-#pragma unroll
-                                for (int yy = 0; yy < CROWS; ++yy) {
-                                    if (yy != yl) continue;
-#pragma unroll
-                                    for (int c = 0; c < 3; ++c)
-                                        cv[yy][c] = fmaf(am, gm[c], fmaf(a0, g0[c], fmaf(aq, gq[c], cv[yy][c])));
-                                }
+                                const int yl = (ss + ii) >> 1;  // compile-time after unrolling
+                                cv[yl] = fmaf(am, gm, fmaf(a0, g0, fmaf(aq, gq, cv[yl])));
                             }
                         }
+                        // fine rows past the image contribute nothing (G = 0 there); the
+                        // tap i = 1 of the last fine row of an even-height image points at
+                        // coarse row Hc: clamp it onto Hc - 1
+                        const int yc = a.Hc - cyb;  // local index of coarse row Hc
+#pragma unroll
+                        for (int k2 = 1; k2 <= CROWS; ++k2)
+                            if (k2 == yc) {
+                                cv[k2 - 1] += cv[k2];
+                                cv[k2] = 0.f;
+                            }
+#pragma unroll
+                        for (int k2 = 0; k2 < CROWS; ++k2) s_cac[(((cyb + k2) & (CR - 1)) * 3 + c) * TXC + cxi] += cv[k2];
                     }
-#pragma unroll
-                    for (int k2 = 0; k2 < CROWS; ++k2)
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) s_cac[(((cyb + k2) & (CR - 1)) * 3 + c) * TXC + cxi] += cv[k2][c];
                 }
             }
+
             cta_sync();  // end of step: B2 warps flushed their rows, B3 accumulations done
 
             if constexpr (UP) {
