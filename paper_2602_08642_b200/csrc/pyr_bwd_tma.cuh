@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(256, 2)
     __syncthreads();
     patch_rows(qstart + R - NPRO * S, qstart + R);
 
-    const int s_a = tid >> 6, rw_a = tid & 63;  // phase A: S rows x 64 threads, RW <= 64 used
-    const int ri_a = RA - R + rw_a;               // smem column of this thread's region pixel
-    const bool act_a = rw_a < RW;
+    const int s_a = tid / RW, rw_a = tid - s_a * RW;  // phase A: S rows x RW columns, dense
+    const int ri_a = RA - R + rw_a;                     // smem column of this thread's region pixel
+    const bool act_a = tid < S * RW;
 
     // ------------------------------------------------ A: softmax, G, inner'
     // (every thread; ends with the CTA barrier, the next prefetch and the
@@ -356,17 +356,39 @@ __global__ void __launch_bounds__(256, 2)
     const bool want = a.want_params != 0;
     const bool acc_mode = a.accum != 0;
 
-    if (tid < 128) {
-        // ==================================================== B1 + B3 warps
-        int cnext = qstart >> 1;
-        const int part = B1SPL == 1 ? 0 : tid / SH::B1ITEMS;
-        const int item = tid - part * SH::B1ITEMS;
-        const int s = item / NQUAD, xi = 4 * (item - s * NQUAD), ri = xi + RA;
-        for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
-            const int qs = qstart + i * S;
-            float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
-            phase_a(i, qs, lgb, reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb));
+    // B1 / B3 role (warps 0-3)
+    int cnext = qstart >> 1;
+    const int part = B1SPL == 1 ? 0 : (tid & 127) / SH::B1ITEMS;
+    const int item = (tid & 127) - part * SH::B1ITEMS;
+    const int s = item / NQUAD, xi = 4 * (item - s * NQUAD), ri = xi + RA;
+    // B2 role (warps 4-7)
+    const int b2 = tid & 127;
+    const int col = b2 / B2SPL, part2 = b2 - col * B2SPL;
+    const int gx2 = x0 + col, ri2 = col + RA;
+    const bool act2 = tid >= 128 && col < TXB && gx2 < W;
+    // the lanes of a column split the tap columns dx (window rows stay compile-time)
+    constexpr int DXN = (K + B2SPL - 1) / B2SPL;
+    const int dx0 = -R + part2 * DXN, ndx = min(DXN, R + 1 - dx0);
+    float* const glo = (float*)a.gl_out + (long long)b * a.in_b;
+    float* const gdo = (L0 && a.gdc_out) ? (float*)a.gdc_out + (long long)b * a.in_b : nullptr;
+    // output rows qs - R + k, k in [0, AW), packed in pairs (2p, 2p+1) so
+    // taps d, d+1 landing on one pair go as one FFMA2
+    float2 win[NPW][3];
+#pragma unroll
+    for (int p = 0; p < NPW; ++p)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) win[p][c] = make_float2(0.f, 0.f);
+    auto wget = [&](int k, int c) { return (k & 1) ? win[k >> 1][c].y : win[k >> 1][c].x; };
+    auto wadd = [&](int k, int c, float v) {
+        if (k & 1) win[k >> 1][c].y += v;
+        else win[k >> 1][c].x += v;
+    };
 
+    for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
+        const int qs = qstart + i * S;
+        float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
+        phase_a(i, qs, lgb, reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb));
+        if (tid < 128) {
             // -------------------------------------------- B1: logit gradients
             const int qy = qs + s, gx = x0 + xi;
             // W is a multiple of 4 on this path: the quad (gx .. gx + 3) is in
@@ -431,12 +453,10 @@ __global__ void __launch_bounds__(256, 2)
                             gp += hw32;
                         }
                     };
-#pragma unroll
-                    for (int pp = 0; pp < B1SPL; ++pp) {
-                        if (part == pp) {
-#pragma unroll
-                            for (int dy = -R + pp * SH::DYS; dy < -R + (pp + 1) * SH::DYS && dy <= R; ++dy) tap_row(dy);
-                        }
+                    {
+                        const int dy_lo = -R + part * SH::DYS, dy_hi = min(dy_lo + SH::DYS, R + 1);
+#pragma unroll 1
+                        for (int dy = dy_lo; dy < dy_hi; ++dy) tap_row(dy);
                     }
                     if constexpr (UP) {
                         if (part == B1SPL - 1) {
@@ -542,60 +562,7 @@ __global__ void __launch_bounds__(256, 2)
                 }
             }
 
-            cta_sync();  // end of step: B2 warps flushed their rows, B3 accumulations done
-
-            if constexpr (UP) {
-                // coarse ghat rows finished by this step (all B3 items are in)
-                const bool bottom = qs + S >= H;
-                const int cend = bottom ? a.Hc : (qs + S) >> 1;
-                const int own0 = y0 >> 1, own1 = (y1 + 1) >> 1;
-                for (int k2 = tid; k2 < (cend - cnext) * TXC; k2 += 128) {
-                    const int rr = k2 / TXC, cxi = k2 - rr * TXC;
-                    const int Y = cnext + rr, X = (x0 >> 1) + cxi;
-                    float v[3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        float* p = &s_cac[((Y & (CR - 1)) * 3 + c) * TXC + cxi];
-                        v[c] = *p;
-                        *p = 0.f;
-                    }
-                    if (Y < own0 || Y >= own1 || X >= a.Wc) continue;
-                    float* gc = (float*)a.ghat_c + (long long)b * a.c_b + (long long)Y * a.Wc + X;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        if (c < nc) gc[c * a.c_c] = v[c];
-                }
-                cnext = cend;
-            }
-        }
-    } else {
-        // ==================================================== B2 warps
-        const int b2 = tid - 128;
-        const int col = b2 / B2SPL, part = b2 - col * B2SPL;
-        const int gx = x0 + col, ri = col + RA;
-        const bool act2 = col < TXB && gx < W;
-        // the lanes of a column split the tap columns dx (window rows stay compile-time)
-        constexpr int DXN = (K + B2SPL - 1) / B2SPL;
-        const int dx0 = -R + part * DXN, ndx = min(DXN, R + 1 - dx0);
-        float* const glo = (float*)a.gl_out + (long long)b * a.in_b;
-        float* const gdo = (L0 && a.gdc_out) ? (float*)a.gdc_out + (long long)b * a.in_b : nullptr;
-        // output rows qs - R + k, k in [0, AW), packed in pairs (2p, 2p+1) so
-        // taps d, d+1 landing on one pair go as one FFMA2
-        float2 win[NPW][3];
-#pragma unroll
-        for (int p = 0; p < NPW; ++p)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) win[p][c] = make_float2(0.f, 0.f);
-        auto wget = [&](int k, int c) { return (k & 1) ? win[k >> 1][c].y : win[k >> 1][c].x; };
-        auto wadd = [&](int k, int c, float v) {
-            if (k & 1) win[k >> 1][c].y += v;
-            else win[k >> 1][c].x += v;
-        };
-        for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
-            const int qs = qstart + i * S;
-            float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;
-            phase_a(i, qs, lgb, reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb));
-
+        } else {
             // taps of tap column dx for every source row of the step: window row
             // k = s + d (compile-time), smem column rj = ri - dx (runtime)
             auto gather_dx = [&](int rj, int dx) {
@@ -624,13 +591,13 @@ __global__ void __launch_bounds__(256, 2)
                 // this lane's tap columns: [dx0, dx0 + ndx)
 #pragma unroll
                 for (int j = 0; j < DXN; ++j)
-                    if (j < ndx) gather_dx(ri - (dx0 + j), dx0 + j);
-                if (part == 0 && (gx == 0 || gx == W - 1)) {
+                    if (j < ndx) gather_dx(ri2 - (dx0 + j), dx0 + j);
+                if (part2 == 0 && (gx2 == 0 || gx2 == W - 1)) {
                     // clamp fold along x: taps of in-image sources that land beyond
                     // the border column are gathered onto it (border columns only)
 #pragma unroll 1
                     for (int e = 1; e <= R; ++e) {
-                        const int Pc = gx == 0 ? -e : W - 1 + e;
+                        const int Pc = gx2 == 0 ? -e : W - 1 + e;
 #pragma unroll 1
                         for (int dx = -R; dx <= R; ++dx) {
                             const int qx = Pc - dx;
@@ -684,7 +651,7 @@ __global__ void __launch_bounds__(256, 2)
                 } else {
                     // round 1: halves (pairs PB, PB+1) between lanes part ^ (B2SPL/2)
                     const int hm = B2SPL / 2;
-                    const bool upper = (part & hm) != 0;
+                    const bool upper = (part2 & hm) != 0;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const float2 lo = PB < NPW ? win[PB][c] : make_float2(0.f, 0.f);
@@ -705,7 +672,7 @@ __global__ void __launch_bounds__(256, 2)
                         nrow = 2;
                     } else {
                         // round 2: components between lanes part ^ 1
-                        const bool odd = (part & 1) != 0;
+                        const bool odd = (part2 & 1) != 0;
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             const float send = odd ? keep[c].x : keep[c].y;
@@ -722,11 +689,11 @@ __global__ void __launch_bounds__(256, 2)
                     if (r >= nrow) break;
                     const int P = qs - R + krow + r;
                     if (P < y0 || P >= y1 || P > H - 1) continue;
-                    const unsigned off = (unsigned)P * (unsigned)W + (unsigned)gx;
+                    const unsigned off = (unsigned)P * (unsigned)W + (unsigned)gx2;
                     if constexpr (L0) {
-                        const float* xr = lin_row_step(qs, P, 0) + ri;
-                        const float* dr = lin_row_step(qs, P, 1) + ri;
-                        const float* uor = ring_row(s_up, P) + ri;  // u * out
+                        const float* xr = lin_row_step(qs, P, 0) + ri2;
+                        const float* dr = lin_row_step(qs, P, 1) + ri2;
+                        const float* uor = ring_row(s_up, P) + ri2;  // u * out
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             if (c >= nc) break;
@@ -759,7 +726,30 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
                     win[p][c] = p + S / 2 < NPW ? win[p + S / 2][c] : make_float2(0.f, 0.f);
-            cta_sync();  // end of step
+        }
+        cta_sync();  // end of step
+        if (UP && tid < 128) {
+            // coarse ghat rows finished by this step (all B3 items are in)
+            const bool bottom = qs + S >= H;
+            const int cend = bottom ? a.Hc : (qs + S) >> 1;
+            const int own0 = y0 >> 1, own1 = (y1 + 1) >> 1;
+            for (int k2 = tid; k2 < (cend - cnext) * TXC; k2 += 128) {
+                const int rr = k2 / TXC, cxi = k2 - rr * TXC;
+                const int Y = cnext + rr, X = (x0 >> 1) + cxi;
+                float v[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float* p = &s_cac[((Y & (CR - 1)) * 3 + c) * TXC + cxi];
+                    v[c] = *p;
+                    *p = 0.f;
+                }
+                if (Y < own0 || Y >= own1 || X >= a.Wc) continue;
+                float* gc = (float*)a.ghat_c + (long long)b * a.c_b + (long long)Y * a.Wc + X;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (c < nc) gc[c * a.c_c] = v[c];
+            }
+            cnext = cend;
         }
     }
 }
