@@ -505,6 +505,16 @@ def gpu_arm(args, rank, world, local_rank, dist):
     else:
         dom_name, step_bytes = "bwd_l0", fwd_b + bwd_b
     dom_ms = kern.get(dom_name)
+    # DRAM traffic of the dominant kernel from the committed ncu capture
+    # (tools/ncu_traffic.py -> profiles/ncu_traffic.json), per launch like `achieved`
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        ent = tr.get(args.workload, {}).get(dom_name)
+        if ent:
+            traffic = int(ent["bytes_per_frame"] * B)
+    except (OSError, ValueError, KeyError):
+        pass
     dom_gbs = dom_b * B / (dom_ms * 1e-3) / 1e9 if dom_ms else None
     step_gbs = step_bytes * B / (ms * 1e-3) / 1e9
     res = {
@@ -529,7 +539,7 @@ def gpu_arm(args, rank, world, local_rank, dist):
                      "fwd_l0 (level-0 forward: softmax, k x k gather, upsample, remod)",
                      "achieved": round(dom_gbs, 1) if dom_gbs else None, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s",
-                     "frac": round(dom_gbs / peak, 4) if dom_gbs else None, "traffic": None,
+                     "frac": round(dom_gbs / peak, 4) if dom_gbs else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": dom_b * B,
                      "ms_per_launch": round(dom_ms, 4) if dom_ms else None,
                      "share_of_step": round(dom_ms / ms, 3) if dom_ms else None},
