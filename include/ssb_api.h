@@ -203,6 +203,32 @@ int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* b
                     float* noisy, float* spp_out, uint8_t* taken_out, void* workspace,
                     ssb_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Temporal path -- replaces images.py `warp_array`
+ * (:88-119) and `warp_backward` (:122-147).  Planar: prev/out/grad (B,C,H,W),
+ * motion (B,2,H,W) = (mx, my), validity (B,H,W) (may be NULL).  dtype
+ * SSB_F32 | SSB_F64.  The transpose is a deterministic gather in the
+ * reference's summation order (float64: bit-exact); workspace: B x 8 bytes.
+ * ---------------------------------------------------------------------- */
+int ssb_warp(int dtype, int B, int C, int H, int W, const void* prev, const void* motion,
+             void* out, void* validity, ssb_stream_t stream);
+int ssb_warp_backward_workspace_bytes(int B, size_t* bytes);
+int ssb_warp_backward(int dtype, int B, int C, int H, int W, const void* grad_out,
+                      const void* motion, void* grad_prev, void* workspace, ssb_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Estimator backward to the density scores --
+ * replaces optimize.py:244-251 (g_spp = sum_f sum_c g_input * grad_density,
+ * scipy gaussian_filter(sigma, mode="nearest"), then 7/8*budget*N *
+ * density.softmax_backward(softmax(scores), g_spp), density.py:43-52).
+ * g_input / grad_density (B,F,C,H,W) planar, scores and g_scores (B,H,W);
+ * dtype SSB_F32 | SSB_F64 (float64 arithmetic inside).  sigma = 0: no blur.
+ * ---------------------------------------------------------------------- */
+int ssb_score_grad_workspace_bytes(int B, int H, int W, size_t* bytes);
+int ssb_score_grad(int dtype, int B, int F, int C, int H, int W, const void* g_input,
+                   const void* grad_density, const void* scores, double budget, double sigma,
+                   void* g_scores, void* workspace, ssb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

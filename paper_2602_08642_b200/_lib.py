@@ -27,6 +27,8 @@ EXPORTS = (
     "ssb_softmax_channels", "ssb_gather", "ssb_upsample2", "ssb_avgpool2",
     "ssb_uniform_grid", "ssb_density_workspace_bytes", "ssb_normalize_density",
     "ssb_allocate", "ssb_stochastic_core", "ssb_estimate", "ssb_place_fused",
+    "ssb_warp", "ssb_warp_backward_workspace_bytes", "ssb_warp_backward",
+    "ssb_score_grad_workspace_bytes", "ssb_score_grad",
 )
 
 vp = C.c_void_p
@@ -120,6 +122,12 @@ def load(build_if_missing: bool = False):
             "ssb_stochastic_core": (C.c_int, [P(EstimateDesc)] + [vp] * 10),
             "ssb_estimate": (C.c_int, [P(EstimateDesc)] + [vp] * 11),
             "ssb_place_fused": (C.c_int, [P(PlaceDesc)] + [vp] * 7),
+            "ssb_warp": (C.c_int, [C.c_int] * 5 + [vp] * 5),
+            "ssb_warp_backward_workspace_bytes": (C.c_int, [C.c_int, P(C.c_size_t)]),
+            "ssb_warp_backward": (C.c_int, [C.c_int] * 5 + [vp] * 5),
+            "ssb_score_grad_workspace_bytes": (C.c_int, [C.c_int] * 3 + [P(C.c_size_t)]),
+            "ssb_score_grad": (C.c_int, [C.c_int] * 6 + [vp, vp, vp, C.c_double, C.c_double,
+                                                         vp, vp, vp]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(lib, name)

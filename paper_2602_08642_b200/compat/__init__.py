@@ -6,7 +6,7 @@
     compat.uninstall()
 
 ``install()`` patches both the defining modules (sparse_sampler.pyramid,
-.density, .estimators, .rng) and every module that bound the names at import
+.density, .estimators, .rng, .images) and every module that bound the names at import
 time (sparse_sampler.optimize, sparse_sampler.estimators, the package
 namespace), and makes the patched functions return the
 reference's own container classes.  Without the reference installed, the
@@ -19,7 +19,7 @@ import importlib
 import importlib.util
 import sys
 
-from . import _dev, _types, density, estimators, pyramid, rng  # noqa: F401
+from . import _dev, _types, density, estimators, images, pyramid, rng  # noqa: F401
 from ._dev import precision, set_precision  # noqa: F401
 
 # name -> compat module providing it, per reference module
@@ -30,8 +30,10 @@ PATCHES = {
     "estimators": ["stochastic_core", "estimate", "estimate_stochastic", "estimate_relaxed",
                    "estimate_straight_through", "estimate_gumbel"],
     "rng": ["uniform_grid", "uniform_grid_batch", "pixel_uniform"],
+    "images": ["warp_array", "warp_backward"],
 }
-_COMPAT = {"pyramid": pyramid, "density": density, "estimators": estimators, "rng": rng}
+_COMPAT = {"pyramid": pyramid, "density": density, "estimators": estimators, "rng": rng,
+           "images": images}
 _saved: list = []
 _saved_types: dict | None = None
 

@@ -68,3 +68,21 @@ def allocate(density, mode: str = "stochastic", mask=None, frame: int = 0, seed:
                                         rule=rule, gumbel_temp=gumbel_temp)
     return _types.make("SampleAllocation", _dev.to_host(base[0]), _dev.to_host(frac[0]),
                        _dev.to_host(u[0]), _dev.to_host(taken[0]))
+
+
+def score_gradient(scores, budget: float, g_inputs, grad_densities, blur: float = 1.5):
+    """The sampler half of optimize.evaluate_step (optimize.py:244-251) as one
+    GPU call: g_spp = sum over frames of sum_c g_input * grad_density, blurred
+    by gaussian_filter(blur, mode="nearest"), then
+    7/8 * budget * N * softmax_backward(softmax(scores), g_spp).
+    scores (H, W); g_inputs / grad_densities: sequences over frames of (H, W, C)."""
+    scores = np.asarray(scores, dtype=np.float64)
+    gi = np.stack([np.asarray(a, dtype=np.float64) for a in g_inputs])
+    gd = np.stack([np.asarray(a, dtype=np.float64) for a in grad_densities])
+    if gi.shape != gd.shape or gi.shape[1:3] != scores.shape:
+        raise ValueError("score gradient: dimensions must match")
+    dt = _dev.dtype()
+    gi_t = _dev.to_dev(np.ascontiguousarray(gi.transpose(0, 3, 1, 2))[None], dt)
+    gd_t = _dev.to_dev(np.ascontiguousarray(gd.transpose(0, 3, 1, 2))[None], dt)
+    out = ops.score_grad(_dev.to_dev(scores, dt)[None], gi_t, gd_t, float(budget), float(blur))
+    return _dev.to_host(out[0]).astype(np.float64)

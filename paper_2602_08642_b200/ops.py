@@ -411,3 +411,90 @@ def place_fused(scores, bank, budget: float, seed: int = 0, frame0: int = 0, noi
                                   _ptr(taken), _ptr(workspace), _stream(scores.device)),
               "ssb_place_fused")
     return noisy, spp, taken
+
+
+# ---------------------------------------------------------------------------
+# temporal path: images.py warp_array / warp_backward
+
+
+def _img_dtype(t, name):
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"{name} must be float32 or float64")
+    return _DT[t.dtype]
+
+
+def warp(prev, motion, want_validity=True):
+    """Bilinear backward warp (ref `warp_array`, images.py:88-119).
+    prev (B, C, H, W), motion (B, 2, H, W) = (mx, my), same dtype ->
+    (out (B, C, H, W), validity (B, H, W) or None)."""
+    lib = _lib.load()
+    _need(prev, "prev")
+    _need(motion, "motion", prev.device, prev.dtype)
+    dt = _img_dtype(prev, "prev")
+    if prev.dim() != 4 or motion.dim() != 4 or motion.shape[1] != 2 or \
+            prev.shape[0] != motion.shape[0] or prev.shape[2:] != motion.shape[2:]:
+        raise ValueError("warp: image and motion dimensions must match")
+    B, Cc, H, W = prev.shape
+    out = torch.empty_like(prev)
+    val = torch.empty((B, H, W), dtype=prev.dtype, device=prev.device) if want_validity else None
+    with torch.cuda.device(prev.device):
+        check(lib.ssb_warp(dt, B, Cc, H, W, _ptr(prev), _ptr(motion), _ptr(out), _ptr(val),
+                           _stream(prev.device)), "ssb_warp")
+    return out, val
+
+
+def warp_backward(grad_out, motion):
+    """Transpose of `warp` w.r.t. prev (ref `warp_backward`, images.py:122-147):
+    a deterministic gather in the reference's summation order."""
+    lib = _lib.load()
+    _need(grad_out, "grad_out")
+    _need(motion, "motion", grad_out.device, grad_out.dtype)
+    dt = _img_dtype(grad_out, "grad_out")
+    if grad_out.dim() != 4 or motion.dim() != 4 or motion.shape[1] != 2 or \
+            grad_out.shape[0] != motion.shape[0] or grad_out.shape[2:] != motion.shape[2:]:
+        raise ValueError("warp: image and motion dimensions must match")
+    B, Cc, H, W = grad_out.shape
+    wb = C.c_size_t()
+    check(lib.ssb_warp_backward_workspace_bytes(B, C.byref(wb)), "ssb_warp_backward_workspace_bytes")
+    ws = torch.empty(wb.value, dtype=torch.uint8, device=grad_out.device)
+    gp = torch.empty_like(grad_out)
+    with torch.cuda.device(grad_out.device):
+        check(lib.ssb_warp_backward(dt, B, Cc, H, W, _ptr(grad_out), _ptr(motion), _ptr(gp), _ptr(ws),
+                                    _stream(grad_out.device)), "ssb_warp_backward")
+    return gp
+
+
+# ---------------------------------------------------------------------------
+# estimator backward to the density scores (SURVEY.md 8(f) row 3)
+
+
+def score_grad(scores, g_input, grad_density, budget: float, sigma: float = 1.5):
+    """Gradient of the loss w.r.t. the density scores (optimize.py:244-251):
+    scores (B, H, W); g_input / grad_density (B, F, C, H, W) -- per frame the
+    filter's input gradient and the estimator's d(noisy)/d(spp).  Returns
+    g_scores (B, H, W), same dtype (float64 arithmetic inside)."""
+    lib = _lib.load()
+    _need(scores, "scores")
+    dt = _img_dtype(scores, "scores")
+    _need(g_input, "g_input", scores.device, scores.dtype)
+    _need(grad_density, "grad_density", scores.device, scores.dtype)
+    if scores.dim() == 2:
+        scores = scores[None]
+    if g_input.dim() == 4:
+        g_input, grad_density = g_input[None], grad_density[None]
+    B, H, W = scores.shape
+    if g_input.dim() != 5 or g_input.shape != grad_density.shape or g_input.shape[0] != B or \
+            tuple(g_input.shape[3:]) != (H, W):
+        raise ValueError("score_grad: g_input / grad_density must be (B, F, C, H, W) matching scores")
+    if not budget > 0:
+        raise ValueError("budget must be positive")
+    F, Cc = g_input.shape[1], g_input.shape[2]
+    wb = C.c_size_t()
+    check(lib.ssb_score_grad_workspace_bytes(B, H, W, C.byref(wb)), "ssb_score_grad_workspace_bytes")
+    ws = torch.empty(wb.value, dtype=torch.uint8, device=scores.device)
+    out = torch.empty_like(scores)
+    with torch.cuda.device(scores.device):
+        check(lib.ssb_score_grad(dt, B, F, Cc, H, W, _ptr(g_input), _ptr(grad_density), _ptr(scores),
+                                 float(budget), float(sigma), _ptr(out), _ptr(ws),
+                                 _stream(scores.device)), "ssb_score_grad")
+    return out

@@ -6,7 +6,8 @@ Run in the build container (the reference is not present on the GPU box):
         python tests/golden/make_golden.py
 
 Every array stored here is an output of the reference's own functions
-(`sparse_sampler.pyramid`, `.density`, `.rng`, `.estimators`, `.banks`) on
+(`sparse_sampler.pyramid`, `.density`, `.rng`, `.estimators`, `.banks`,
+`.images`, and scipy's gaussian_filter exactly as optimize.py calls it) on
 seeded inputs that are stored alongside.  The oracle is pinned against these
 files (tests/test_oracle_golden.py) and the GPU parity tests reuse them.
 Level counts other than the reference's default 5 are produced by setting
@@ -30,7 +31,9 @@ import sparse_sampler.pyramid as P  # noqa: E402
 from sparse_sampler import density as D  # noqa: E402
 from sparse_sampler import estimators as E  # noqa: E402
 from sparse_sampler import rng as R  # noqa: E402
+from sparse_sampler import images as I  # noqa: E402
 from sparse_sampler.banks import SampleBank  # noqa: E402
+from scipy.ndimage import gaussian_filter  # noqa: E402  (the reference's own blur, optimize.py:20)
 
 PYRAMID_CASES = [
     # name, H, W, levels, demod, prev, want_param_grads, logit scale
@@ -156,14 +159,87 @@ def placement(seed):
     return d
 
 
-def main():
-    for i, case in enumerate(PYRAMID_CASES):
-        d = pyramid_case(*case, seed=1000 + i)
-        np.savez_compressed(os.path.join(HERE, f"{case[0]}.npz"), **d)
-    np.savez_compressed(os.path.join(HERE, "primitives.npz"), **primitives(77))
-    np.savez_compressed(os.path.join(HERE, "placement.npz"), **placement(88))
-    print("wrote", len(PYRAMID_CASES) + 2, "fixtures to", HERE)
+WARP_CASES = [
+    # name, H, W, C, motion kind
+    ("subpixel", 11, 13, 3, "uniform3"),
+    ("integer", 9, 7, 3, "integer"),
+    ("zero", 6, 8, 3, "zero"),
+    ("large", 10, 12, 2, "uniform9"),
+    ("single_channel", 5, 16, 1, "uniform2"),
+]
+
+
+def temporal(seed):
+    """images.warp_array / warp_backward (images.py:88-147) on seeded inputs."""
+    rng = np.random.default_rng(seed)
+    d = {}
+    for name, h, w, c, kind in WARP_CASES:
+        if kind == "zero":
+            motion = np.zeros((h, w, 2))
+        elif kind == "integer":
+            motion = rng.integers(-2, 3, (h, w, 2)).astype(np.float64)
+        else:
+            a = float(kind[len("uniform"):])
+            motion = rng.uniform(-a, a, (h, w, 2))
+        prev = rng.lognormal(-1.0, 1.5, (h, w, c))
+        gout = rng.normal(0.0, 1.0, (h, w, c))
+        out, valid = I.warp_array(prev, motion)
+        d[f"{name}_motion"], d[f"{name}_prev"], d[f"{name}_gout"] = motion, prev, gout
+        d[f"{name}_out"], d[f"{name}_validity"] = out, valid
+        d[f"{name}_gprev"] = I.warp_backward(gout, motion)
+    d["names"] = np.array([c[0] for c in WARP_CASES])
+    return d
+
+
+SCORE_CASES = [
+    # name, H, W, frames, channels, budget, sigma
+    ("blur", 12, 10, 2, 3, 0.25, 1.5),
+    ("noblur", 9, 14, 2, 3, 0.5, 0.0),
+    ("wide", 16, 16, 1, 3, 1.0, 2.5),
+]
+
+
+def scores(seed):
+    """The sampler half of optimize.evaluate_step (optimize.py:244-251) written
+    with the reference's own functions: density.softmax / softmax_backward and
+    scipy's gaussian_filter(mode="nearest")."""
+    rng = np.random.default_rng(seed)
+    d = {}
+    for name, h, w, f, c, budget, sigma in SCORE_CASES:
+        sc = rng.normal(0.0, 1.0, (h, w))
+        gi = rng.normal(0.0, 1.0, (f, h, w, c))
+        gd = rng.normal(0.0, 1.0, (f, h, w, c)) * rng.uniform(0.1, 2.0, (f, h, w, 1))
+        g_spp = None
+        for k in range(f):
+            t = (gi[k] * gd[k]).sum(axis=-1)
+            g_spp = t if g_spp is None else g_spp + t
+        if sigma > 0:
+            g_spp = gaussian_filter(g_spp, sigma, mode="nearest")
+        wts = D.softmax(sc)
+        total = (7.0 / 8.0) * budget * wts.size
+        d[f"{name}_scores"], d[f"{name}_gin"], d[f"{name}_gd"] = sc, gi, gd
+        d[f"{name}_budget"], d[f"{name}_sigma"] = np.float64(budget), np.float64(sigma)
+        d[f"{name}_gspp"] = g_spp
+        d[f"{name}_gscores"] = total * D.softmax_backward(wts, g_spp)
+    d["names"] = np.array([c[0] for c in SCORE_CASES])
+    return d
+
+
+def main(which=None):
+    which = set(which or ["pyramid", "primitives", "placement", "temporal", "scores"])
+    n = 0
+    if "pyramid" in which:
+        for i, case in enumerate(PYRAMID_CASES):
+            d = pyramid_case(*case, seed=1000 + i)
+            np.savez_compressed(os.path.join(HERE, f"{case[0]}.npz"), **d)
+            n += 1
+    for name, fn, seed in (("primitives", primitives, 77), ("placement", placement, 88),
+                           ("temporal", temporal, 99), ("scores", scores, 111)):
+        if name in which:
+            np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **fn(seed))
+            n += 1
+    print("wrote", n, "fixtures to", HERE)
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])  # e.g. `make_golden.py temporal scores` regenerates only those

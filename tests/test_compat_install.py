@@ -35,6 +35,9 @@ def test_install_patches_definers_and_importers(ref_pkg):
         assert O.allocate is compat.density.allocate and D.allocate is compat.density.allocate
         assert O.estimate is compat.estimators.estimate
         assert ref_pkg.allocate is compat.density.allocate
+        import sparse_sampler.images as I
+        assert I.warp_array is compat.images.warp_array
+        assert O.warp_array is compat.images.warp_array and O.warp_backward is compat.images.warp_backward
         # results are built from the reference's own classes while installed
         assert compat._types.TYPES["DensityMap"] is D.DensityMap
         assert compat.install()  # idempotent

@@ -308,3 +308,57 @@ def test_stochastic_core_broadcasts_leading_axis(cp):
     ref = oe.stochastic_core("relaxed", spp, frac, u, bs, ho, lam=10.0)
     for a, b in zip(got, ref):
         np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- temporal warp
+# mirrors pkg/tests/test_images.py::TestWarp on the drop-in (f64 and f32)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_warp_kats(cp, precision):
+    cp.set_precision(precision)
+    try:
+        rng = np.random.default_rng(0)
+        img = rng.uniform(0, 5, (6, 8, 3))
+        out, validity = cp.images.warp_array(img, np.zeros((6, 8, 2)))
+        np.testing.assert_allclose(out, img, rtol=1e-6)
+        np.testing.assert_allclose(validity, 1.0)
+        img = rng.uniform(0, 5, (6, 10, 3))
+        out, _ = cp.images.warp_array(img, np.tile([3.0, 0.0], (6, 10, 1)))
+        np.testing.assert_allclose(out[:, :7], img[:, 3:], rtol=1e-6)
+        out, validity = cp.images.warp_array(np.ones((4, 4, 3)), np.tile([100.0, 0.0], (4, 4, 1)))
+        np.testing.assert_array_equal(out, 0.0)
+        np.testing.assert_array_equal(validity, 0.0)
+        a, b = rng.uniform(0, 3, (5, 5, 3)), rng.uniform(0, 3, (5, 5, 3))
+        m = rng.uniform(-1.5, 1.5, (5, 5, 2))
+        wab, _ = cp.images.warp_array(2.0 * a + 3.0 * b, m)
+        np.testing.assert_allclose(wab, 2.0 * cp.images.warp_array(a, m)[0] + 3.0 * cp.images.warp_array(b, m)[0],
+                                   rtol=1e-5)
+        img = rng.uniform(0, 2, (6, 7, 3))
+        m = rng.uniform(-2, 2, (6, 7, 2))
+        g = rng.normal(0, 1, (6, 7, 3))
+        out, _ = cp.images.warp_array(img, m)
+        gin = cp.images.warp_backward(g, m)
+        assert np.isclose((out * g).sum(), (img * gin).sum(), rtol=1e-5)
+        with pytest.raises(ValueError):
+            cp.images.warp_array(img, np.zeros((5, 7, 2)))
+    finally:
+        cp.set_precision("f64")
+
+
+def test_warp_golden_through_compat(cp):
+    d = load("temporal")
+    for n in d["names"]:
+        out, val = cp.images.warp_array(d[f"{n}_prev"], d[f"{n}_motion"])
+        np.testing.assert_array_equal(out, d[f"{n}_out"])
+        np.testing.assert_array_equal(val, d[f"{n}_validity"])
+        np.testing.assert_array_equal(cp.images.warp_backward(d[f"{n}_gout"], d[f"{n}_motion"]), d[f"{n}_gprev"])
+
+
+def test_score_gradient_golden_through_compat(cp):
+    d = load("scores")
+    for n in d["names"]:
+        r = cp.density.score_gradient(d[f"{n}_scores"], float(d[f"{n}_budget"]), list(d[f"{n}_gin"]),
+                                      list(d[f"{n}_gd"]), float(d[f"{n}_sigma"]))
+        ref = d[f"{n}_gscores"]
+        np.testing.assert_allclose(r, ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())

@@ -129,3 +129,36 @@ def test_radius_generalised_gradcheck(k):
             arr[idx] = old
             fd = (lp - lm) / (2 * eps)
             assert abs(grad[idx] - fd) <= 1e-5 * max(1.0, abs(fd))
+
+
+def test_temporal_warp_bit_exact():
+    """oracle/temporal.py vs images.warp_array / warp_backward (8(f) row 2)."""
+    from oracle import temporal as ot
+    d = load("temporal")
+    for n in d["names"]:
+        out, val = ot.warp_array(d[f"{n}_prev"], d[f"{n}_motion"])
+        np.testing.assert_array_equal(out, d[f"{n}_out"])
+        np.testing.assert_array_equal(val, d[f"{n}_validity"])
+        np.testing.assert_array_equal(ot.warp_backward(d[f"{n}_gout"], d[f"{n}_motion"]), d[f"{n}_gprev"])
+
+
+def test_temporal_warp_adjoint():
+    from oracle import temporal as ot
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(9, 11, 3))
+    g = rng.normal(size=(9, 11, 3))
+    m = rng.uniform(-4, 4, (9, 11, 2))
+    lhs = (ot.warp_array(x, m)[0] * g).sum()
+    rhs = (x * ot.warp_backward(g, m)).sum()
+    assert abs(lhs - rhs) < 1e-12 * max(1.0, abs(lhs))
+
+
+def test_score_grad_bit_exact():
+    """oracle/scores.py vs the reference's softmax_backward chain with scipy's
+    gaussian_filter (optimize.py:244-251; 8(f) row 3)."""
+    from oracle import scores as osc
+    d = load("scores")
+    for n in d["names"]:
+        r = osc.score_grad(d[f"{n}_scores"], float(d[f"{n}_budget"]), list(d[f"{n}_gin"]),
+                           list(d[f"{n}_gd"]), float(d[f"{n}_sigma"]))
+        np.testing.assert_array_equal(r, d[f"{n}_gscores"])
