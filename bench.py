@@ -634,7 +634,8 @@ def main():
 
 
 def also_measurements():
-    """Second BASELINE config on the same box: c3 (4K, L4, k7, bf16 logits)."""
+    """The other BASELINE configs on the same box: c3 (4K, L4, k7, bf16
+    logits), c4b (8K fwd), and the 8(f) rows (temporal warp, score gradient)."""
     import torch
     out = {}
     frames, H, W, L, k, ldt, desc = WORKLOADS["c3"]
@@ -664,6 +665,62 @@ def also_measurements():
                   "ms_per_frame": round(ms, 4),
                   "fwd_frac_of_hbm": round(fwd_b / (ms * 1e-3) / 1e9 / peak, 4),
                   "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
+    del noisy, demod, logits, up, r
+    torch.cuda.empty_cache()
+    out.update(next_rows(peak))
+    return out
+
+
+def _time_cuda(fn, steps=20, warmup=3):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def next_rows(peak):
+    """SURVEY.md 8(f) rows measured on the same box: the temporal warp and its
+    transpose (8 x 1080p, fp32, |motion| <= 2 px) and the estimator backward to
+    the density scores (8 x 1080p, fp32, 2 frames, sigma 1.5).  Algorithmic
+    bytes: warp 36 B/px (prev, motion, out, validity), transpose 32 B/px
+    (grad_out, motion, grad_prev), score grad 56 B/px (2 frames of g_input and
+    grad_density, scores, g_scores)."""
+    import torch
+
+    from paper_2602_08642_b200 import ops
+    B, H, W = 8, 1080, 1920
+    n = B * H * W
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    dev = torch.device("cuda")
+    prev = torch.rand((B, 3, H, W), device=dev, generator=gen)
+    motion = (torch.rand((B, 2, H, W), device=dev, generator=gen) - 0.5) * 4
+    g = torch.randn((B, 3, H, W), device=dev, generator=gen)
+    ms_w = _time_cuda(lambda: ops.warp(prev, motion))
+    ms_b = _time_cuda(lambda: ops.warp_backward(g, motion))
+    out = {"temporal_warp": {
+        "workload": "8 x 1920x1080 fp32, 3 channels, motion U(-2, 2) px",
+        "warp_mpix_s": round(n / (ms_w * 1e-3) / 1e6, 1), "warp_ms": round(ms_w, 4),
+        "warp_frac_of_hbm": round(36 * n / (ms_w * 1e-3) / 1e9 / peak, 4),
+        "transpose_mpix_s": round(n / (ms_b * 1e-3) / 1e6, 1), "transpose_ms": round(ms_b, 4),
+        "transpose_frac_of_hbm": round(32 * n / (ms_b * 1e-3) / 1e9 / peak, 4)}}
+    del prev, motion, g
+    sc = torch.randn((B, H, W), device=dev, generator=gen)
+    gi = torch.randn((B, 2, 3, H, W), device=dev, generator=gen)
+    gd = torch.randn((B, 2, 3, H, W), device=dev, generator=gen)
+    ms_s = _time_cuda(lambda: ops.score_grad(sc, gi, gd, 0.25, 1.5))
+    out["score_grad"] = {
+        "workload": "8 x 1920x1080 fp32 (float64 reductions), 2 frames, blur sigma 1.5",
+        "mpix_s": round(n / (ms_s * 1e-3) / 1e6, 1), "ms": round(ms_s, 4),
+        "frac_of_hbm": round(56 * n / (ms_s * 1e-3) / 1e9 / peak, 4)}
+    del sc, gi, gd
+    torch.cuda.empty_cache()
     return out
 
 

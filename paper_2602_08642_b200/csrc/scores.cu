@@ -11,6 +11,7 @@
 // few bytes per pixel; the reductions are deterministic two-level trees).
 #include <math.h>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -27,19 +28,21 @@ struct BlurWeights {
     int r;
 };
 
+// block-wide reduction for 256-thread blocks of any shape (linear thread id)
 __device__ __forceinline__ double sg_block_reduce(double v, bool is_max) {
     __shared__ double sh[kSgThreads / 32];
+    const int t = threadIdx.y * blockDim.x + threadIdx.x;
     for (int o = 16; o > 0; o >>= 1) {
-        const double t = __shfl_xor_sync(0xffffffffu, v, o);
-        v = is_max ? fmax(v, t) : v + t;
+        const double u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmax(v, u) : v + u;
     }
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    if ((t & 31) == 0) sh[t >> 5] = v;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        v = threadIdx.x < kSgThreads / 32 ? sh[threadIdx.x] : (is_max ? -INFINITY : 0.0);
+    if (t < 32) {
+        v = t < kSgThreads / 32 ? sh[t] : (is_max ? -INFINITY : 0.0);
         for (int o = 16; o > 0; o >>= 1) {
-            const double t = __shfl_xor_sync(0xffffffffu, v, o);
-            v = is_max ? fmax(v, t) : v + t;
+            const double u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = is_max ? fmax(v, u) : v + u;
         }
     }
     __syncthreads();
@@ -136,6 +139,165 @@ __global__ void k_sg_apply(long long n, const T* __restrict__ scores, const doub
     }
 }
 
+
+// ---- fused path (blur radius <= 16): dot + score max, tiled 2-D blur + the
+// softmax partial sums, per-frame reduction, apply -- three passes over the
+// pixels instead of six
+constexpr int SG_TX = 32, SG_TY = 8, SG_RMAX = 16;
+constexpr int kDotBlocks = 1024;  // dot + max pass: blocks per frame
+
+template <typename T>
+__device__ __forceinline__ double sg_exp(T s, double m) {
+    if constexpr (sizeof(T) == 8) return exp(s - m);
+    else return (double)__expf((float)((double)s - m));  // float32 path: 2-ulp exp
+}
+
+// float32 inputs compute the per-pixel dot and the blur in float32 (the
+// reductions stay float64); float64 inputs keep float64 throughout
+template <typename T>
+using acc_t = typename std::conditional<sizeof(T) == 8, double, float>::type;
+
+template <typename T>
+__global__ void k_score_dot_max(int F, int C, long long n, const T* __restrict__ gin, const T* __restrict__ gd,
+                                const T* __restrict__ scores, acc_t<T>* __restrict__ gspp, double* pmax) {
+    using A = acc_t<T>;
+    const int b = blockIdx.y;
+    double m = -INFINITY;
+    for (long long p = (long long)blockIdx.x * kSgThreads + threadIdx.x; p < n; p += (long long)gridDim.x * kSgThreads) {
+        A tot = (A)0;
+        for (int f = 0; f < F; ++f) {
+            const long long base = ((long long)(b * F + f) * C) * n + p;
+            A s = (A)gin[base] * (A)gd[base];
+            for (int c = 1; c < C; ++c) s = s + (A)gin[base + c * n] * (A)gd[base + c * n];
+            tot = f == 0 ? s : tot + s;
+        }
+        gspp[(long long)b * n + p] = tot;
+        m = fmax(m, (double)scores[(long long)b * n + p]);
+    }
+    m = sg_block_reduce(m, true);
+    if (threadIdx.x == 0) pmax[b * kDotBlocks + blockIdx.x] = m;
+}
+
+__global__ void k_max_reduce(const double* __restrict__ pmax, double* __restrict__ fmaxv) {
+    const int b = blockIdx.x;
+    double m = -INFINITY;
+    for (int k = threadIdx.x; k < kDotBlocks; k += kSgThreads) m = fmax(m, pmax[b * kDotBlocks + k]);
+    m = sg_block_reduce(m, true);
+    if (threadIdx.x == 0) fmaxv[b] = m;
+}
+
+// blur (axis 0 then axis 1, scipy order) of one 32 x 8 tile from shared
+// memory; writes the blurred g and the block's partial sums of e and e * g
+template <typename T>
+__global__ void __launch_bounds__(SG_TX * SG_TY) k_blur_sums(int H, int W, BlurWeights bw,
+                                                             const acc_t<T>* __restrict__ g0,
+                                                             const T* __restrict__ scores,
+                                                             const double* __restrict__ pmax,
+                                                             acc_t<T>* __restrict__ g1, double* __restrict__ pse,
+                                                             double* __restrict__ psd) {
+    using A = acc_t<T>;
+    __shared__ A s_in[(SG_TY + 2 * SG_RMAX) * (SG_TX + 2 * SG_RMAX)];
+    __shared__ A s_v[SG_TY * (SG_TX + 2 * SG_RMAX)];
+    __shared__ A s_w[SG_RMAX + 1];
+    __shared__ double s_m;
+    const int b = blockIdx.z, r = bw.r;
+    const int x0 = blockIdx.x * SG_TX, y0 = blockIdx.y * SG_TY;
+    const int tid = threadIdx.y * SG_TX + threadIdx.x;
+    const int nx = SG_TX + 2 * r, ny = SG_TY + 2 * r;
+    const A* gb = g0 + (long long)b * H * W;
+    if (tid == 0) s_m = pmax[b];  // per-frame max (k_max_reduce)
+    if (tid <= r) s_w[tid] = (A)bw.w[tid];
+    for (int i = tid; i < nx * ny; i += SG_TX * SG_TY) {
+        const int yy = clampi(y0 - r + i / nx, 0, H - 1), xx = clampi(x0 - r + i % nx, 0, W - 1);
+        s_in[i] = gb[(long long)yy * W + xx];
+    }
+    __syncthreads();
+    for (int i = tid; i < SG_TY * nx; i += SG_TX * SG_TY) {  // axis 0
+        const int ty = i / nx, tx = i % nx;
+        const A* c = s_in + (ty + r) * nx + tx;
+        A v = c[0] * s_w[0];
+        for (int j = r; j >= 1; --j) v = v + (c[-j * nx] + c[j * nx]) * s_w[j];
+        s_v[ty * nx + tx] = v;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+    double se = 0.0, sd = 0.0;
+    if (x < W && y < H) {
+        const A* c = s_v + threadIdx.y * nx + threadIdx.x + r;
+        A v = c[0] * s_w[0];  // axis 1
+        for (int j = r; j >= 1; --j) v = v + (c[-j] + c[j]) * s_w[j];
+        const long long o = (long long)b * H * W + (long long)y * W + x;
+        g1[o] = v;
+        const double e = sg_exp(scores[o], s_m);
+        se = e;
+        sd = e * (double)v;
+    }
+    se = sg_block_reduce(se, false);
+    sd = sg_block_reduce(sd, false);
+    if (tid == 0) {  // (the reduced value lives in thread 0)
+        const long long k = ((long long)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        pse[k] = se;
+        psd[k] = sd;
+    }
+}
+
+// per-frame totals of the tile partials (fixed order: deterministic)
+__global__ void k_sums_reduce(int nblk, const double* __restrict__ pse, const double* __restrict__ psd,
+                              double* __restrict__ tot) {
+    const int b = blockIdx.x;
+    double se = 0.0, sd = 0.0;
+    for (int k = threadIdx.x; k < nblk; k += kSgThreads) {
+        se += pse[(long long)b * nblk + k];
+        sd += psd[(long long)b * nblk + k];
+    }
+    se = sg_block_reduce(se, false);
+    sd = sg_block_reduce(sd, false);
+    if (threadIdx.x == 0) {
+        tot[2 * b] = se;
+        tot[2 * b + 1] = sd;
+    }
+}
+
+template <typename T>
+__global__ void k_sg_apply_tot(long long n, const T* __restrict__ scores, const acc_t<T>* __restrict__ g,
+                               const double* pmax, const double* __restrict__ tot, double total, T* __restrict__ out) {
+    const int b = blockIdx.y;
+    __shared__ double sm, ss, inner;
+    if (threadIdx.x == 0) {
+        sm = pmax[b];
+        ss = tot[2 * b];
+        inner = tot[2 * b + 1] / ss;  // sum(w * g)
+    }
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * kSgThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kSgThreads) {
+        const double w = sg_exp(scores[(long long)b * n + i], sm) / ss;
+        out[(long long)b * n + i] = (T)(total * (w * ((double)g[(long long)b * n + i] - inner)));
+    }
+}
+
+template <typename T>
+int score_grad_fused(int B, int F, int C, int H, int W, const T* gin, const T* gd, const T* sc, double total,
+                     const BlurWeights& bw, T* out, char* ws, cudaStream_t s) {
+    const long long n = (long long)H * W;
+    using A = acc_t<T>;
+    A* g0 = (A*)ws;
+    A* g1 = g0 + (size_t)B * n;
+    dim3 tgrid((W + SG_TX - 1) / SG_TX, (H + SG_TY - 1) / SG_TY, B);
+    const int nblk = tgrid.x * tgrid.y;
+    double* pmax = (double*)(ws + 2 * (size_t)B * n * sizeof(double));  // B x kDotBlocks
+    double* fmx = pmax + (size_t)B * kDotBlocks;  // B
+    double* pse = fmx + B;
+    double* psd = pse + (size_t)B * nblk;
+    double* tot = psd + (size_t)B * nblk;
+    SSB_LAUNCH(s, k_score_dot_max<T><<<dim3(kDotBlocks, B), kSgThreads, 0, s>>>(F, C, n, gin, gd, sc, g0, pmax));
+    SSB_LAUNCH(s, k_max_reduce<<<B, kSgThreads, 0, s>>>(pmax, fmx));
+    SSB_LAUNCH(s, k_blur_sums<T><<<tgrid, dim3(SG_TX, SG_TY), 0, s>>>(H, W, bw, g0, sc, fmx, g1, pse, psd));
+    SSB_LAUNCH(s, k_sums_reduce<<<B, kSgThreads, 0, s>>>(nblk, pse, psd, tot));
+    const unsigned ag = (unsigned)((n + kSgThreads - 1) / kSgThreads < 4096 ? (n + kSgThreads - 1) / kSgThreads : 4096);
+    SSB_LAUNCH(s, k_sg_apply_tot<T><<<dim3(ag, B), kSgThreads, 0, s>>>(n, sc, g1, fmx, tot, total, out));
+    return 0;
+}
+
 }  // namespace ssb
 
 using namespace ssb;
@@ -148,7 +310,9 @@ int ssb_score_grad_workspace_bytes(int B, int H, int W, size_t* bytes) {
         return SSB_EINVAL;
     }
     const size_t n = (size_t)H * W;
-    *bytes = 2 * (size_t)B * n * sizeof(double) + 3 * (size_t)B * kSgBlocks * sizeof(double);
+    const size_t nblk = (size_t)((W + SG_TX - 1) / SG_TX) * ((H + SG_TY - 1) / SG_TY);
+    *bytes = (2 * (size_t)B * n + (size_t)B * (kDotBlocks > 3 * kSgBlocks ? kDotBlocks : 3 * kSgBlocks) +
+              (size_t)B + 2 * (size_t)B * nblk + 2 * (size_t)B) * sizeof(double);
     return 0;
 }
 
@@ -181,6 +345,20 @@ int ssb_score_grad(int dtype, int B, int F, int C, int H, int W, const void* g_i
     }
     cudaStream_t s = (cudaStream_t)stream;
     const long long n = (long long)H * W;
+    if (bw.r <= SG_RMAX) {
+        if (sigma == 0.0) {
+            bw.r = 0;
+            bw.w[0] = 1.0;  // identity "blur": the tile pass only forms the sums
+        }
+        const double tot = (7.0 / 8.0) * budget * (double)n;
+        if (dtype == SSB_F64)
+            score_grad_fused<double>(B, F, C, H, W, (const double*)g_input, (const double*)grad_density,
+                                     (const double*)scores, tot, bw, (double*)g_scores, (char*)workspace, s);
+        else
+            score_grad_fused<float>(B, F, C, H, W, (const float*)g_input, (const float*)grad_density,
+                                    (const float*)scores, tot, bw, (float*)g_scores, (char*)workspace, s);
+        return cuda_check("ssb_score_grad");
+    }
     double* g0 = (double*)workspace;
     double* g1 = g0 + (size_t)B * n;
     double* pmax = g1 + (size_t)B * n;
