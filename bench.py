@@ -720,6 +720,29 @@ def next_rows(peak):
         "mpix_s": round(n / (ms_s * 1e-3) / 1e6, 1), "ms": round(ms_s, 4),
         "frac_of_hbm": round(56 * n / (ms_s * 1e-3) / 1e9 / peak, 4)}
     del sc, gi, gd
+    # tonemap + loss epilogue of one training step (8(f) row 4): tonemap of the
+    # frame, losses + gradients against a reference with a warped history,
+    # tonemap backward; algorithmic 12 (radiance) + 12 (ldr write) + 4 x 12
+    # (ldr, ref, ldr0_w, ref_w) + 4 (mask) + 4 (validity) + 2 x 12 (gradients)
+    # + 12 + 12 + 12 (tonemap backward: radiance, upstream, grad) = 152 B/px
+    rad = torch.rand((B, 3, H, W), device=dev, generator=gen) * 4
+    ref = torch.rand((B, 3, H, W), device=dev, generator=gen)
+    l0w = torch.rand((B, 3, H, W), device=dev, generator=gen)
+    rw = torch.rand((B, 3, H, W), device=dev, generator=gen)
+    val = (torch.rand((B, H, W), device=dev, generator=gen) > 0.1).float()
+    msk = torch.ones((B, H, W), device=dev)
+    tmo = (0.0, 1.0, 1.0, 0.5, 0.5)
+
+    def epilogue():
+        ldr = ops.tonemap(rad, tmo)
+        r = ops.losses(ldr, ref, l0w, rw, validity=val, mask=msk, want_maps=False, want_grads=True)
+        return ops.tonemap_backward(rad, tmo, r["g_ldr1"])
+    ms_e = _time_cuda(epilogue)
+    out["loss_epilogue"] = {
+        "workload": "8 x 1920x1080 fp32: tonemap, masked spatial + temporal losses with gradients, tonemap backward",
+        "mpix_s": round(n / (ms_e * 1e-3) / 1e6, 1), "ms": round(ms_e, 4),
+        "frac_of_hbm": round(152 * n / (ms_e * 1e-3) / 1e9 / peak, 4)}
+    del rad, ref, l0w, rw, val, msk
     torch.cuda.empty_cache()
     return out
 

@@ -229,6 +229,26 @@ int ssb_score_grad(int dtype, int B, int F, int C, int H, int W, const void* g_i
                    const void* grad_density, const void* scores, double budget, double sigma,
                    void* g_scores, void* workspace, ssb_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Tonemap + loss epilogue -- replaces tonemap.py
+ * `tonemap_array` (:87-88) / `tonemap_backward` (:95-118) and losses.py
+ * `spatial_loss` / `temporal_loss` / `combined_loss` (:58-91) with the loss
+ * gradients of optimize.py:219-231.  Images (B,3,H,W), maps (B,H,W); tmo =
+ * {exposure, contrast, saturation, toe, shoulder} (host doubles).
+ * ssb_losses: ldr0_w/ref_w (history) and validity/mask may be NULL; any
+ * output may be NULL; losses = B x {spatial, temporal, combined} (device
+ * doubles, needs the workspace).
+ * ---------------------------------------------------------------------- */
+int ssb_tonemap(int dtype, int B, int H, int W, const double* tmo, const void* radiance, void* ldr,
+                ssb_stream_t stream);
+int ssb_tonemap_backward(int dtype, int B, int H, int W, const double* tmo, const void* radiance,
+                         const void* upstream, void* grad, ssb_stream_t stream);
+int ssb_losses_workspace_bytes(int B, size_t* bytes);
+int ssb_losses(int dtype, int B, int H, int W, const void* ldr1, const void* ref, const void* ldr0_w,
+               const void* ref_w, const void* validity, const void* mask, void* sp_map, void* tm_map,
+               void* cb_map, double* losses, void* g_ldr1, void* g_ldr0_w, void* workspace,
+               ssb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,8 +1,8 @@
 """CPU oracle for the sparse-sampler hot path -- TEST INFRASTRUCTURE ONLY.
 
 This package is a numpy restatement of the reference algorithms
-(`/root/reference/pkg/src/sparse_sampler/{rng,density,estimators,pyramid,images}.py`,
-and the score-gradient lines of `optimize.py`)
+(`/root/reference/pkg/src/sparse_sampler/{rng,density,estimators,pyramid,images,tonemap,losses}.py`,
+and the score- and loss-gradient lines of `optimize.py`)
 generalised to any odd kernel size k and any level count L.  It exists to
 *check* the CUDA product path, never to stand in for it:
 
@@ -16,4 +16,4 @@ bit-for-bit in float64 (tests/test_oracle_golden.py, against fixtures generated
 by ``tests/golden/make_golden.py`` from the reference itself).
 """
 
-from . import rng, density, estimators, pyramid, scores, temporal  # noqa: F401
+from . import rng, density, estimators, pyramid, scores, temporal, tonemap  # noqa: F401

@@ -29,6 +29,7 @@ EXPORTS = (
     "ssb_allocate", "ssb_stochastic_core", "ssb_estimate", "ssb_place_fused",
     "ssb_warp", "ssb_warp_backward_workspace_bytes", "ssb_warp_backward",
     "ssb_score_grad_workspace_bytes", "ssb_score_grad",
+    "ssb_tonemap", "ssb_tonemap_backward", "ssb_losses_workspace_bytes", "ssb_losses",
 )
 
 vp = C.c_void_p
@@ -128,6 +129,10 @@ def load(build_if_missing: bool = False):
             "ssb_score_grad_workspace_bytes": (C.c_int, [C.c_int] * 3 + [P(C.c_size_t)]),
             "ssb_score_grad": (C.c_int, [C.c_int] * 6 + [vp, vp, vp, C.c_double, C.c_double,
                                                          vp, vp, vp]),
+            "ssb_tonemap": (C.c_int, [C.c_int] * 4 + [P(C.c_double)] + [vp] * 3),
+            "ssb_tonemap_backward": (C.c_int, [C.c_int] * 4 + [P(C.c_double)] + [vp] * 4),
+            "ssb_losses_workspace_bytes": (C.c_int, [C.c_int, P(C.c_size_t)]),
+            "ssb_losses": (C.c_int, [C.c_int] * 4 + [vp] * 14),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(lib, name)

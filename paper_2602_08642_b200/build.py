@@ -28,7 +28,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
 # per-file extra flags: placement decisions must round exactly like numpy
-EXTRA = {"place.cu": ["-fmad=false"], "temporal.cu": ["-fmad=false"], "scores.cu": ["-fmad=false"]}
+EXTRA = {"place.cu": ["-fmad=false"], "temporal.cu": ["-fmad=false"], "scores.cu": ["-fmad=false"], "tonemap.cu": ["-fmad=false"]}
 
 
 def nvcc() -> str:

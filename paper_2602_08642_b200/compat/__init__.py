@@ -6,7 +6,7 @@
     compat.uninstall()
 
 ``install()`` patches both the defining modules (sparse_sampler.pyramid,
-.density, .estimators, .rng, .images) and every module that bound the names at import
+.density, .estimators, .rng, .images, .tonemap, .losses) and every module that bound the names at import
 time (sparse_sampler.optimize, sparse_sampler.estimators, the package
 namespace), and makes the patched functions return the
 reference's own container classes.  Without the reference installed, the
@@ -19,7 +19,7 @@ import importlib
 import importlib.util
 import sys
 
-from . import _dev, _types, density, estimators, images, pyramid, rng  # noqa: F401
+from . import _dev, _types, density, estimators, images, losses, pyramid, rng, tonemap  # noqa: F401
 from ._dev import precision, set_precision  # noqa: F401
 
 # name -> compat module providing it, per reference module
@@ -31,9 +31,11 @@ PATCHES = {
                    "estimate_straight_through", "estimate_gumbel"],
     "rng": ["uniform_grid", "uniform_grid_batch", "pixel_uniform"],
     "images": ["warp_array", "warp_backward"],
+    "tonemap": ["tonemap_array", "tonemap_backward"],
+    "losses": ["spatial_loss", "temporal_loss"],
 }
 _COMPAT = {"pyramid": pyramid, "density": density, "estimators": estimators, "rng": rng,
-           "images": images}
+           "images": images, "tonemap": tonemap, "losses": losses}
 _saved: list = []
 _saved_types: dict | None = None
 

@@ -498,3 +498,93 @@ def score_grad(scores, g_input, grad_density, budget: float, sigma: float = 1.5)
                                  float(budget), float(sigma), _ptr(out), _ptr(ws),
                                  _stream(scores.device)), "ssb_score_grad")
     return out
+
+
+# ---------------------------------------------------------------------------
+# tonemap + loss epilogue
+
+
+def _tmo(tmo):
+    vals = [float(v) for v in tmo]
+    if len(vals) != 5:
+        raise ValueError("tmo must be (exposure, contrast, saturation, toe, shoulder)")
+    return (C.c_double * 5)(*vals)  # passed by reference (ctypes array -> double*)
+
+
+def tonemap(radiance, tmo):
+    """Filmic tonemap (ref `tonemap_array`, tonemap.py:87-88): radiance
+    (B, 3, H, W) -> LDR (B, 3, H, W); tmo = (exposure, contrast, saturation,
+    toe, shoulder)."""
+    lib = _lib.load()
+    _need(radiance, "radiance")
+    dt = _img_dtype(radiance, "radiance")
+    if radiance.dim() != 4 or radiance.shape[1] != 3:
+        raise ValueError("radiance must be (B, 3, H, W)")
+    B, _, H, W = radiance.shape
+    out = torch.empty_like(radiance)
+    with torch.cuda.device(radiance.device):
+        check(lib.ssb_tonemap(dt, B, H, W, _tmo(tmo), _ptr(radiance), _ptr(out), _stream(radiance.device)),
+              "ssb_tonemap")
+    return out
+
+
+def tonemap_backward(radiance, tmo, upstream):
+    """d(tonemap)/d(radiance) applied to `upstream` (ref `tonemap_backward`,
+    tonemap.py:95-118)."""
+    lib = _lib.load()
+    _need(radiance, "radiance")
+    dt = _img_dtype(radiance, "radiance")
+    _need(upstream, "upstream", radiance.device, radiance.dtype)
+    if radiance.dim() != 4 or radiance.shape[1] != 3 or upstream.shape != radiance.shape:
+        raise ValueError("radiance / upstream must be (B, 3, H, W)")
+    B, _, H, W = radiance.shape
+    g = torch.empty_like(radiance)
+    with torch.cuda.device(radiance.device):
+        check(lib.ssb_tonemap_backward(dt, B, H, W, _tmo(tmo), _ptr(radiance), _ptr(upstream), _ptr(g),
+                                       _stream(radiance.device)), "ssb_tonemap_backward")
+    return g
+
+
+def losses(ldr1, ref, ldr0_w=None, ref_w=None, validity=None, mask=None, want_maps=True,
+           want_grads=False):
+    """Masked spatial, temporal and max-combined losses (losses.py:58-91) and,
+    with want_grads, their gradients w.r.t. ldr1 and the warped history as
+    optimize.evaluate_step forms them (optimize.py:219-231).  Images
+    (B, 3, H, W); validity / mask (B, H, W).  Returns a dict with 'losses'
+    (B, 3) float64 = (spatial, temporal, combined), the maps, 'g_ldr1',
+    'g_ldr0_w'."""
+    lib = _lib.load()
+    _need(ldr1, "ldr1")
+    dt = _img_dtype(ldr1, "ldr1")
+    dev = ldr1.device
+    _need(ref, "ref", dev, ldr1.dtype)
+    if ldr1.dim() != 4 or ldr1.shape[1] != 3 or ref.shape != ldr1.shape:
+        raise ValueError("loss: image dimensions must match")
+    if (ldr0_w is None) != (ref_w is None):
+        raise ValueError("loss: the warped history needs both ldr0_w and ref_w")
+    B, _, H, W = ldr1.shape
+    for t, nm in ((ldr0_w, "ldr0_w"), (ref_w, "ref_w")):
+        if t is not None:
+            _need(t, nm, dev, ldr1.dtype)
+            if t.shape != ldr1.shape:
+                raise ValueError("temporal loss: image dimensions must match")
+    for t, nm in ((validity, "validity"), (mask, "mask")):
+        if t is not None:
+            _need(t, nm, dev, ldr1.dtype)
+            if tuple(t.shape) != (B, H, W):
+                raise ValueError(f"{nm} must be (B, H, W)")
+    if validity is not None and ldr0_w is None:
+        raise ValueError("validity needs the warped history")
+    maps = [torch.empty((B, H, W), dtype=ldr1.dtype, device=dev) for _ in range(3)] if want_maps else [None] * 3
+    vals = torch.empty((B, 3), dtype=torch.float64, device=dev)
+    g1 = torch.empty_like(ldr1) if want_grads else None
+    g0 = torch.empty_like(ldr1) if (want_grads and ldr0_w is not None) else None
+    wb = C.c_size_t()
+    check(lib.ssb_losses_workspace_bytes(B, C.byref(wb)), "ssb_losses_workspace_bytes")
+    ws = torch.empty(wb.value, dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        check(lib.ssb_losses(dt, B, H, W, _ptr(ldr1), _ptr(ref), _ptr(ldr0_w), _ptr(ref_w), _ptr(validity),
+                             _ptr(mask), _ptr(maps[0]), _ptr(maps[1]), _ptr(maps[2]), _ptr(vals), _ptr(g1),
+                             _ptr(g0), _ptr(ws), _stream(dev)), "ssb_losses")
+    return {"losses": vals, "spatial_map": maps[0], "temporal_map": maps[1], "combined_map": maps[2],
+            "g_ldr1": g1, "g_ldr0_w": g0}

@@ -7,7 +7,8 @@ Run in the build container (the reference is not present on the GPU box):
 
 Every array stored here is an output of the reference's own functions
 (`sparse_sampler.pyramid`, `.density`, `.rng`, `.estimators`, `.banks`,
-`.images`, and scipy's gaussian_filter exactly as optimize.py calls it) on
+`.images`, `.tonemap`, `.losses`, and scipy's gaussian_filter exactly as
+optimize.py calls it) on
 seeded inputs that are stored alongside.  The oracle is pinned against these
 files (tests/test_oracle_golden.py) and the GPU parity tests reuse them.
 Level counts other than the reference's default 5 are produced by setting
@@ -32,6 +33,8 @@ from sparse_sampler import density as D  # noqa: E402
 from sparse_sampler import estimators as E  # noqa: E402
 from sparse_sampler import rng as R  # noqa: E402
 from sparse_sampler import images as I  # noqa: E402
+from sparse_sampler import losses as LS  # noqa: E402
+from sparse_sampler import tonemap as TM  # noqa: E402
 from sparse_sampler.banks import SampleBank  # noqa: E402
 from scipy.ndimage import gaussian_filter  # noqa: E402  (the reference's own blur, optimize.py:20)
 
@@ -225,8 +228,45 @@ def scores(seed):
     return d
 
 
+def tonemap_losses(seed):
+    """tonemap.tonemap_array / tonemap_backward, losses.spatial_loss /
+    temporal_loss / combined_loss / make_mask("gradmag"), and the loss
+    gradients as optimize.evaluate_step forms them (optimize.py:219-231, inline
+    code there: restated here on the reference's own maps)."""
+    rng = np.random.default_rng(seed)
+    h, w = 13, 17
+    d = {}
+    tmos = [TM.TmoParams(), TM.sample_tmo(3), TM.sample_tmo(7)]
+    rad = rng.lognormal(-1.0, 2.0, (h, w, 3))
+    rad[0, :3] = [0.0, 1e-9, 5e-9]  # below the log floor (zero gradient)
+    rad[1, 0] = 1e-12
+    up = rng.normal(0.0, 1.0, (h, w, 3))
+    d["rad"], d["up"] = rad, up
+    for i, p in enumerate(tmos):
+        d[f"tmo{i}"] = np.array([p.exposure, p.contrast, p.saturation, p.toe, p.shoulder])
+        d[f"tm_ldr{i}"] = TM.tonemap_array(rad, p)
+        d[f"gtm{i}"] = TM.tonemap_backward(rad, p, up)
+    ldr1, ref, ldr0w, refw = (rng.uniform(0, 1, (h, w, 3)) for _ in range(4))
+    ldr1[2, 2] = ref[2, 2]  # a sign(0) pixel
+    validity = rng.choice([0.0, 0.5, 1.0], size=(h, w), p=[0.2, 0.1, 0.7])
+    mask = LS.make_mask("gradmag", ref)
+    d.update(ldr1=ldr1, ref=ref, ldr0w=ldr0w, refw=refw, validity=validity, mask=mask.weights)
+    sp_map, sp = LS.spatial_loss(ldr1, ref, mask)
+    tm_map, tm = LS.temporal_loss(ldr1, ldr0w, ref, refw, validity)
+    cb_map, cb = LS.combined_loss(sp_map, tm_map)
+    d.update(sp_map=sp_map, tm_map=tm_map, cb_map=cb_map, losses=np.array([sp, tm, cb]))
+    n_pix = cb_map.size
+    wins = (LS.TEMPORAL_WEIGHT * tm_map) > sp_map
+    g_sp = (~wins).astype(np.float64) / n_pix
+    g_tm = np.where(wins, LS.TEMPORAL_WEIGHT / n_pix, 0.0)
+    d["g_ldr1"] = (np.sign(ldr1 - ref) * (g_sp * mask.weights)[..., None] / 3.0
+                   + np.sign((ldr1 - ldr0w) - (ref - refw)) * g_tm[..., None] / 3.0)
+    d["g_ldr0w"] = -np.sign((ldr1 - ldr0w) - (ref - refw)) * g_tm[..., None] / 3.0
+    return d
+
+
 def main(which=None):
-    which = set(which or ["pyramid", "primitives", "placement", "temporal", "scores"])
+    which = set(which or ["pyramid", "primitives", "placement", "temporal", "scores", "tonemap"])
     n = 0
     if "pyramid" in which:
         for i, case in enumerate(PYRAMID_CASES):
@@ -234,7 +274,8 @@ def main(which=None):
             np.savez_compressed(os.path.join(HERE, f"{case[0]}.npz"), **d)
             n += 1
     for name, fn, seed in (("primitives", primitives, 77), ("placement", placement, 88),
-                           ("temporal", temporal, 99), ("scores", scores, 111)):
+                           ("temporal", temporal, 99), ("scores", scores, 111),
+                           ("tonemap", tonemap_losses, 123)):
         if name in which:
             np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **fn(seed))
             n += 1

@@ -38,6 +38,8 @@ def test_install_patches_definers_and_importers(ref_pkg):
         import sparse_sampler.images as I
         assert I.warp_array is compat.images.warp_array
         assert O.warp_array is compat.images.warp_array and O.warp_backward is compat.images.warp_backward
+        assert O.tonemap_array is compat.tonemap.tonemap_array and O.tonemap_backward is compat.tonemap.tonemap_backward
+        assert O.spatial_loss is compat.losses.spatial_loss and O.temporal_loss is compat.losses.temporal_loss
         # results are built from the reference's own classes while installed
         assert compat._types.TYPES["DensityMap"] is D.DensityMap
         assert compat.install()  # idempotent

@@ -362,3 +362,29 @@ def test_score_gradient_golden_through_compat(cp):
                                       list(d[f"{n}_gd"]), float(d[f"{n}_sigma"]))
         ref = d[f"{n}_gscores"]
         np.testing.assert_allclose(r, ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
+
+
+# ---------------------------------------------------------------- tonemap + losses
+# mirrors pkg/tests/test_tonemap.py / test_losses.py kinds of checks
+
+
+def test_tonemap_losses_through_compat(cp):
+    import types
+    d = load("tonemap")
+    t = d["tmo1"]
+    p = types.SimpleNamespace(exposure=t[0], contrast=t[1], saturation=t[2], toe=t[3], shoulder=t[4])
+    np.testing.assert_allclose(cp.tonemap.tonemap_array(d["rad"], p), d["tm_ldr1"], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(cp.tonemap.tonemap_backward(d["rad"], p, d["up"]), d["gtm1"], rtol=1e-12,
+                               atol=1e-13 * np.abs(d["gtm1"]).max())
+    mask = types.SimpleNamespace(weights=d["mask"])
+    sp_map, sp = cp.losses.spatial_loss(d["ldr1"], d["ref"], mask)
+    np.testing.assert_array_equal(sp_map, d["sp_map"])
+    assert abs(sp - d["losses"][0]) <= 1e-13 * abs(d["losses"][0])
+    tm_map, tm = cp.losses.temporal_loss(d["ldr1"], d["ldr0w"], d["ref"], d["refw"], d["validity"])
+    np.testing.assert_array_equal(tm_map, d["tm_map"])
+    assert abs(tm - d["losses"][1]) <= 1e-13 * abs(d["losses"][1])
+    g1, g0 = cp.losses.loss_gradients(d["ldr1"], d["ref"], d["ldr0w"], d["refw"], d["validity"], mask)
+    np.testing.assert_array_equal(g1, d["g_ldr1"])
+    np.testing.assert_array_equal(g0, d["g_ldr0w"])
+    with pytest.raises(ValueError):
+        cp.losses.spatial_loss(d["ldr1"], d["ref"][:-1], mask)

@@ -1,0 +1,85 @@
+"""GPU parity of the tonemap + loss epilogue through
+the C ABI: tonemap.py:87-118, losses.py:58-91 and the loss gradient of
+optimize.py:219-231, against the reference's golden outputs (float64) and the
+oracle (float32)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import tonemap as otm  # noqa: E402
+from tests._golden import load  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_08642_b200 import ops as _ops
+    return _ops
+
+
+def planar(a, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a).transpose(2, 0, 1))[None]).cuda().to(dtype)
+
+
+def hwc(t):
+    return t[0].permute(1, 2, 0).double().cpu().numpy()
+
+
+def test_tonemap_f64_vs_reference(ops):
+    d = load("tonemap")
+    for i in range(3):
+        t = tuple(d[f"tmo{i}"])
+        ldr = hwc(ops.tonemap(planar(d["rad"]), t))
+        np.testing.assert_allclose(ldr, d[f"tm_ldr{i}"], rtol=1e-13, atol=1e-15)
+        g = hwc(ops.tonemap_backward(planar(d["rad"]), t, planar(d["up"])))
+        ref = d[f"gtm{i}"]
+        np.testing.assert_allclose(g, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+        assert np.all(g[0, 0] == 0.0) and np.all(g[1, 0][ref[1, 0] == 0] == 0.0)  # below the log floor
+
+
+def test_losses_f64_vs_reference(ops):
+    d = load("tonemap")
+    cu = lambda a: torch.from_numpy(np.asarray(a)[None]).cuda()  # noqa: E731
+    r = ops.losses(planar(d["ldr1"]), planar(d["ref"]), planar(d["ldr0w"]), planar(d["refw"]),
+                   validity=cu(d["validity"]), mask=cu(d["mask"]), want_grads=True)
+    np.testing.assert_array_equal(r["spatial_map"][0].cpu().numpy(), d["sp_map"])
+    np.testing.assert_array_equal(r["temporal_map"][0].cpu().numpy(), d["tm_map"])
+    np.testing.assert_array_equal(r["combined_map"][0].cpu().numpy(), d["cb_map"])
+    np.testing.assert_allclose(r["losses"][0].cpu().numpy(), d["losses"], rtol=1e-13)
+    np.testing.assert_array_equal(hwc(r["g_ldr1"]), d["g_ldr1"])
+    np.testing.assert_array_equal(hwc(r["g_ldr0_w"]), d["g_ldr0w"])
+
+
+def test_tonemap_and_losses_f32_vs_oracle(ops):
+    rng = np.random.default_rng(4)
+    h, w = 135, 240
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    rad = f32(rng.lognormal(-1.0, 2.0, (h, w, 3)))
+    up = f32(rng.normal(size=(h, w, 3)))
+    t = (0.3, 1.1, 0.9, 0.4, 0.6)
+    ldr = hwc(ops.tonemap(planar(rad, torch.float32), t))
+    np.testing.assert_allclose(ldr, otm.tonemap(rad, t), rtol=1e-5, atol=1e-6)
+    g = hwc(ops.tonemap_backward(planar(rad, torch.float32), t, planar(up, torch.float32)))
+    gr = otm.tonemap_backward(rad, t, up)
+    np.testing.assert_allclose(g, gr, rtol=1e-4, atol=1e-5 * np.abs(gr).max())
+    a, b = f32(rng.uniform(0, 1, (h, w, 3))), f32(rng.uniform(0, 1, (h, w, 3)))
+    r = ops.losses(planar(a, torch.float32), planar(b, torch.float32), want_grads=True)
+    sp, _, _, vals = otm.losses(a, b)
+    np.testing.assert_allclose(r["spatial_map"][0].double().cpu().numpy(), sp, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(r["losses"][0, 0].item(), vals[0], rtol=1e-6)
+    g1, _ = otm.loss_grads(a, b)
+    np.testing.assert_allclose(hwc(r["g_ldr1"]), g1, rtol=1e-6, atol=1e-12)
+
+
+def test_losses_reject_bad_inputs(ops):
+    x = torch.zeros((1, 3, 8, 8), device="cuda", dtype=torch.float64)
+    with pytest.raises(ValueError):
+        ops.losses(x, torch.zeros((1, 3, 8, 9), device="cuda", dtype=torch.float64))
+    with pytest.raises(ValueError):
+        ops.losses(x, x, ldr0_w=x)
+    with pytest.raises(ValueError):
+        ops.tonemap(x, (0.0, 1.0, 1.0, 1.5, 0.5))  # toe outside (0, 1)

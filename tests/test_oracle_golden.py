@@ -162,3 +162,22 @@ def test_score_grad_bit_exact():
         r = osc.score_grad(d[f"{n}_scores"], float(d[f"{n}_budget"]), list(d[f"{n}_gin"]),
                            list(d[f"{n}_gd"]), float(d[f"{n}_sigma"]))
         np.testing.assert_array_equal(r, d[f"{n}_gscores"])
+
+
+def test_tonemap_and_losses_bit_exact():
+    """oracle/tonemap.py vs tonemap.py / losses.py and the loss gradient of
+    optimize.py:219-231 (8(f) row 4)."""
+    from oracle import tonemap as otm
+    d = load("tonemap")
+    for i in range(3):
+        t = tuple(d[f"tmo{i}"])
+        np.testing.assert_array_equal(otm.tonemap(d["rad"], t), d[f"tm_ldr{i}"])
+        np.testing.assert_array_equal(otm.tonemap_backward(d["rad"], t, d["up"]), d[f"gtm{i}"])
+    sp, tm, cb, vals = otm.losses(d["ldr1"], d["ref"], d["ldr0w"], d["refw"], d["validity"], d["mask"])
+    np.testing.assert_array_equal(sp, d["sp_map"])
+    np.testing.assert_array_equal(tm, d["tm_map"])
+    np.testing.assert_array_equal(cb, d["cb_map"])
+    np.testing.assert_array_equal(np.array(vals), d["losses"])
+    g1, g0 = otm.loss_grads(d["ldr1"], d["ref"], d["ldr0w"], d["refw"], d["validity"], d["mask"])
+    np.testing.assert_array_equal(g1, d["g_ldr1"])
+    np.testing.assert_array_equal(g0, d["g_ldr0w"])
