@@ -339,11 +339,26 @@ class BandRunner:
                                   self.demod, ksize=self.k)
 
 
+def chain_order():
+    """The library's level-0-last backward (float32, 3 channels, demodulated,
+    no history, L >= 2; csrc/pyr_chain.cuh) -- every bench workload uses it
+    unless SSB_NO_CHAIN / SSB_NO_TMA disable it."""
+    return os.environ.get("SSB_NO_CHAIN") != "1" and os.environ.get("SSB_NO_TMA") != "1"
+
+
 def launches_per_step(L, fwd_only=False):
-    # forward: (L-1) pooling + L level kernels; backward: L level kernels + final sweep
+    # forward: (L-1) pooling + L level kernels
     names = [f"pool{l}->{l + 1}" for l in range(L - 1)]
     names += [f"fwd_l{l}" for l in range(L - 1, -1, -1)]
-    if not fwd_only:
+    if fwd_only:
+        return names
+    if chain_order():
+        # backward, level 0 last: upsample-transpose pre-pass, levels 1..L-1,
+        # the level-1 pool chain (L >= 3), level 0 (final outputs)
+        names += ["bwd_up"] + [f"bwd_l{l}" for l in range(1, L)]
+        names += (["bwd_chain"] if L >= 3 else []) + ["bwd_l0"]
+    else:
+        # backward: L level kernels (fine -> coarse) + the coarse -> fine sweep
         names += [f"bwd_l{l}" for l in range(L)] + ["bwd_final"]
     return names
 

@@ -167,6 +167,11 @@ int make_plan(const ssb_pyr_desc* d, PyrPlan* p) {
         p->gl_off[l] = w;
         w += bytes;
     }
+    p->lse_off = 0;
+    if (p->esz == 4) {  // float32: level-0 log-sum-exp for the level-0-last backward
+        p->lse_off = t;
+        t += align256((size_t)p->B * p->H * p->W * sizeof(float));
+    }
     // kernels address channels of one frame with 32-bit offsets
     if ((unsigned long long)p->nlog[0] * (unsigned long long)p->H * (unsigned long long)p->W >=
         (1ull << 32)) {

@@ -42,9 +42,13 @@ struct TmaMaps {
     CUtensorMap up;   // upstream (level 0) or ghat^l, box (RX, S, 3)
     CUtensorMap out;  // forward output (level 0) or Lhat^l, box (RX, S, 3)
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
+    CUtensorMap t1;   // CH (level 0 last): T1 = level-1 input gradient incl. the pool chain, box (CB, CT, 3)
 };
 
-template <int K, typename TL, bool L0, bool UP, bool TIED>
+// CH: level 0 runs after the coarser levels (pyr_chain.cuh): no upsample
+// transpose (ghat^1 comes from k_up_transpose) and the flush adds the pool
+// chain T1(parent) / count, writing the final g_noisy / g_demod
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
 struct TmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
@@ -83,12 +87,16 @@ struct TmaShape {
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
     static constexpr int UPF = al32(3 * S * RX);       // floats per upstream / output block
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
+    static constexpr int CT = (S + 2 * R + 1) / 2 + 1;  // coarse rows of the flushed fine rows (bottom step: AW rows)
+    static constexpr int T1F = CH ? al32(3 * CT * CB) : 0;
+    static constexpr bool B3ON = UP && !CH;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
-    static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0);
+    static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
+                                        (CH ? 3 * CT * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + 1) * UPF + 2 * LHF +
-                                     3 * S * RX + S * RX + (UP ? CR * 3 * TXC : 0);
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + 1) * UPF + 2 * LHF + 2 * T1F +
+                                     3 * S * RX + S * RX + (B3ON ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
     static_assert(TXB * B2SPL <= 128 && 3 * TXC <= 128 && TXB % 4 == 0, "B2/B3 items exceed their warps");
@@ -159,10 +167,12 @@ __device__ __forceinline__ float rcp_fast(float x) {  // MUFU.RCP (x >= 1e-3 her
 }
 __device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0, 256;" ::: "memory"); }
 
-template <int K, typename TL, bool L0, bool UP, bool TIED>
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
 __global__ void __launch_bounds__(256, 2)
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH>;
+    constexpr bool B3ON = SH::B3ON;
+    constexpr int CT = SH::CT, T1F = SH::T1F;
     constexpr bool SEP = SH::SEP;
     constexpr int R = SH::R, NT = SH::NT, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
     constexpr int RA = SH::RA, RW = SH::RW, NQUAD = SH::NQUAD;
@@ -179,7 +189,8 @@ __global__ void __launch_bounds__(256, 2)
     float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]  (level 0: u * out after A)
     float* s_ob = s_up + NBU * UPF;                    // [3][S][RX]  forward output / Lhat^l
     float* s_lhc = s_ob + UPF;                         // [2][3][CROWS][CB]
-    float* s_g = s_lhc + 2 * SH::LHF;                  // [3][S][RX]  G = gout / sum
+    float* s_t1 = s_lhc + 2 * SH::LHF;                 // [2][3][CT][CB]   (CH)
+    float* s_g = s_t1 + 2 * T1F;                       // [3][S][RX]  G = gout / sum
     float* s_inn = s_g + 3 * PL;                       // [S][RX]     inner' = sum_c gin_c out_c / sum
     float* s_cac = s_inn + PL;                         // [CR][3][TXC] coarse ghat accumulators
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
@@ -226,6 +237,7 @@ __global__ void __launch_bounds__(256, 2)
         tma_load_4d(ring_block(s_up, j), &mp.up, xs0, qs, c0, b, bar);
         tma_load_4d(s_ob, &mp.out, xs0, qs, c0, b, bar);
         if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
+        if constexpr (CH) tma_load_4d(s_t1 + (j & 1) * T1F, &mp.t1, cxs, (qs - R) >> 1, c0, b, bar);
     };
 
     // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion);
@@ -267,7 +279,7 @@ __global__ void __launch_bounds__(256, 2)
     };
 
     // ---- prologue
-    if constexpr (UP)
+    if constexpr (B3ON)
         for (int i = tid; i < CR * 3 * TXC; i += 256) s_cac[i] = 0.f;
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
@@ -521,7 +533,7 @@ __global__ void __launch_bounds__(256, 2)
             // 2X-1 (tap j=1), 2X (j=0,1), 2X+1 (j=0; and j=1 at the last coarse
             // column, W even); coarse row (y+i)/2 per fine row y and tap row i,
             // clamped onto Hc-1 at the image bottom (fixed up below)
-            if constexpr (UP) {
+            if constexpr (B3ON) {
                 if (tid < 3 * TXC) {
                     const int c = tid / TXC, cxi = tid - c * TXC;
                     const int X = (x0 >> 1) + cxi;
@@ -690,7 +702,29 @@ __global__ void __launch_bounds__(256, 2)
                     const int P = qs - R + krow + r;
                     if (P < y0 || P >= y1 || P > H - 1) continue;
                     const unsigned off = (unsigned)P * (unsigned)W + (unsigned)gx2;
-                    if constexpr (L0) {
+                    if constexpr (L0 && CH) {
+                        // final outputs: the pool chain of the coarser levels,
+                        // T1(parent) / (children of the parent), joins the
+                        // level-0 input gradient; g_d masked by d > floor
+                        // (pyramid.py:415-421, 436-447)
+                        const float* xr = lin_row_step(qs, P, 0) + ri2;
+                        const float* dr = lin_row_step(qs, P, 1) + ri2;
+                        const float* uor = ring_row(s_up, P) + ri2;  // u * out
+                        const int Yp = P >> 1, Xp = gx2 >> 1;
+                        const bool hy = 2 * Yp + 1 < H, hx = 2 * Xp + 1 < W;
+                        const float rcnt = (hy && hx) ? 0.25f : ((hy || hx) ? 0.5f : 1.f);
+                        const float* t1 = s_t1 + (i & 1) * T1F + (Yp - ((qs - R) >> 1)) * CB + (Xp - cxs);
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            if (c >= nc) break;
+                            const unsigned o = c * hw32 + off;
+                            const float d = dr[c * PL];
+                            const float rd = rcp_fast(fmaxf(d, (float)kDemodFloor));
+                            const float v = fmaf(t1[c * CT * CB], rcnt, vout[r][c]);
+                            __stcs(glo + o, v * rd);
+                            if (gdo) __stcs(gdo + o, d > (float)kDemodFloor ? (uor[c * PL] - v * xr[c * PL]) * rd : 0.f);
+                        }
+                    } else if constexpr (L0) {
                         const float* xr = lin_row_step(qs, P, 0) + ri2;
                         const float* dr = lin_row_step(qs, P, 1) + ri2;
                         const float* uor = ring_row(s_up, P) + ri2;  // u * out
@@ -728,7 +762,7 @@ __global__ void __launch_bounds__(256, 2)
                     win[p][c] = p + S / 2 < NPW ? win[p + S / 2][c] : make_float2(0.f, 0.f);
         }
         cta_sync();  // end of step
-        if (UP && tid < 128) {
+        if (B3ON && tid < 128) {
             // coarse ghat rows finished by this step (all B3 items are in)
             const bool bottom = qs + S >= H;
             const int cend = bottom ? a.Hc : (qs + S) >> 1;

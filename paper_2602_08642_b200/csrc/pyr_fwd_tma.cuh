@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
         mbar_wait(&bars[0], i & 1);
         // softmax of this thread's own pixel, from smem into registers
         float e[NW];
+        float mk;
         {
             float z[NLOG];
 #pragma unroll
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
             float m = z[0];
 #pragma unroll
             for (int t = 1; t < NLOG; ++t) m = fmaxf(m, z[t]);
-            const float mk = m * kLog2e;
+            mk = m * kLog2e;
 #pragma unroll
             for (int t = 0; t < NT; ++t) e[t] = ex2_ftz(fmaf(z[t], kLog2e, -mk));
             if constexpr (UP) {
@@ -186,6 +187,9 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
 #pragma unroll
             for (int t = 0; t < NW; ++t) sum += e[t];
             const float inv = frcp(sum);
+            if constexpr (L0) {  // base-2 log-sum-exp for the backward's upsample-transpose pre-pass
+                if (a.lse) ((float*)a.lse)[(size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx] = mk + __log2f(sum);
+            }
             float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {

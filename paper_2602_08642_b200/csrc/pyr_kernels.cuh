@@ -16,6 +16,8 @@
 //    owned by exactly one thread per phase.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ssb {
@@ -34,6 +36,7 @@ struct FwdLevel {
     const void* lhat_c;  // coarse Lhat^{l+1}
     long long c_b, c_c;
     void* out;  // Lhat^l (l > 0) or out (l == 0); same strides as lin
+    void* lse;  // l == 0, float32: per-pixel base-2 log-sum-exp of the logits (B, H, W); may be null
 };
 
 struct BwdLevel {
@@ -57,6 +60,7 @@ struct BwdLevel {
     const void* lhat_c;
     long long c_b, c_c;
     void* ghat_c;  // coarse ghat^{l+1}
+    const void* t1;  // level 0 after the coarse levels (CH): T1 = level-1 input gradient incl. the pool chain
 };
 
 // Load one pixel's logits in weight order (denoise, 4 upsample -- the tied
@@ -156,11 +160,12 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
         }
     }
 
+    T mk = (T)0;
     if (valid) {
         T m = e[0];
 #pragma unroll
         for (int t = 1; t < NW; ++t) m = tmax(m, e[t]);
-        const T mk = prep_max(m);
+        mk = prep_max(m);
 #pragma unroll
         for (int t = 0; t < NW; ++t) {
             e[t] = softmax_exp(e[t], mk);
@@ -172,6 +177,10 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
 
     const T inv = frcp(sum);
     const long long off = (long long)y * W + x;
+    if constexpr (L0 && std::is_same<T, float>::value && !PREV) {
+        // w_t = 2^(z_t log2 e - lse2): the backward's upsample-transpose pre-pass
+        if (a.lse) ((float*)a.lse)[(long long)b * H * W + off] = mk + __log2f(sum);
+    }
     T* outp = (T*)a.out + b * a.in_b;
     const T* lhc = UP ? (const T*)a.lhat_c + b * a.c_b : nullptr;
     int cy0 = 0, cy1 = 0, cx0 = 0, cx1 = 0;

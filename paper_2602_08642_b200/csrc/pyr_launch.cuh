@@ -6,6 +6,7 @@
 #include <type_traits>
 
 #include "pyr_bwd_tma.cuh"
+#include "pyr_chain.cuh"
 #include "pyr_fwd_tma.cuh"
 #include "pyr_kernels.cuh"
 
@@ -24,6 +25,7 @@ struct PyrPlan {
     size_t pool_off[SSB_MAX_LEVELS], lhat_off[SSB_MAX_LEVELS], tape_bytes;
     // workspace: ghat^l and gL_l for l >= 1
     size_t ghat_off[SSB_MAX_LEVELS], gl_off[SSB_MAX_LEVELS], ws_bytes;
+    size_t lse_off;  // tape (float32 plans): level-0 base-2 log-sum-exp, B x H x W floats
 };
 
 int make_plan(const ssb_pyr_desc* d, PyrPlan* p);
@@ -98,19 +100,20 @@ inline int pick_segment(int strips, int H, int B) {
 // TMA-pipelined level backward (fp32 images, fp32/bf16 logits, no temporal
 // group, demodulated level 0); returns false if the tensors are not
 // TMA-addressable.
-template <int K, typename TL, bool L0, bool UP, bool TIED>
-bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
-    using SH = TmaShape<K, TL, L0, UP, TIED>;
+inline bool tma_disabled() {
+    const char* e = getenv("SSB_NO_TMA");
+    return e && e[0] == '1';
+}
+
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
+bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH>;
     // needs the forward output (level 0) / Lhat^l for the softmax-backward inner product
-    if ((L0 && !a0.demod) || !a0.outp) return false;
-    if (const char* e = getenv("SSB_NO_TMA")) {
-        if (e[0] == '1') return false;
-    }
+    if ((L0 && !a0.demod) || !a0.outp || tma_disabled()) return false;
     const long long plane = (long long)a0.H * a0.W;
     auto base = [&](const void* p, long long pl) {
         return p ? (const void*)((const float*)p - (long long)a0.c0 * pl) : nullptr;
     };
-    TmaMaps mp;
     const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     bool ok = make_tma_map_4d(&mp.lg, a0.logits, tma_dtype<TL>(), sizeof(TL), a0.W, a0.H, a0.nlog,
                               a0.batch, SH::RX, SH::S, SH::NLOG) &&
@@ -127,8 +130,18 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
     if (ok && UP)
         ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
-    if (!ok) return false;
-    auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED>;
+    if (ok && CH)
+        ok = a0.t1 && make_tma_map_4d(&mp.t1, base(a0.t1, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc, a0.Hc,
+                                      a0.ctot, a0.batch, SH::CB, SH::CT, 3);
+    return ok;
+}
+
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
+bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH>;
+    TmaMaps mp;
+    if (!prepare_bwd_tma<K, TL, L0, UP, TIED, CH>(a0, mp)) return false;
+    auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED, CH>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
@@ -218,6 +231,14 @@ void launch_pool(int B, int nc, int H, int W, const T* in, long long in_b, long 
     SSB_LAUNCH(s, k_pool2<T><<<grid, block, 0, s>>>(nc, H, W, in, in_b, in_c, dem, out, out_b, out_c));
 }
 
+// float32, 3 channels, no history, demodulated, >= 2 levels: the backward
+// runs level 0 last (pyr_chain.cuh) from the forward's log-sum-exp
+inline bool chain_path(const ssb_pyr_desc* d, const PyrPlan& p, const void* demod) {
+    if (p.esz != 4 || p.C != 3 || d->has_prev || !demod || p.L < 2 || tma_disabled()) return false;
+    const char* e = getenv("SSB_NO_CHAIN");
+    return !(e && e[0] == '1');
+}
+
 template <int K, typename TL, typename T>
 int run_forward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_fwd_io* io, void* tape,
                 cudaStream_t s) {
@@ -259,6 +280,7 @@ int run_forward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_fwd_io* i
                 a.demod = dem;
                 a.prev = io->prev ? (const T*)io->prev + coff0 : nullptr;
                 a.out = (T*)io->out + coff0;
+                a.lse = chain_path(d, p, io->demod) ? (void*)(tp + p.lse_off) : nullptr;
             } else {
                 a.lin = (const T*)(tp + p.pool_off[l]) + (long long)c0 * e_l;
                 a.out = (T*)(tp + p.lhat_off[l]) + (long long)c0 * e_l;
@@ -278,6 +300,111 @@ int run_forward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_fwd_io* i
     return cuda_check("ssb_pyr_forward");
 }
 
+// level-b backward descriptor (channel group 0, C = 3) shared by both orders
+template <typename T>
+BwdLevel bwd_level(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const char* tp,
+                   char* wp, int l, bool want, int accum) {
+    BwdLevel a{};
+    a.nc = p.C < kMaxCh ? p.C : kMaxCh;
+    a.H = p.hl[l];
+    a.W = p.wl[l];
+    a.c0 = 0;
+    a.ctot = p.C;
+    a.batch = p.B;
+    a.nlog = p.nlog[l];
+    const long long e_l = lvl_elems(p, l);
+    a.want_params = want ? 1 : 0;
+    a.accum = accum;
+    a.logits = io->logits[l];
+    a.lg_b = (long long)p.nlog[l] * e_l;
+    a.glogits = want ? io->g_logits[l] : nullptr;
+    a.in_b = (long long)p.C * e_l;
+    a.in_c = e_l;
+    if (l == 0) {
+        a.lin = io->noisy;
+        a.demod = io->demod;
+        a.gin = io->upstream;
+        a.outp = io->out;
+        a.gl_out = io->g_noisy;
+        a.gdc_out = io->g_demod;
+    } else {
+        a.lin = tp + p.pool_off[l];
+        a.outp = tp + p.lhat_off[l];
+        a.gin = wp + p.ghat_off[l];
+        a.gl_out = wp + p.gl_off[l];
+    }
+    if (l < p.L - 1) {
+        const long long e_c = lvl_elems(p, l + 1);
+        a.Hc = p.hl[l + 1];
+        a.Wc = p.wl[l + 1];
+        a.lhat_c = tp + p.lhat_off[l + 1];
+        a.ghat_c = wp + p.ghat_off[l + 1];
+        a.c_b = (long long)p.C * e_c;
+        a.c_c = e_c;
+    }
+    return a;
+}
+
+// backward with level 0 LAST (pyr_chain.cuh): ghat^1 from the up-transpose
+// pre-pass, levels 1..L-1, the level-1 pool chain, then level 0 writing the
+// final g_noisy / g_demod (no coarse->fine sweep kernel).  Returns 1 without
+// launching anything if level 0 is not TMA-addressable.
+template <int K, typename TL, bool TIED>
+int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
+                       void* ws, cudaStream_t s) {
+    const char* tp = (const char*)tape;
+    char* wp = (char*)ws;
+    const bool want = io->g_logits[0] != nullptr;
+    const int accum = io->accumulate_logits ? 1 : 0;
+    BwdLevel a0 = bwd_level<float>(d, p, io, tp, wp, 0, want, accum);
+    a0.t1 = wp + p.gl_off[1];
+    TmaMaps mp0;
+    if (!prepare_bwd_tma<K, TL, true, true, TIED, true>(a0, mp0)) return 1;
+    {
+        UpTransposeArgs u{};
+        u.H = p.H;
+        u.W = p.W;
+        u.Hc = p.hl[1];
+        u.Wc = p.wl[1];
+        u.nlog = p.nlog[0];
+        u.logits = io->logits[0];
+        u.lg_b = (long long)p.nlog[0] * lvl_elems(p, 0);
+        u.lse = (const float*)(tp + p.lse_off);
+        u.up = (const float*)io->upstream;
+        u.demod = (const float*)io->demod;
+        u.ghat = (float*)(wp + p.ghat_off[1]);
+        dim3 grid((u.Wc + UPT_X - 1) / UPT_X, (u.Hc + UPT_Y - 1) / UPT_Y, p.B);
+        SSB_LAUNCH(s, (k_up_transpose<K * K, TIED, TL><<<grid, dim3(UPT_X, UPT_Y), 0, s>>>(u)));
+    }
+    for (int l = 1; l < p.L; ++l) {
+        BwdLevel a = bwd_level<float>(d, p, io, tp, wp, l, want, accum);
+        dispatch_bwd<K, TL, float>(a, p.B, false, l < p.L - 1, TIED, false, s);
+    }
+    if (p.L >= 3) {
+        ChainArgs c{};
+        c.levels = p.L;
+        for (int l = 0; l < p.L; ++l) {
+            c.dims_h[l] = p.hl[l];
+            c.dims_w[l] = p.wl[l];
+            c.gl[l] = l >= 1 ? (float*)(wp + p.gl_off[l]) : nullptr;
+        }
+        dim3 grid((p.wl[1] + 127) / 128, (p.hl[1] + 7) / 8, p.B);
+        SSB_LAUNCH(s, k_pool_chain<<<grid, dim3(32, 8), 0, s>>>(c));
+    }
+    using SH = TmaShape<K, TL, true, true, TIED, true>;
+    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
+        attr_set = true;
+    }
+    const int strips = (a0.W + SH::TXB - 1) / SH::TXB;
+    a0.seg_h = pick_segment(strips, a0.H, a0.batch);
+    dim3 grid(strips, (a0.H + a0.seg_h - 1) / a0.seg_h, a0.batch);
+    SSB_LAUNCH(s, kern<<<grid, 256, SH::SMEM, s>>>(a0, mp0));
+    return cuda_check("ssb_pyr_backward");
+}
+
 template <int K, typename TL, typename T>
 int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io,
                  const void* tape, void* ws, cudaStream_t s) {
@@ -285,6 +412,13 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
     char* wp = (char*)ws;
     const bool tied = d->blend_mode == SSB_BLEND_TIED;
     const bool want = io->g_logits[0] != nullptr;
+    if constexpr (std::is_same<T, float>::value && !std::is_same<TL, double>::value) {
+        if (chain_path(d, p, io->demod) && io->out) {
+            const int rc = tied ? run_backward_chain<K, TL, true>(d, p, io, tape, ws, s)
+                                : run_backward_chain<K, TL, false>(d, p, io, tape, ws, s);
+            if (rc != 1) return rc;  // 1: not TMA-addressable, take the general order below
+        }
+    }
     for (int c0 = 0; c0 < p.C; c0 += kMaxCh) {
         const int nc = p.C - c0 < kMaxCh ? p.C - c0 : kMaxCh;
         const long long coff0 = (long long)c0 * p.H * p.W;

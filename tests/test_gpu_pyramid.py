@@ -346,3 +346,36 @@ def test_tma_and_generic_paths_agree(ops, monkeypatch):
     for a_, b_ in [(g1.input, g2.input), (g1.demod, g2.demod)] + list(zip(g1.logits, g2.logits)):
         scale = b_.abs().max().item()
         assert (a_ - b_).abs().max().item() <= 2e-5 * scale
+
+
+@pytest.mark.parametrize("H,W,L,k,ldt", [(67, 132, 3, 5, "f32"), (66, 136, 2, 5, "f32"), (45, 96, 4, 7, "bf16"),
+                                         (33, 64, 5, 3, "f32")])
+def test_level0_last_order_matches_general_order(H, W, L, k, ldt, monkeypatch):
+    """The level-0-last backward (up-transpose pre-pass, pool chain, level 0
+    writing final outputs; csrc/pyr_chain.cuh) against the general order
+    (fine -> coarse + the coarse -> fine sweep kernel) on the same inputs."""
+    from paper_2602_08642_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(H * W + L)
+    dev = torch.device("cuda")
+    noisy = torch.rand((2, 3, H, W), device=dev, generator=g) * 2
+    demod = torch.rand((2, 3, H, W), device=dev, generator=g) * 0.99 + 0.0005
+    shapes = ops.level_shapes(H, W, L)
+    logits = [torch.randn((2, ops.logit_channels(l, L, k), h, w), device=dev, generator=g)
+              for l, (h, w) in enumerate(shapes)]
+    if ldt == "bf16":
+        logits = [z.to(torch.bfloat16) for z in logits]
+    up = torch.randn((2, 3, H, W), device=dev, generator=g)
+    res = {}
+    for mode in ("chain", "general"):
+        if mode == "general":
+            monkeypatch.setenv("SSB_NO_CHAIN", "1")
+        out, tape = ops.pyramid_forward(noisy, logits, demod, ksize=k)
+        gr = ops.pyramid_backward(tape, up)
+        res[mode] = (out, gr)
+        monkeypatch.delenv("SSB_NO_CHAIN", raising=False)
+    (o1, g1), (o2, g2) = res["chain"], res["general"]
+    assert torch.equal(o1, o2)
+    for a, b in [(g1.input, g2.input), (g1.demod, g2.demod)] + list(zip(g1.logits, g2.logits)):
+        a, b = a.double(), b.double()
+        tol = 2e-2 if ldt == "bf16" else 1e-5
+        assert torch.allclose(a, b, rtol=tol, atol=tol * b.abs().max().item()), (a - b).abs().max().item()
