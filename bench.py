@@ -682,7 +682,74 @@ def also_measurements():
                   "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
     del noisy, demod, logits, up, r
     torch.cuda.empty_cache()
+    out.update(small_configs(peak))
     out.update(next_rows(peak))
+    return out
+
+
+def small_configs(peak):
+    """The remaining BASELINE configs: c2 (64 x 256^2, L4 k5 fp32 fwd+bwd) as
+    throughput; c1 (one 1080p frame: fused placement + demod + L3 k5 forward)
+    and c0 (one 256^2 frame, the same pipeline; L2-resident) as per-frame
+    latency of a CUDA-graph replay of the whole inference path."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2602_08642_b200 import ops
+    out = {}
+    frames, H, W, L, k, ldt, desc = WORKLOADS["c2"]
+    noisy, demod, logits, up = synthetic_inputs(frames, H, W, L, k, ldt, torch.device("cuda"), seed=97)
+    r = Runner(noisy, demod, logits, up, k)
+    ms, kern, _ = time_device(r, 20, 3, L, None, 1)
+    fwd_b, bwd_b, dom_b = algorithmic_bytes(H, W, L, k, 4, 4)
+    out["c2"] = {"workload": desc, "mpix_s": round(frames * H * W / (ms * 1e-3) / 1e6, 1),
+                 "ms_per_step": round(ms, 4),
+                 "step_frac_of_hbm": round(frames * (fwd_b + bwd_b) / (ms * 1e-3) / 1e9 / peak, 4),
+                 "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
+    del noisy, demod, logits, up, r
+    for name, H, W in (("c1", 1080, 1920), ("c0", 256, 256)):
+        L, k = 3, 5
+        dev = torch.device("cuda")
+        g = torch.Generator(device=dev).manual_seed(7)
+        z = torch.randn(1, 1, H, W, generator=g, device=dev)
+        ker = torch.exp(-torch.arange(-24, 25, device=dev, dtype=torch.float32) ** 2 / 128.0)
+        ker = ker / ker.sum()
+        z = F.conv2d(F.pad(z, (24, 24, 0, 0), mode="circular"), ker.view(1, 1, 1, -1))
+        z = F.conv2d(F.pad(z, (0, 0, 24, 24), mode="circular"), ker.view(1, 1, -1, 1))
+        scores = torch.log(F.softplus((z - z.mean()) / z.std()))[0].contiguous()
+        bank = torch.exp(-1.0 + 1.5 * torch.randn(1, 2, 3, H, W, generator=g, device=dev))
+        bank = torch.where(torch.rand(1, 2, 1, H, W, generator=g, device=dev) < 0.01, bank * 100, bank).contiguous()
+        demod = torch.rand(1, 3, H, W, generator=g, device=dev) * 0.95 + 0.05
+        logits = [torch.randn(1, logit_channels(l, L, k), h, w, generator=g, device=dev)
+                  for l, (h, w) in enumerate(level_shapes(H, W, L))]
+        noisy = torch.empty(1, 3, H, W, device=dev)
+        wsb = C.c_size_t()
+        ops._lib.load().ssb_density_workspace_bytes(1, H, W, C.byref(wsb))
+        ws = torch.empty(wsb.value, dtype=torch.uint8, device=dev)
+        outb = torch.empty_like(noisy)
+
+        def infer():
+            ops.place_fused(scores, bank, 0.25, seed=3, noisy=noisy, workspace=ws)
+            ops.pyramid_forward(noisy, logits, demod, ksize=k, out=outb)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                infer()
+        torch.cuda.current_stream().wait_stream(s)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            infer()
+        reps = 200
+        ms = _time_cuda(graph.replay, steps=reps, warmup=10)
+        fwd_b, _, _ = algorithmic_bytes(H, W, L, k, 4, 4)
+        out[name] = {"workload": f"{name}: one {W}x{H} frame, fused placement (0.25 spp) + demod + "
+                                 f"3-level 5x5 forward, fp32, CUDA-graph replay",
+                     "us_per_frame": round(ms * 1e3, 2),
+                     "mpix_s": round(H * W / (ms * 1e-3) / 1e6, 1),
+                     "fwd_frac_of_hbm": round((fwd_b + 19 * H * W) / (ms * 1e-3) / 1e9 / peak, 4)}
+        del graph, scores, bank, demod, logits, noisy, outb
+    torch.cuda.empty_cache()
     return out
 
 
