@@ -550,7 +550,7 @@ def gpu_arm(args, rank, world, local_rank, dist):
                    "logit_dtype": ldt, "parallelism": f"frame-sharded x{world}, no collective",
                    "l2": "working set >> 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "bwd_l0 (level-0 backward: softmax recompute, "
-                     "logit grads, gather-transpose, upsample-transpose)" if not fwd_only else
+                     "logit grads, gather-transpose, final g_noisy/g_demod)" if not fwd_only else
                      "fwd_l0 (level-0 forward: softmax, k x k gather, upsample, remod)",
                      "achieved": round(dom_gbs, 1) if dom_gbs else None, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s",
