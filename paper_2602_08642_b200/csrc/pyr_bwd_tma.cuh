@@ -90,12 +90,18 @@ struct TmaShape {
     static constexpr int CT = (S + 2 * R + 1) / 2 + 1;  // coarse rows of the flushed fine rows (bottom step: AW rows)
     static constexpr int T1F = CH ? al32(3 * CT * CB) : 0;
     static constexpr bool B3ON = UP && !CH;
+    // EARLY: the next step's TMA is issued at the top of the step (right after
+    // the previous step's end barrier) instead of after phase A -- every
+    // buffer it overwrites belongs to step i-1; needs a second output block,
+    // and for fp32 logits only (bf16 would need a second staging box)
+    static constexpr bool EARLY = !SEP;
+    static constexpr int NOB = EARLY ? 2 : 1;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
     static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
                                         (CH ? 3 * CT * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + 1) * UPF + 2 * LHF + 2 * T1F +
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + 2 * LHF + 2 * T1F +
                                      3 * S * RX + S * RX + (B3ON ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
@@ -187,8 +193,8 @@ __global__ void __launch_bounds__(256, 2)
     float* s_lg = reinterpret_cast<float*>(smem_tma);  // [2][NLOG][S][RX] | [NLOG][S][RX] + staging
     float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RX]
     float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]  (level 0: u * out after A)
-    float* s_ob = s_up + NBU * UPF;                    // [3][S][RX]  forward output / Lhat^l
-    float* s_lhc = s_ob + UPF;                         // [2][3][CROWS][CB]
+    float* s_ob = s_up + NBU * UPF;                    // [NOB][3][S][RX]  forward output / Lhat^l
+    float* s_lhc = s_ob + SH::NOB * UPF;               // [2][3][CROWS][CB]
     float* s_t1 = s_lhc + 2 * SH::LHF;                 // [2][3][CT][CB]   (CH)
     float* s_g = s_t1 + 2 * T1F;                       // [3][S][RX]  G = gout / sum
     float* s_inn = s_g + 3 * PL;                       // [S][RX]     inner' = sum_c gin_c out_c / sum
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(256, 2)
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
         tma_load_4d(ring_block(s_up, j), &mp.up, xs0, qs, c0, b, bar);
-        tma_load_4d(s_ob, &mp.out, xs0, qs, c0, b, bar);
+        tma_load_4d(s_ob + (SH::EARLY ? (j & 1) * UPF : 0), &mp.out, xs0, qs, c0, b, bar);
         if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
         if constexpr (CH) tma_load_4d(s_t1 + (j & 1) * T1F, &mp.t1, cxs, (qs - R) >> 1, c0, b, bar);
     };
@@ -310,6 +316,14 @@ __global__ void __launch_bounds__(256, 2)
     // (every thread; ends with the CTA barrier, the next prefetch and the
     // clamp patch of the image rows that arrived with this step)
     auto phase_a = [&](int i, int qs, float* lgb, const TL* lgs) {
+        if constexpr (SH::EARLY) {
+            // every thread passed step i-1's end barrier: the buffers of step
+            // i+1 (those of step i-1) are free -- prefetch a full step ahead
+            if (tid == 0 && i + 1 < nsteps) {
+                fence_proxy_async();
+                issue_step(i + 1);
+            }
+        }
         mbar_wait(&bars[i & 1], (i >> 1) & 1);
         if (act_a) {
             float e[NLOG];
@@ -338,7 +352,7 @@ __global__ void __launch_bounds__(256, 2)
             const float inv = rcp_fast(sum);
             convert_block(i, s_a, ri_a);  // (block i = slot sl_i)
             float* ub = ring_block(s_up, i) + s_a * RX + ri_a;
-            const float* ob = s_ob + s_a * RX + ri_a;
+            const float* ob = s_ob + (SH::EARLY ? (i & 1) * UPF : 0) + s_a * RX + ri_a;
             float dq[3] = {1.f, 1.f, 1.f};
             if constexpr (L0) {
                 const float* dr = lin_row_step(qs, qs + s_a, 1) + ri_a;
@@ -356,11 +370,13 @@ __global__ void __launch_bounds__(256, 2)
             s_inn[s_a * RX + ri_a] = inner * inv;
         }
         cta_sync();
-        // every thread has finished the previous step and this step's phase A:
-        // the buffers of step i+1 are free
-        if (tid == 0 && i + 1 < nsteps) {
-            fence_proxy_async();
-            issue_step(i + 1);
+        if constexpr (!SH::EARLY) {
+            // every thread has finished the previous step and this step's phase A:
+            // the buffers of step i+1 are free
+            if (tid == 0 && i + 1 < nsteps) {
+                fence_proxy_async();
+                issue_step(i + 1);
+            }
         }
         if (col_border || qs + R + S > H) patch_rows(qs + R, qs + R + S);
     };
