@@ -65,7 +65,7 @@ struct TmaShape {
     static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
     // upstream ring (level 0: the flush needs u * out, R rows behind); other
     // levels and the forward output / Lhat^l: one block (read in phase A only)
-    static constexpr int NBU = L0 ? (R + S - 1) / S + 2 : 1;
+    static constexpr int NBU = L0 ? (R + S - 1) / S + 2 : (LGE == 4 ? 2 : 1);  // (2: early issue, below)
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
     // B1: S * NQUAD pixel quads on warps 0-3; tap rows split in B1SPL warp-uniform parts
     static constexpr int NB1 = S * NQUAD;
