@@ -65,7 +65,7 @@ struct TmaShape {
     static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
     // upstream ring (level 0: the flush needs u * out, R rows behind); other
     // levels and the forward output / Lhat^l: one block (read in phase A only)
-    static constexpr int NBU = L0 ? (R + S - 1) / S + 2 : (LGE == 4 ? 2 : 1);  // (2: early issue, below)
+    static constexpr int NBU0 = L0 ? (R + S - 1) / S + 2 : 2;  // gradient-input ring (2 at l >= 1 with early issue)
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
     // B1: S * NQUAD pixel quads on warps 0-3; tap rows split in B1SPL warp-uniform parts
     static constexpr int NB1 = S * NQUAD;
@@ -75,14 +75,20 @@ struct TmaShape {
     // B2: TXB columns x B2SPL tap-column groups on warps 4-7 (adjacent lanes)
     static constexpr int B2SPL = TXB * 4 <= 128 ? 4 : (TXB * 2 <= 128 ? 2 : 1);
     static constexpr int AW = S + 2 * R, NPW = (AW + 1) / 2;  // output-row window (float2 pairs)
-    static constexpr int CR = 4, CB = 36, CROWS = S / 2 + 1;  // coarse box: aligned start, TXC + 1 + 2 cols
+    // coarse box: 16-B aligned start (x0/2 rounded down to 4), TXC + 1 + 3 cols
+    static constexpr int CR = 4, CB = ((TXB / 2 + 4 + 3) / 4) * 4, CROWS = S / 2 + 1;
     // every TMA destination starts 128-B aligned (sizes rounded up to 32 floats)
     static constexpr int al32(int n) { return (n + 31) & ~31; }
-    static constexpr int LGF = al32(NLOG * S * RX);    // floats per exponentials buffer
+    // exponentials: fp32 logits = in place in the staging box (pitch RX);
+    // bf16 = a separate fp32 buffer with a tighter pitch RXE over the columns
+    // phase A fills, shifted by ESH (keeps 16-B alignment of pixel quads)
+    static constexpr int ESH = SEP ? RA - 4 : 0;
+    static constexpr int RXE = SEP ? ((TXB + R + 4 + 3) / 4) * 4 : RX;
+    static constexpr int EPL = S * RXE;                // floats per exponential plane
+    static constexpr int LGF = al32(NLOG * EPL);       // floats per exponentials buffer
     // logits staging (storage type): fp32 = the two exponential buffers
-    // themselves (in place); bf16 = one staging box + one fp32 buffer
-    static constexpr int LGS = SEP ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
-    static constexpr int LGBUF = SEP ? LGF + LGS : 2 * LGF;
+    // themselves (in place); bf16 = staging box(es) + one fp32 buffer
+    static constexpr int LGS1 = SEP ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
     static constexpr int DEMOFF = al32(3 * S * RX);    // demod plane offset inside a ring block
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
     static constexpr int UPF = al32(3 * S * RX);       // floats per upstream / output block
@@ -94,13 +100,20 @@ struct TmaShape {
     // the previous step's end barrier) instead of after phase A -- every
     // buffer it overwrites belongs to step i-1; needs a second output block,
     // and for fp32 logits only (bf16 would need a second staging box)
+    static constexpr size_t FL_BASE = (size_t)NBL * BLKF + 2 * LHF + 2 * T1F + 3 * S * RX + S * RX +
+                                      (B3ON ? CR * 3 * TXC : 0);
+    // (bf16: measured no gain at k = 7 with the second staging box -- kept off)
+    static constexpr bool EARLY_FITS = ((size_t)LGF + 2 * LGS1 + FL_BASE + (NBU0 + 2) * UPF) * 4 + 64 <= 113 * 1024;
     static constexpr bool EARLY = !SEP;
     static constexpr int NOB = EARLY ? 2 : 1;
+    static constexpr int LGS = EARLY ? 2 * LGS1 : LGS1;  // staging floats (both boxes)
+    static constexpr int LGBUF = SEP ? LGF + LGS : 2 * LGF;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
     static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
                                         (CH ? 3 * CT * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
+    static constexpr int NBU = L0 ? NBU0 : (EARLY ? 2 : 1);
     static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + 2 * LHF + 2 * T1F +
                                      3 * S * RX + S * RX + (B3ON ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
@@ -185,6 +198,7 @@ __global__ void __launch_bounds__(256, 2)
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
     constexpr int NI = SH::NI, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
     constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF;
+    constexpr int EPL = SH::EPL, RXE = SH::RXE, ESH = SH::ESH, LGS1 = SH::LGS1;
     constexpr int B1SPL = SH::B1SPL, B2SPL = SH::B2SPL, AW = SH::AW, NPW = SH::NPW;
     constexpr int PL = S * RX;  // floats per image plane in a block
     constexpr int RUP = (R + 1) & ~1;
@@ -237,7 +251,8 @@ __global__ void __launch_bounds__(256, 2)
         uint64_t* bar = &bars[j & 1];
         const int qs = qstart + j * S;
         mbar_expect_tx(bar, SH::TX_STEP);
-        tma_load_4d(SEP ? s_lg + LGF : s_lg + (j & 1) * LGF, &mp.lg, xs0, qs, 0, b, bar);
+        tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? (j & 1) * LGS1 : 0) : s_lg + (j & 1) * LGF, &mp.lg, xs0, qs,
+                    0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
         tma_load_4d(ring_block(s_up, j), &mp.up, xs0, qs, c0, b, bar);
@@ -348,7 +363,7 @@ __global__ void __launch_bounds__(256, 2)
                 sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];
             }
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) lgb[t * PL + s_a * RX + ri_a] = e[t];
+            for (int t = 0; t < NLOG; ++t) lgb[t * EPL + s_a * RXE + ri_a - ESH] = e[t];
             const float inv = rcp_fast(sum);
             convert_block(i, s_a, ri_a);  // (block i = slot sl_i)
             float* ub = ring_block(s_up, i) + s_a * RX + ri_a;
@@ -415,7 +430,8 @@ __global__ void __launch_bounds__(256, 2)
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = qstart + i * S;
         float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
-        phase_a(i, qs, lgb, reinterpret_cast<const TL*>(SEP ? s_lg + LGF : lgb));
+        phase_a(i, qs, lgb,
+                reinterpret_cast<const TL*>(SEP ? s_lg + LGF + (SH::EARLY ? (i & 1) * LGS1 : 0) : lgb));
         if (tid < 128) {
             // -------------------------------------------- B1: logit gradients
             const int qy = qs + s, gx = x0 + xi;
@@ -433,7 +449,7 @@ __global__ void __launch_bounds__(256, 2)
                 }
                 const float4 inn4 = *reinterpret_cast<const float4*>(s_inn + s * RX + ri);
                 const float inn[4] = {inn4.x, inn4.y, inn4.z, inn4.w};
-                const float* ep = lgb + s * RX + ri;
+                const float* ep = lgb + s * RXE + ri - ESH;
                 auto body = [&](auto acc_t) {
                     constexpr bool ACC = decltype(acc_t)::value;
                     constexpr int OFF = 4 - R;  // window value m = x(ri - 4 + m); pixel p, tap d -> m = p + d + OFF
@@ -476,7 +492,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
                         for (int d = 0; d < K; ++d) {
                             const int t = (dy + R) * K + d;
-                            const float4 e4 = *reinterpret_cast<const float4*>(ep + t * PL);
+                            const float4 e4 = *reinterpret_cast<const float4*>(ep + t * EPL);
                             st_gz4<ACC>(gp, e4.x * gw[0][d], e4.y * gw[1][d], e4.z * gw[2][d], e4.w * gw[3][d]);
                             gp += hw32;
                         }
@@ -524,7 +540,7 @@ __global__ void __launch_bounds__(256, 2)
                                     for (int jj = 0; jj < 2; ++jj) gu[p][2 * ii + jj] = dotc[p][(p + jj) >> 1];
                             }
                             if constexpr (TIED) {
-                                const float4 e4 = *reinterpret_cast<const float4*>(ep + NT * PL);
+                                const float4 e4 = *reinterpret_cast<const float4*>(ep + NT * EPL);
                                 float z[4];
 #pragma unroll
                                 for (int p = 0; p < 4; ++p) z[p] = (gu[p][0] + gu[p][1]) + (gu[p][2] + gu[p][3]);
@@ -532,7 +548,7 @@ __global__ void __launch_bounds__(256, 2)
                             } else {
 #pragma unroll
                                 for (int t4 = 0; t4 < 4; ++t4) {
-                                    const float4 e4 = *reinterpret_cast<const float4*>(ep + (NT + t4) * PL);
+                                    const float4 e4 = *reinterpret_cast<const float4*>(ep + (NT + t4) * EPL);
                                     st_gz4<ACC>(gp, e4.x * gu[0][t4], e4.y * gu[1][t4], e4.z * gu[2][t4], e4.w * gu[3][t4]);
                                     gp += hw32;
                                 }
@@ -566,8 +582,8 @@ __global__ void __launch_bounds__(256, 2)
                             const float gm = gr[-1], g0 = gr[0], gq = gr[1];
 #pragma unroll
                             for (int ii = 0; ii < 2; ++ii) {
-                                const float* w0 = lgb + (TIED ? NT : NT + 2 * ii) * PL + ss * RX + rj;
-                                const float* w1 = lgb + (TIED ? NT : NT + 2 * ii + 1) * PL + ss * RX + rj;
+                                const float* w0 = lgb + (TIED ? NT : NT + 2 * ii) * EPL + ss * RXE + rj - ESH;
+                                const float* w1 = lgb + (TIED ? NT : NT + 2 * ii + 1) * EPL + ss * RXE + rj - ESH;
                                 const float am = w1[-1], a0 = w0[0] + w1[0];
                                 const float aq = lastX ? w0[1] + w1[1] : w0[1];
                                 const int yl = (ss + ii) >> 1;  // compile-time after unrolling
@@ -600,7 +616,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) g[c] = s_g[c * PL + ss * RX + rj];
 #pragma unroll
-                    for (int d = 0; d < K; ++d) w[d] = lgb[(d * K + dx + R) * PL + ss * RX + rj];
+                    for (int d = 0; d < K; ++d) w[d] = lgb[(d * K + dx + R) * EPL + ss * RXE + rj - ESH];
 #pragma unroll
                     for (int d = 0; d < K; ++d) {
                         const int k = ss + d;
