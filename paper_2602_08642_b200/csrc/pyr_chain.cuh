@@ -128,42 +128,63 @@ struct ChainArgs {
 // T1(P) = gL1(P) + sum over ancestors A at level l >= 2 of gL_l(A) / (children
 // counts along the chain) -- the coarse part of sweep 2 at level 1
 static __global__ void k_pool_chain(const ChainArgs a) {
-    // four level-1 pixels per thread along x (independent loads in flight)
+    // four level-1 pixels per thread along x: one float4 of gL1 per channel,
+    // the coarser ancestors of the quad loaded once (their per-pixel children
+    // counts differ only at the image edge)
     const int x4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int b = blockIdx.z;
-    if (x4 >= a.dims_w[1] || y >= a.dims_h[1]) return;
+    const int W1 = a.dims_w[1], H1 = a.dims_h[1];
+    if (x4 >= W1 || y >= H1) return;
     const int top = a.levels - 1;
-    const size_t hw1 = (size_t)a.dims_h[1] * a.dims_w[1];
+    const size_t hw1 = (size_t)H1 * W1;
+    const bool vec = (W1 & 3) == 0;  // whole quad inside the row, 16-B aligned
+    float pb[4][3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int x = x4 + k;
-        if (x >= a.dims_w[1]) break;
-        float pb[3] = {0.f, 0.f, 0.f};
-        if (top >= 2) {
-            // ancestor of level-1 pixel (y, x) at level l: (y >> (l - 1), x >> (l - 1))
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pb[k][c] = 0.f;
+    if (top >= 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x = min(x4 + k, W1 - 1);
             const size_t hwt = (size_t)a.dims_h[top] * a.dims_w[top];
             const size_t ot = (size_t)(y >> (top - 1)) * a.dims_w[top] + (x >> (top - 1));
 #pragma unroll
-            for (int c = 0; c < 3; ++c) pb[c] = a.gl[top][((size_t)b * 3 + c) * hwt + ot];
-            for (int l = top - 1; l >= 1; --l) {
+            for (int c = 0; c < 3; ++c) pb[k][c] = __ldg(&a.gl[top][((size_t)b * 3 + c) * hwt + ot]);
+        }
+        for (int l = top - 1; l >= 1; --l) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int x = min(x4 + k, W1 - 1);
                 const int Yp = y >> l, Xp = x >> l;  // the level-(l+1) ancestor, its children at level l
                 const bool hy = 2 * Yp + 1 < a.dims_h[l], hx = 2 * Xp + 1 < a.dims_w[l];
                 const float rcnt = (hy && hx) ? 0.25f : ((hy || hx) ? 0.5f : 1.f);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) pb[c] *= rcnt;
-                if (l == 1) break;
+                for (int c = 0; c < 3; ++c) pb[k][c] *= rcnt;
+                if (l == 1) continue;
                 const size_t hwl = (size_t)a.dims_h[l] * a.dims_w[l];
                 const size_t ol = (size_t)(y >> (l - 1)) * a.dims_w[l] + (x >> (l - 1));
 #pragma unroll
-                for (int c = 0; c < 3; ++c) pb[c] += a.gl[l][((size_t)b * 3 + c) * hwl + ol];
+                for (int c = 0; c < 3; ++c) pb[k][c] += __ldg(&a.gl[l][((size_t)b * 3 + c) * hwl + ol]);
             }
         }
-        const size_t o1 = (size_t)y * a.dims_w[1] + x;
+    }
+    const size_t o1 = (size_t)y * W1 + x4;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            float* p = &a.gl[1][((size_t)b * 3 + c) * hw1 + o1];
-            *p = *p + pb[c];
+    for (int c = 0; c < 3; ++c) {
+        float* p = &a.gl[1][((size_t)b * 3 + c) * hw1 + o1];
+        if (vec) {
+            float4 v = *reinterpret_cast<const float4*>(p);
+            v.x += pb[0][c];
+            v.y += pb[1][c];
+            v.z += pb[2][c];
+            v.w += pb[3][c];
+            *reinterpret_cast<float4*>(p) = v;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (x4 + k < W1) p[k] = p[k] + pb[k][c];
         }
     }
 }
