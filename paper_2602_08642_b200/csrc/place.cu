@@ -238,10 +238,26 @@ __device__ __forceinline__ double frame_max(const double* pmax, int b) {
     return m;
 }
 
+__device__ __forceinline__ double frame_sum(const double* psum, int b) {
+    double s = 0.0;
+    for (int k = 0; k < kRedBlocks; ++k) s += psum[b * kRedBlocks + k];
+    return s;
+}
+
+// the frame's max / sum of the partials, once per frame (same serial order as
+// frame_max / frame_sum): out[2b] = max, out[2b+1] = sum (when psum given)
+__global__ void k_frame_stats(const double* pmax, const double* psum, double* out) {
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (psum) out[2 * b + 1] = frame_sum(psum, b);
+        else out[2 * b] = frame_max(pmax, b);
+    }
+}
+
 template <typename TS>
-__global__ void k_partial_sum(long long n, const TS* scores, const double* pmax, double* psum) {
+__global__ void k_partial_sum(long long n, const TS* scores, const double* fstat, double* psum) {
     const int b = blockIdx.y;
-    const double m = frame_max(pmax, b);
+    const double m = fstat[2 * b];
     const TS* p = scores + (long long)b * n;
     double s = 0.0;
     for (long long i = (long long)blockIdx.x * kRedThreads + threadIdx.x; i < n;
@@ -251,22 +267,12 @@ __global__ void k_partial_sum(long long n, const TS* scores, const double* pmax,
     if (threadIdx.x == 0) psum[b * kRedBlocks + blockIdx.x] = s;
 }
 
-__device__ __forceinline__ double frame_sum(const double* psum, int b) {
-    double s = 0.0;
-    for (int k = 0; k < kRedBlocks; ++k) s += psum[b * kRedBlocks + k];
-    return s;
-}
 
 // spp = budget/8 + (7/8 * budget * N) * (e / sum)   (density.py:63-64)
-__global__ void k_density_apply(long long n, const double* scores, const double* pmax,
-                                const double* psum, double budget, double* spp) {
+__global__ void k_density_apply(long long n, const double* scores, const double* fstat, double budget,
+                                double* spp) {
     const int b = blockIdx.y;
-    __shared__ double sm, ss;
-    if (threadIdx.x == 0) {
-        sm = frame_max(pmax, b);
-        ss = frame_sum(psum, b);
-    }
-    __syncthreads();
+    const double sm = fstat[2 * b], ss = fstat[2 * b + 1];
     const double adaptive = (1.0 - 0.125) * budget * (double)n;
     for (long long i = (long long)blockIdx.x * kRedThreads + threadIdx.x; i < n;
          i += (long long)gridDim.x * kRedThreads) {
@@ -276,19 +282,13 @@ __global__ void k_density_apply(long long n, const double* scores, const double*
 }
 
 // fused inference placement: scores f32 -> spp -> counts/mask -> noisy f32
-__global__ void k_place_fused(ssb_place_desc d, const float* scores, const double* pmax,
-                              const double* psum, const float* bank, float* noisy, float* spp_out,
-                              uint8_t* taken_out) {
+__global__ void k_place_fused(ssb_place_desc d, const float* scores, const double* fstat, const float* bank,
+                              float* noisy, float* spp_out, uint8_t* taken_out) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int b = blockIdx.z;
-    __shared__ double sm, ss;
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-        sm = frame_max(pmax, b);
-        ss = frame_sum(psum, b);
-    }
-    __syncthreads();
     if (x >= d.W || y >= d.H) return;
+    const double sm = fstat[2 * b], ss = fstat[2 * b + 1];
     const long long hw = (long long)d.H * d.W, p = (long long)y * d.W + x;
     const double adaptive = (1.0 - 0.125) * d.budget * (double)hw;
     const double e = exp((double)scores[b * hw + p] - sm);
@@ -312,12 +312,16 @@ __global__ void k_place_fused(ssb_place_desc d, const float* scores, const doubl
     if (taken_out) taken_out[b * hw + p] = taken;
 }
 
+// partial maxima -> frame max -> partial sums of exp(s - max) -> frame sum
+// (fstat[2b] = max, fstat[2b+1] = sum)
 template <typename TS>
 static void launch_reductions(int B, long long n, const TS* scores, double* pmax, double* psum,
-                              cudaStream_t s) {
+                              double* fstat, cudaStream_t s) {
     dim3 grid(kRedBlocks, B);
     SSB_LAUNCH(s, k_partial_max<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax));
-    SSB_LAUNCH(s, k_partial_sum<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax, psum));
+    SSB_LAUNCH(s, k_frame_stats<<<B, 32, 0, s>>>(pmax, nullptr, fstat));
+    SSB_LAUNCH(s, k_partial_sum<TS><<<grid, kRedThreads, 0, s>>>(n, scores, fstat, psum));
+    SSB_LAUNCH(s, k_frame_stats<<<B, 32, 0, s>>>(pmax, psum, fstat));
 }
 
 }  // namespace ssb
@@ -342,7 +346,7 @@ int ssb_density_workspace_bytes(int B, int H, int W, size_t* bytes) {
         set_error("ssb_density_workspace_bytes: bad arguments");
         return SSB_EINVAL;
     }
-    *bytes = (size_t)2 * B * kRedBlocks * sizeof(double);
+    *bytes = ((size_t)2 * B * kRedBlocks + 2 * (size_t)B) * sizeof(double);
     return SSB_OK;
 }
 
@@ -359,9 +363,10 @@ int ssb_normalize_density(int B, int H, int W, const double* scores, double budg
     const long long n = (long long)H * W;
     double* pmax = (double*)workspace;
     double* psum = pmax + (size_t)B * kRedBlocks;
+    double* fstat = psum + (size_t)B * kRedBlocks;
     cudaStream_t s = (cudaStream_t)stream;
-    launch_reductions<double>(B, n, scores, pmax, psum, s);
-    SSB_LAUNCH(s, k_density_apply<<<dim3(kRedBlocks, B), kRedThreads, 0, s>>>(n, scores, pmax, psum, budget, spp));
+    launch_reductions<double>(B, n, scores, pmax, psum, fstat, s);
+    SSB_LAUNCH(s, k_density_apply<<<dim3(kRedBlocks, B), kRedThreads, 0, s>>>(n, scores, fstat, budget, spp));
     return cuda_check("ssb_normalize_density");
 }
 
@@ -446,10 +451,11 @@ int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* b
     const long long n = (long long)d->H * d->W;
     double* pmax = (double*)workspace;
     double* psum = pmax + (size_t)d->B * kRedBlocks;
+    double* fstat = psum + (size_t)d->B * kRedBlocks;
     cudaStream_t s = (cudaStream_t)stream;
-    launch_reductions<float>(d->B, n, scores, pmax, psum, s);
+    launch_reductions<float>(d->B, n, scores, pmax, psum, fstat, s);
     dim3 block(32, 8), grid((d->W + 31) / 32, (d->H + 7) / 8, d->B);
-    SSB_LAUNCH(s, k_place_fused<<<grid, block, 0, s>>>(*d, scores, pmax, psum, bank, noisy, spp_out, taken_out));
+    SSB_LAUNCH(s, k_place_fused<<<grid, block, 0, s>>>(*d, scores, fstat, bank, noisy, spp_out, taken_out));
     return cuda_check("ssb_place_fused");
 }
 
