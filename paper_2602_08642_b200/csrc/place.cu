@@ -199,7 +199,7 @@ __global__ void k_allocate(ssb_alloc_desc d, const double* spp, const int64_t* r
 
 // ---------------------------------------------------------------- frame-global softmax
 constexpr int kRedThreads = 256;
-constexpr int kRedBlocks = 256;  // partials per frame
+constexpr int kRedBlocks = 1024;  // partials per frame
 
 __device__ __forceinline__ double block_reduce(double v, bool is_max) {
     __shared__ double sh[kRedThreads / 32];
@@ -232,25 +232,29 @@ __global__ void k_partial_max(long long n, const TS* scores, double* pmax) {
     if (threadIdx.x == 0) pmax[b * kRedBlocks + blockIdx.x] = m;
 }
 
-__device__ __forceinline__ double frame_max(const double* pmax, int b) {
+__device__ __forceinline__ double frame_max(const double* pmax, int b, int nblk = kRedBlocks) {
     double m = -INFINITY;
-    for (int k = 0; k < kRedBlocks; ++k) m = fmax(m, pmax[b * kRedBlocks + k]);
+    for (int k = 0; k < nblk; ++k) m = fmax(m, pmax[b * kRedBlocks + k]);
     return m;
 }
 
-__device__ __forceinline__ double frame_sum(const double* psum, int b) {
+__device__ __forceinline__ double frame_sum(const double* psum, int b, int nblk = kRedBlocks) {
     double s = 0.0;
-    for (int k = 0; k < kRedBlocks; ++k) s += psum[b * kRedBlocks + k];
+    for (int k = 0; k < nblk; ++k) s += psum[b * kRedBlocks + k];
     return s;
 }
 
 // the frame's max / sum of the partials, once per frame (same serial order as
 // frame_max / frame_sum): out[2b] = max, out[2b+1] = sum (when psum given)
-__global__ void k_frame_stats(const double* pmax, const double* psum, double* out) {
+__global__ void k_frame_stats(const double* pmax, const double* psum, double* out, int nblk) {
+    __shared__ double sh[kRedBlocks];
     const int b = blockIdx.x;
-    if (threadIdx.x == 0) {
-        if (psum) out[2 * b + 1] = frame_sum(psum, b);
-        else out[2 * b] = frame_max(pmax, b);
+    const double* src = psum ? psum : pmax;
+    for (int k = threadIdx.x; k < nblk; k += blockDim.x) sh[k] = src[b * kRedBlocks + k];
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the serial order of frame_max / frame_sum, from shared memory
+        if (psum) out[2 * b + 1] = frame_sum(sh, 0, nblk);
+        else out[2 * b] = frame_max(sh, 0, nblk);
     }
 }
 
@@ -300,12 +304,13 @@ __global__ void k_place_fused(ssb_place_desc d, const float* scores, const doubl
     const int S = d.capacity;
     const int idx = (int)(fl < (double)(S - 1) ? fl : (double)(S - 1));
     const double sden = spp > 1e-8 ? spp : 1e-8;
+    const double rs = 1.0 / sden;  // one division; the float32 result rounds the same to ~1 ulp
     const float* bp = bank + (long long)b * S * 3 * hw + p;
     for (int c = 0; c < 3; ++c) {
         double acc = 0.0;
         for (int j = 0; j < idx; ++j) acc += (double)bp[(j * 3 + c) * hw];
         if (taken) acc += (double)bp[(idx * 3 + c) * hw];
-        const double nv = acc / sden;
+        const double nv = acc * rs;
         noisy[(b * 3 + c) * hw + p] = (float)(nv > 0.0 ? nv : 0.0);
     }
     if (spp_out) spp_out[b * hw + p] = (float)spp;
@@ -317,11 +322,15 @@ __global__ void k_place_fused(ssb_place_desc d, const float* scores, const doubl
 template <typename TS>
 static void launch_reductions(int B, long long n, const TS* scores, double* pmax, double* psum,
                               double* fstat, cudaStream_t s) {
-    dim3 grid(kRedBlocks, B);
+    // ~8 values per thread, 1..kRedBlocks blocks per frame (small frames: few blocks)
+    long long nb = (n + kRedThreads * 8 - 1) / (kRedThreads * 8);
+    nb = nb < 1 ? 1 : (nb > kRedBlocks ? kRedBlocks : nb);
+    dim3 grid((unsigned)nb, B), sgrid(B, (unsigned)nb);  // (k_frame_stats reads nb from gridDim.y)
     SSB_LAUNCH(s, k_partial_max<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax));
-    SSB_LAUNCH(s, k_frame_stats<<<B, 32, 0, s>>>(pmax, nullptr, fstat));
+    SSB_LAUNCH(s, k_frame_stats<<<dim3(B, 1), 256, 0, s>>>(pmax, nullptr, fstat, (int)nb));
     SSB_LAUNCH(s, k_partial_sum<TS><<<grid, kRedThreads, 0, s>>>(n, scores, fstat, psum));
-    SSB_LAUNCH(s, k_frame_stats<<<B, 32, 0, s>>>(pmax, psum, fstat));
+    SSB_LAUNCH(s, k_frame_stats<<<dim3(B, 1), 256, 0, s>>>(pmax, psum, fstat, (int)nb));
+    (void)sgrid;
 }
 
 }  // namespace ssb
