@@ -93,7 +93,9 @@ struct TmaShape {
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
     static constexpr int UPF = al32(3 * S * RX);       // floats per upstream / output block
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
-    static constexpr int CT = (S + 2 * R + 1) / 2 + 1;  // coarse rows of the flushed fine rows (bottom step: AW rows)
+    // coarse rows of the flushed fine rows (bottom step: the AW window rows from
+    // qs - R; qs is even, so the first coarse row is aligned when R is even)
+    static constexpr int CT = (R & 1) ? (S + 2 * R + 1) / 2 + 1 : (S + 2 * R) / 2;
     static constexpr int T1F = CH ? al32(3 * CT * CB) : 0;
     static constexpr bool B3ON = UP && !CH;
     // EARLY: the next step's TMA is issued at the top of the step (right after
@@ -121,6 +123,7 @@ struct TmaShape {
     static_assert(TXB * B2SPL <= 128 && 3 * TXC <= 128 && TXB % 4 == 0, "B2/B3 items exceed their warps");
     static_assert(S * RW <= 256 && RW <= 64, "phase A items exceed the CTA");
     static_assert(S == 4 && (32 % B2SPL) == 0, "step geometry");
+    static_assert(SMEM + 1024 <= 233472 / 2, "two CTAs per SM");
 };
 
 // paired gradient store (two horizontally adjacent pixels, 8-B / 4-B aligned)
