@@ -178,6 +178,44 @@ __global__ void k_score_dot_max(int F, int C, long long n, const T* __restrict__
     if (threadIdx.x == 0) pmax[b * kDotBlocks + blockIdx.x] = m;
 }
 
+// float32, four pixels per thread (16-B loads; n % 4 == 0, aligned planes):
+// the same per-pixel float sums as k_score_dot_max
+__global__ void __launch_bounds__(kSgThreads) k_score_dot_max_f32v4(int F, int C, unsigned n4,
+                                                                    const float* __restrict__ gin,
+                                                                    const float* __restrict__ gd,
+                                                                    const float* __restrict__ scores,
+                                                                    float* __restrict__ gspp, double* pmax) {
+    const int b = blockIdx.y;
+    const unsigned n = 4u * n4;
+    const float4* sc4 = reinterpret_cast<const float4*>(scores + (size_t)b * n);
+    float4* out4 = reinterpret_cast<float4*>(gspp + (size_t)b * n);
+    float m = -INFINITY;
+    for (unsigned p = blockIdx.x * kSgThreads + threadIdx.x; p < n4; p += gridDim.x * kSgThreads) {
+        float tot[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int f = 0; f < F; ++f) {
+            const float4* g4 = reinterpret_cast<const float4*>(gin + ((size_t)(b * F + f) * C) * n) + p;
+            const float4* d4 = reinterpret_cast<const float4*>(gd + ((size_t)(b * F + f) * C) * n) + p;
+            float4 gg = __ldcs(g4), dd = __ldcs(d4);
+            float sv[4] = {gg.x * dd.x, gg.y * dd.y, gg.z * dd.z, gg.w * dd.w};
+            for (int c = 1; c < C; ++c) {
+                gg = __ldcs(g4 + (size_t)c * n4);
+                dd = __ldcs(d4 + (size_t)c * n4);
+                sv[0] = sv[0] + gg.x * dd.x;
+                sv[1] = sv[1] + gg.y * dd.y;
+                sv[2] = sv[2] + gg.z * dd.z;
+                sv[3] = sv[3] + gg.w * dd.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tot[j] = f == 0 ? sv[j] : tot[j] + sv[j];
+        }
+        out4[p] = make_float4(tot[0], tot[1], tot[2], tot[3]);
+        const float4 s4 = __ldg(sc4 + p);
+        m = fmaxf(m, fmaxf(fmaxf(s4.x, s4.y), fmaxf(s4.z, s4.w)));
+    }
+    const double md = sg_block_reduce((double)m, true);
+    if (threadIdx.x == 0) pmax[b * kDotBlocks + blockIdx.x] = md;
+}
+
 __global__ void k_max_reduce(const double* __restrict__ pmax, double* __restrict__ fmaxv) {
     const int b = blockIdx.x;
     double m = -INFINITY;
@@ -241,6 +279,80 @@ __global__ void __launch_bounds__(SG_TX * SG_TY) k_blur_sums(int H, int W, BlurW
     }
 }
 
+// compile-time radius R: 64 x 16 tile per CTA (four outputs per thread),
+// unrolled taps, constant-divisor window indexing -- same sums in the same
+// order as k_blur_sums
+constexpr int SB_TX = 64, SB_TY = 16;
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_blur_sums_r(int H, int W, BlurWeights bw, const acc_t<T>* __restrict__ g0,
+                                                     const T* __restrict__ scores, const double* __restrict__ pmax,
+                                                     acc_t<T>* __restrict__ g1, double* __restrict__ pse,
+                                                     double* __restrict__ psd) {
+    using A = acc_t<T>;
+    constexpr int NX = SB_TX + 2 * R, NY = SB_TY + 2 * R, NWIN = NX * NY;
+    extern __shared__ __align__(16) unsigned char smem_blur[];
+    A* s_in = reinterpret_cast<A*>(smem_blur);  // [NY][NX]
+    A* s_v = s_in + NWIN;                        // [SB_TY][NX]
+    const int b = blockIdx.z, tid = threadIdx.x;
+    const int x0 = blockIdx.x * SB_TX, y0 = blockIdx.y * SB_TY;
+    const A* gb = g0 + (size_t)b * H * W;
+    A w[R + 1];
+#pragma unroll
+    for (int j = 0; j <= R; ++j) w[j] = (A)bw.w[j];
+    const double m = pmax[b];
+    constexpr int NIT = (NWIN + 255) / 256;
+    A v[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {  // every load issued before the stores
+        const int i = tid + it * 256;
+        const int wy = i / NX, wx = i - wy * NX;
+        const int yy = clampi(y0 - R + wy, 0, H - 1), xx = clampi(x0 - R + wx, 0, W - 1);
+        v[it] = i < NWIN ? gb[(size_t)yy * W + xx] : (A)0;
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it)
+        if (tid + it * 256 < NWIN) s_in[tid + it * 256] = v[it];
+    __syncthreads();
+    for (int i = tid; i < SB_TY * NX; i += 256) {  // axis 0
+        const int ty = i / NX, tx = i - ty * NX;
+        const A* c = s_in + (ty + R) * NX + tx;
+        A a = c[0] * w[0];
+#pragma unroll
+        for (int j = R; j >= 1; --j) a = a + (c[-j * NX] + c[j * NX]) * w[j];
+        s_v[i] = a;
+    }
+    __syncthreads();
+    double se = 0.0, sd = 0.0;
+    const int lx = tid & 63, ly = tid >> 6;
+#pragma unroll
+    for (int h = 0; h < SB_TY / 4; ++h) {  // axis 1
+        const int ty = ly + 4 * h, x = x0 + lx, y = y0 + ty;
+        if (x >= W || y >= H) continue;
+        const A* c = s_v + ty * NX + lx + R;
+        A a = c[0] * w[0];
+#pragma unroll
+        for (int j = R; j >= 1; --j) a = a + (c[-j] + c[j]) * w[j];
+        const size_t o = (size_t)b * H * W + (size_t)y * W + x;
+        g1[o] = a;
+        const double e = sg_exp(scores[o], m);
+        se += e;
+        sd += e * (double)a;
+    }
+    se = sg_block_reduce(se, false);
+    sd = sg_block_reduce(sd, false);
+    if (tid == 0) {
+        const long long k = ((long long)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        pse[k] = se;
+        psd[k] = sd;
+    }
+}
+
+template <typename T, int R>
+size_t blur_r_smem() {
+    return (size_t)((SB_TX + 2 * R) * (SB_TY + 2 * R) + SB_TY * (SB_TX + 2 * R)) * sizeof(acc_t<T>);
+}
+
 // per-frame totals of the tile partials (fixed order: deterministic)
 __global__ void k_sums_reduce(int nblk, const double* __restrict__ pse, const double* __restrict__ psd,
                               double* __restrict__ tot) {
@@ -275,6 +387,46 @@ __global__ void k_sg_apply_tot(long long n, const T* __restrict__ scores, const 
     }
 }
 
+// float32 apply, four pixels per thread; w = e * (1 / sum e) (<= 1 ulp of
+// float64 off the division, far below the float32 output rounding)
+__global__ void __launch_bounds__(kSgThreads) k_sg_apply_f32v4(unsigned n4, const float* __restrict__ scores,
+                                                               const float* __restrict__ g, const double* pmax,
+                                                               const double* __restrict__ tot, double total,
+                                                               float* __restrict__ out) {
+    const int b = blockIdx.y;
+    const unsigned n = 4u * n4;
+    const double sm = pmax[b], rs = 1.0 / tot[2 * b], inner = tot[2 * b + 1] / tot[2 * b];
+    const float4* s4 = reinterpret_cast<const float4*>(scores + (size_t)b * n);
+    const float4* g4 = reinterpret_cast<const float4*>(g + (size_t)b * n);
+    float4* o4 = reinterpret_cast<float4*>(out + (size_t)b * n);
+    for (unsigned i = blockIdx.x * kSgThreads + threadIdx.x; i < n4; i += gridDim.x * kSgThreads) {
+        const float4 sv = __ldcs(s4 + i), gv = __ldcs(g4 + i);
+        const float ss[4] = {sv.x, sv.y, sv.z, sv.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w};
+        float r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = (float)(total * ((sg_exp(ss[j], sm) * rs) * ((double)gg[j] - inner)));
+        __stcs(o4 + i, make_float4(r[0], r[1], r[2], r[3]));
+    }
+}
+
+template <typename T, int R>
+bool launch_blur_r(int r, dim3 grid, int H, int W, const BlurWeights& bw, const acc_t<T>* g0, const T* sc,
+                   const double* fmx, acc_t<T>* g1, double* pse, double* psd, cudaStream_t s) {
+    if constexpr (R > SG_RMAX) {
+        return false;
+    } else {
+        if (r != R) return launch_blur_r<T, R + 1>(r, grid, H, W, bw, g0, sc, fmx, g1, pse, psd, s);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_blur_sums_r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)blur_r_smem<T, R>());
+            attr = true;
+        }
+        SSB_LAUNCH(s, k_blur_sums_r<T, R><<<grid, 256, blur_r_smem<T, R>(), s>>>(H, W, bw, g0, sc, fmx, g1, pse, psd));
+        return true;
+    }
+}
+
 template <typename T>
 int score_grad_fused(int B, int F, int C, int H, int W, const T* gin, const T* gd, const T* sc, double total,
                      const BlurWeights& bw, T* out, char* ws, cudaStream_t s) {
@@ -282,19 +434,41 @@ int score_grad_fused(int B, int F, int C, int H, int W, const T* gin, const T* g
     using A = acc_t<T>;
     A* g0 = (A*)ws;
     A* g1 = g0 + (size_t)B * n;
-    dim3 tgrid((W + SG_TX - 1) / SG_TX, (H + SG_TY - 1) / SG_TY, B);
+    // f32: the radius-templated 64 x 16 tiles; f64 (parity mode): 32 x 8
+    constexpr bool RT = sizeof(T) == 4;
+    dim3 tgrid = RT ? dim3((W + SB_TX - 1) / SB_TX, (H + SB_TY - 1) / SB_TY, B)
+                    : dim3((W + SG_TX - 1) / SG_TX, (H + SG_TY - 1) / SG_TY, B);
     const int nblk = tgrid.x * tgrid.y;
     double* pmax = (double*)(ws + 2 * (size_t)B * n * sizeof(double));  // B x kDotBlocks
     double* fmx = pmax + (size_t)B * kDotBlocks;  // B
     double* pse = fmx + B;
     double* psd = pse + (size_t)B * nblk;
     double* tot = psd + (size_t)B * nblk;
-    SSB_LAUNCH(s, k_score_dot_max<T><<<dim3(kDotBlocks, B), kSgThreads, 0, s>>>(F, C, n, gin, gd, sc, g0, pmax));
+    bool v4 = false;
+    if constexpr (RT) {
+        v4 = n % 4 == 0 && 3 * n < (1ll << 31);
+        for (const void* q : {(const void*)gin, (const void*)gd, (const void*)sc, (const void*)out})
+            if (reinterpret_cast<size_t>(q) & 15) v4 = false;
+    }
+    if (v4)
+        SSB_LAUNCH(s, k_score_dot_max_f32v4<<<dim3(kDotBlocks, B), kSgThreads, 0, s>>>(
+                          F, C, (unsigned)(n / 4), (const float*)gin, (const float*)gd, (const float*)sc,
+                          (float*)g0, pmax));
+    else
+        SSB_LAUNCH(s, k_score_dot_max<T><<<dim3(kDotBlocks, B), kSgThreads, 0, s>>>(F, C, n, gin, gd, sc, g0, pmax));
     SSB_LAUNCH(s, k_max_reduce<<<B, kSgThreads, 0, s>>>(pmax, fmx));
-    SSB_LAUNCH(s, k_blur_sums<T><<<tgrid, dim3(SG_TX, SG_TY), 0, s>>>(H, W, bw, g0, sc, fmx, g1, pse, psd));
+    if (RT) {
+        if (!launch_blur_r<T, 0>(bw.r, tgrid, H, W, bw, g0, sc, fmx, g1, pse, psd, s)) return SSB_EUNSUPPORTED;
+    } else {
+        SSB_LAUNCH(s, k_blur_sums<T><<<tgrid, dim3(SG_TX, SG_TY), 0, s>>>(H, W, bw, g0, sc, fmx, g1, pse, psd));
+    }
     SSB_LAUNCH(s, k_sums_reduce<<<B, kSgThreads, 0, s>>>(nblk, pse, psd, tot));
     const unsigned ag = (unsigned)((n + kSgThreads - 1) / kSgThreads < 4096 ? (n + kSgThreads - 1) / kSgThreads : 4096);
-    SSB_LAUNCH(s, k_sg_apply_tot<T><<<dim3(ag, B), kSgThreads, 0, s>>>(n, sc, g1, fmx, tot, total, out));
+    if (v4)
+        SSB_LAUNCH(s, k_sg_apply_f32v4<<<dim3((ag + 3) / 4, B), kSgThreads, 0, s>>>(
+                          (unsigned)(n / 4), (const float*)sc, (const float*)g1, fmx, tot, total, (float*)out));
+    else
+        SSB_LAUNCH(s, k_sg_apply_tot<T><<<dim3(ag, B), kSgThreads, 0, s>>>(n, sc, g1, fmx, tot, total, out));
     return 0;
 }
 

@@ -4,10 +4,11 @@
 //   warp_backward images.py:122-147  grad_prev = transpose (np.add.at scatter)
 // The transpose is computed as a deterministic GATHER: every target pixel
 // scans the sources that can reach it (|q - p| <= ceil(max|motion|) + 1,
-// staged in shared memory per tile when max|motion| <= 5), in float64 in the
+// staged in shared memory per tile when max|motion| <= 5; float32 with
+// max|motion| <= 3 through per-cell landing masks), in float64 in the
 // reference's own order (tap-major, then sources in raster order) so the
-// result reproduces np.add.at bit for bit; float32 in one raster pass.  No
-// atomics: results are run-to-run identical.
+// result reproduces np.add.at bit for bit; float32 in a fixed order.  No
+// floating-point atomics: results are run-to-run identical.
 // Compiled with -fmad=false (products and sums rounded like numpy).
 #include <math.h>
 #include <string>
@@ -98,6 +99,81 @@ __global__ void __launch_bounds__(256) k_warp(int C, int H, int W, const T* __re
     }
 }
 
+// float32, 3 channels: the CTA stages prev over its tile + a 4-pixel halo
+// (coalesced rows) and gathers the taps from shared memory; a tap outside the
+// staged window (|motion| > 3) falls back to a global load, per thread.
+constexpr int WF_X = 32, WF_Y = 16, WF_WX = WF_X + 8, WF_WY = WF_Y + 8;
+
+__global__ void __launch_bounds__(256) k_warp_staged(int H, int W, const float* __restrict__ prev,
+                                                     const float* __restrict__ motion, float* __restrict__ out,
+                                                     float* __restrict__ validity) {
+    constexpr int NWIN = WF_WY * WF_WX;
+    __shared__ float s_p[3][NWIN];
+    const int b = blockIdx.z, tid = threadIdx.x;
+    const int tx0 = blockIdx.x * WF_X, ty0 = blockIdx.y * WF_Y;
+    const int wx0 = tx0 - 4, wy0 = ty0 - 4;
+    const unsigned hw = (unsigned)H * (unsigned)W;
+    const float* mb = motion + (size_t)b * 2 * hw;
+    const float* pb = prev + (size_t)b * 3 * hw;
+    constexpr int NIT = (NWIN + 255) / 256;
+    float pv[NIT][3];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {  // every load issued before the stores
+        const int i = tid + it * 256;
+        const int wj = i / WF_WX, wi = i - wj * WF_WX;
+        const int qx = wx0 + wi, qy = wy0 + wj;
+        const bool in = i < NWIN && qx >= 0 && qx < W && qy >= 0 && qy < H;
+        const unsigned q = in ? (unsigned)qy * (unsigned)W + (unsigned)qx : 0u;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pv[it][c] = in ? __ldg(pb + c * hw + q) : 0.f;
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const int i = tid + it * 256;
+        if (i < NWIN)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) s_p[c][i] = pv[it][c];
+    }
+    __syncthreads();
+    const int lx = tid & 31;
+#pragma unroll
+    for (int h = 0; h < WF_Y / 8; ++h) {
+        const int x = tx0 + lx, y = ty0 + (tid >> 5) + 8 * h;
+        if (x >= W || y >= H) continue;
+        const unsigned p = (unsigned)y * (unsigned)W + (unsigned)x;
+        const float mx = __ldg(mb + p), my = __ldg(mb + hw + p);
+        float w[4], v[4][3];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int ix, iy;
+            warp_tap(k, x, y, W, H, mx, my, w[k], ix, iy);
+            const int li = ix - wx0, lj = iy - wy0;
+            if ((unsigned)li < (unsigned)WF_WX && (unsigned)lj < (unsigned)WF_WY) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v[k][c] = s_p[c][lj * WF_WX + li];
+            } else {
+                const unsigned src = (unsigned)iy * (unsigned)W + (unsigned)ix;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) v[k][c] = __ldg(pb + c * hw + src);
+            }
+        }
+        float* ob = out + (size_t)b * 3 * hw;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc = acc + w[k] * v[k][c];
+            __stcs(ob + c * hw + p, acc);
+        }
+        if (validity) {
+            float vs = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) vs = vs + w[k];
+            __stcs(validity + (size_t)b * hw + p, vs);
+        }
+    }
+}
+
 // per-frame max |motion| as ordered float bits (non-negative floats order like
 // their bit patterns), for the gather window of the transpose
 template <typename T>
@@ -116,16 +192,45 @@ __global__ void k_motion_absmax(long long n, const T* __restrict__ motion, unsig
     if ((threadIdx.x & 31) == 0) atomicMax(amax + b, (unsigned long long)__double_as_longlong(m));
 }
 
-// Tiled transpose for |motion| <= WMAX: the CTA stages, for every source of
-// its window (tile + MR halo), the integer floor offset, the fractions and
-// the gradient, then every target scans its (2 MR + 1)^2 sources from shared
-// memory.  EXACT (float64): one pass per tap, sources in raster order -- the
-// np.add.at order; otherwise one pass over the sources (raster order, each
-// source reaches a target through at most one tap): deterministic.
+// float32: max over the bit patterns of |m| (NaN ignored), 16-B loads when
+// the frame stride allows; stored as the double bits k_motion_absmax writes
+__global__ void k_motion_absmax_f32(long long n2, const float* __restrict__ motion, unsigned long long* amax) {
+    const int b = blockIdx.y;
+    const float* mb = motion + (size_t)b * n2;
+    unsigned m = 0u;
+    auto take = [&](float v) {
+        const unsigned a = __float_as_uint(v) & 0x7fffffffu;
+        m = max(m, a > 0x7f800000u ? 0u : a);
+    };
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    if (((reinterpret_cast<size_t>(mb)) & 15) == 0) {
+        const long long n4 = n2 >> 2;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+            const float4 v = __ldcs(reinterpret_cast<const float4*>(mb) + i);
+            take(v.x);
+            take(v.y);
+            take(v.z);
+            take(v.w);
+        }
+        for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) take(mb[i]);
+    } else {
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) take(mb[i]);
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m)
+        atomicMax(amax + b, (unsigned long long)__double_as_longlong((double)__uint_as_float(m)));
+}
+
+// Float64 tiled transpose for |motion| <= WMAX - 1: the CTA stages, for every
+// source of its window (tile + MR halo), the integer floor offset, the
+// fractions and the gradient, then every target scans its (2 MR + 1)^2
+// sources from shared memory, one pass per tap, sources in raster order --
+// the np.add.at order (bit-exact).
 constexpr int WT_X = 32, WT_Y = 8, WMAX = 6;
+constexpr int WM_MR = 4;  // float32 frames with MR <= WM_MR: k_warp_backward_mask
 constexpr int WWX = WT_X + 2 * WMAX, WWY = WT_Y + 2 * WMAX;
 
-template <typename T, bool EXACT>
+template <typename T>
 __global__ void __launch_bounds__(WT_X * WT_Y) k_warp_backward_tiled(
     int C, int H, int W, const T* __restrict__ gout, const T* __restrict__ motion,
     const unsigned long long* __restrict__ amax, T* __restrict__ gprev) {
@@ -213,33 +318,19 @@ __global__ void __launch_bounds__(WT_X * WT_Y) k_warp_backward_tiled(
 #pragma unroll
             for (int c = 0; c < 3; ++c) acc[c] = acc[c] + wgt * s_g[c][li];
         };
-        if constexpr (EXACT) {
-            for (int k = 0; k < 4; ++k) {
-                const int kdy = k >> 1, kdx = k & 1;
-                for (int j = j0; j <= j1; ++j) {
-                    const int qy = y - MR + j;
-                    if (qy < 0 || qy >= H) continue;
-                    for (int i = i0; i <= i1; ++i) {
-                        const int qx = x - MR + i;
-                        if (qx < 0 || qx >= W) continue;
-                        const int li = (ly0 + j) * wnx + lx0 + i;
-                        const int off = s_off[li];
-                        if (off < 0) continue;
-                        // tap k of q lands on (qx + ox + kdx, qy + oy + kdy)
-                        if (qx + (off & 255) - 128 + kdx != x || qy + (off >> 8) - 128 + kdy != y) continue;
-                        take(li, kdx, kdy, s_fx[li], s_fy[li]);
-                    }
-                }
-            }
-        } else {
+        for (int k = 0; k < 4; ++k) {
+            const int kdy = k >> 1, kdx = k & 1;
             for (int j = j0; j <= j1; ++j) {
+                const int qy = y - MR + j;
+                if (qy < 0 || qy >= H) continue;
                 for (int i = i0; i <= i1; ++i) {
+                    const int qx = x - MR + i;
+                    if (qx < 0 || qx >= W) continue;
                     const int li = (ly0 + j) * wnx + lx0 + i;
                     const int off = s_off[li];
                     if (off < 0) continue;
-                    const int kdx = x - (x - MR + i) - ((off & 255) - 128);
-                    const int kdy = y - (y - MR + j) - ((off >> 8) - 128);
-                    if ((unsigned)kdx > 1u || (unsigned)kdy > 1u) continue;
+                    // tap k of q lands on (qx + ox + kdx, qy + oy + kdy)
+                    if (qx + (off & 255) - 128 + kdx != x || qy + (off >> 8) - 128 + kdy != y) continue;
                     take(li, kdx, kdy, s_fx[li], s_fy[li]);
                 }
             }
@@ -248,20 +339,153 @@ __global__ void __launch_bounds__(WT_X * WT_Y) k_warp_backward_tiled(
     }
 }
 
-// general transpose (any |motion|; frames whose max |motion| exceeds WMAX - 1)
+// float32 transpose for max|motion| <= 3 (MR <= 4): instead of scanning
+// every candidate source per target, each source of the window marks its
+// tap-0 landing cell t0 = q + o (o = floor offset) in a per-cell bit mask
+// (native shared atomicOr, order independent), then target p visits, tap by
+// tap, the set bits of cell p - k in ascending order -- ~4 hits instead of
+// ~25 candidates, deterministic.  Masks: NWD = 1 word per cell when
+// max|motion| <= 2 (o in [-2, 2]^2, bit (oy + 2) * 5 + ox + 2), NWD = 2 when
+// <= 3 (o in [-3, 3]^2, word oy > 0, bit ((oy + 3) & 3) * 8 + ox + 3).  The
+// sources keep their four tap weights; a bit decodes to the source's window
+// offset through a small table.  Larger motion runs the general per-target
+// scan in the same kernel (one launch either way).
+constexpr int WM_X = 32, WM_Y = 16;                 // tile
+constexpr int WM_WX = WM_X + 7, WM_WY = WM_Y + 7;   // sources q - p in [-4, 3] per axis
+constexpr int WM_MX = WM_X + 1, WM_MY = WM_Y + 1;   // landing cells t0 in [tile - 1, tile)
+
 template <typename T>
-__global__ void k_warp_backward(int C, int H, int W, const T* __restrict__ gout,
-                                const T* __restrict__ motion, const unsigned long long* __restrict__ amax,
-                                T* __restrict__ gprev) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+__device__ void warp_backward_scan(int C, int H, int W, int b, int x, int y, int MR, const T* __restrict__ gout,
+                                   const T* __restrict__ motion, T* __restrict__ gprev);
+
+struct MaskSmem {
+    static constexpr int NWIN = WM_WY * WM_WX;
+    float4 wg[4][NWIN];  // per source and tap: w_k * g_c (c < 3), w_k = wx * wy (images.py:101-117)
+    unsigned m[2][WM_MY * WM_MX];
+    int lut[64];         // bit -> window offset of the source from its cell
+};
+
+template <int NWD>
+__device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, int W, int b, int tx0, int ty0,
+                                                   const float* __restrict__ gout, const float* __restrict__ motion,
+                                                   float* __restrict__ gprev) {
+    constexpr int NWIN = MaskSmem::NWIN, OB = NWD == 1 ? 2 : 3;  // |o| bound
+    const int tid = threadIdx.x, lx = tid & 31, ly0 = tid >> 5;
+    const int wx0 = tx0 - 4, wy0 = ty0 - 4;  // window origin; cell origin is tile - 1
+    const unsigned hw = (unsigned)H * (unsigned)W;
+    const float* mb = motion + (size_t)b * 2 * hw;
+    for (int i = tid; i < NWD * WM_MY * WM_MX; i += 256) (&sm.m[0][0])[i] = 0u;
+    if (tid < 32 * NWD) {
+        int oy, ox;
+        if (NWD == 1) {
+            oy = tid / 5 - 2;
+            ox = tid % 5 - 2;
+        } else {
+            oy = ((tid & 31) >> 3) + (tid >= 32 ? 1 : -3);
+            ox = (tid & 7) - 3;
+        }
+        sm.lut[tid] = (3 - oy) * WM_WX + (3 - ox);
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < C; c0 += 3) {
+        const int nc = min(3, C - c0);
+        if (c0 > 0) __syncthreads();
+        // stage: landing masks (first group), tap weights times the gradient;
+        // every load of the thread's window items is issued before any use
+        constexpr int NIT = (NWIN + 255) / 256;
+        const float* gp = gout + ((size_t)b * C + c0) * hw;  // 32-bit offsets below (C*H*W < 2^31)
+        float mv[NIT][2], gv[NIT][3];
+        bool inw[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int i = tid + it * 256;
+            const int wj = i / WM_WX, wi = i - wj * WM_WX;
+            const int qx = wx0 + wi, qy = wy0 + wj;
+            inw[it] = i < NWIN && qx >= 0 && qx < W && qy >= 0 && qy < H;  // others never land
+            const unsigned q = inw[it] ? (unsigned)qy * (unsigned)W + (unsigned)qx : 0u;
+            mv[it][0] = inw[it] ? __ldg(mb + q) : 0.f;
+            mv[it][1] = inw[it] ? __ldg(mb + hw + q) : 0.f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) gv[it][c] = (inw[it] && c < nc) ? __ldg(gp + (c * hw + q)) : 0.f;
+        }
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            if (!inw[it]) continue;
+            const int i = tid + it * 256;
+            const int wj = i / WM_WX, wi = i - wj * WM_WX;
+            const float mx = mv[it][0], my = mv[it][1];
+            const float fmx = floorf(mx), fmy = floorf(my);
+            const float fx = mx - fmx, fy = my - fmy;
+            if (c0 == 0 && fmx >= (float)-OB && fmx <= (float)OB && fmy >= (float)-OB && fmy <= (float)OB) {
+                const int ox = (int)fmx, oy = (int)fmy;  // (false for NaN motion)
+                const int u = wi - 3 + ox, v = wj - 3 + oy;  // cell of t0 = q + o
+                if (u >= 0 && u < WM_MX && v >= 0 && v < WM_MY) {
+                    if (NWD == 1) atomicOr(&sm.m[0][v * WM_MX + u], 1u << ((oy + 2) * 5 + ox + 2));
+                    else atomicOr(&sm.m[oy > 0][v * WM_MX + u], 1u << (((oy + 3) & 3) * 8 + ox + 3));
+                }
+            }
+            const float wk[4] = {(1.f - fx) * (1.f - fy), fx * (1.f - fy), (1.f - fx) * fy, fx * fy};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                sm.wg[k][i] = make_float4(wk[k] * gv[it][0], wk[k] * gv[it][1], wk[k] * gv[it][2], 0.f);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < WM_Y / 8; ++h) {
+            const int ly = ly0 + 8 * h, x = tx0 + lx, y = ty0 + ly;
+            if (x >= W || y >= H) continue;
+            float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int cell = (ly + 1 - (k >> 1)) * WM_MX + lx + 1 - (k & 1);  // t0 = p - k
+                const float4* wgk = sm.wg[k] + (ly + 1 - (k >> 1)) * WM_WX + lx + 1 - (k & 1);
+#pragma unroll
+                for (int wd = 0; wd < NWD; ++wd) {
+                    unsigned m = sm.m[wd][cell];
+                    while (m) {
+                        const int bit = __ffs(m) - 1;
+                        m &= m - 1;
+                        const float4 t = wgk[sm.lut[wd * 32 + bit]];  // source q = t0 - o
+                        acc[0] = acc[0] + t.x;
+                        acc[1] = acc[1] + t.y;
+                        acc[2] = acc[2] + t.z;
+                    }
+                }
+            }
+            float* op = gprev + ((size_t)b * C + c0) * hw + ((unsigned)y * (unsigned)W + x);
+            for (int c = 0; c < nc; ++c) __stcs(op + c * hw, acc[c]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_warp_backward_mask(int C, int H, int W, const float* __restrict__ gout,
+                                                            const float* __restrict__ motion,
+                                                            const unsigned long long* __restrict__ amax,
+                                                            float* __restrict__ gprev) {
+    extern __shared__ __align__(16) unsigned char smem_mask[];
+    MaskSmem& sm = *reinterpret_cast<MaskSmem*>(smem_mask);
     const int b = blockIdx.z;
-    if (x >= W || y >= H) return;
-    const long long hw = (long long)H * W;
+    const int tx0 = blockIdx.x * WM_X, ty0 = blockIdx.y * WM_Y;
     const double mm = __longlong_as_double((long long)amax[b]);
-    if ((int)ceil(mm) + 1 <= WMAX) return;  // handled by the tiled kernel
-    // sources farther than ceil(max|m|) + 1 cannot land on this pixel
-    const int MR = (int)fmin(ceil(mm) + 1.0, (double)(H > W ? H : W));
+    if (mm <= 2.0) {
+        warp_bwd_mask_body<1>(sm, C, H, W, b, tx0, ty0, gout, motion, gprev);
+    } else if (mm <= 3.0) {
+        warp_bwd_mask_body<2>(sm, C, H, W, b, tx0, ty0, gout, motion, gprev);
+    } else {  // large (or non-finite) motion: general scan
+        const int MR = (int)fmin(ceil(mm) + 1.0, (double)(H > W ? H : W));
+        for (int h = 0; h < WM_Y / 8; ++h) {
+            const int x = tx0 + (threadIdx.x & 31), y = ty0 + (threadIdx.x >> 5) + 8 * h;
+            if (x < W && y < H) warp_backward_scan<float>(C, H, W, b, x, y, MR, gout, motion, gprev);
+        }
+    }
+}
+
+// general transpose (any |motion|): target (x, y) scans every source within
+// MR, np.add.at order (tap-major, sources in raster order)
+template <typename T>
+__device__ void warp_backward_scan(int C, int H, int W, int b, int x, int y, int MR, const T* __restrict__ gout,
+                                   const T* __restrict__ motion, T* __restrict__ gprev) {
+    const long long hw = (long long)H * W;
     const int qy0 = max(y - MR, 0), qy1 = min(y + MR, H - 1);
     const int qx0 = max(x - MR, 0), qx1 = min(x + MR, W - 1);
     constexpr int CMAX = 4;
@@ -270,7 +494,7 @@ __global__ void k_warp_backward(int C, int H, int W, const T* __restrict__ gout,
         T acc[CMAX];
 #pragma unroll
         for (int c = 0; c < CMAX; ++c) acc[c] = (T)0;
-        for (int k = 0; k < 4; ++k) {  // np.add.at order: tap-major, sources in raster order
+        for (int k = 0; k < 4; ++k) {
             for (int qy = qy0; qy <= qy1; ++qy) {
                 for (int qx = qx0; qx <= qx1; ++qx) {
                     const long long q = (long long)qy * W + qx;
@@ -287,6 +511,22 @@ __global__ void k_warp_backward(int C, int H, int W, const T* __restrict__ gout,
         }
         for (int c = 0; c < nc; ++c) gprev[((long long)b * C + c0 + c) * hw + (long long)y * W + x] = acc[c];
     }
+}
+
+// float64 frames whose max |motion| exceeds WMAX - 1
+template <typename T>
+__global__ void k_warp_backward(int C, int H, int W, const T* __restrict__ gout,
+                                const T* __restrict__ motion, const unsigned long long* __restrict__ amax,
+                                T* __restrict__ gprev) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int b = blockIdx.z;
+    if (x >= W || y >= H) return;
+    const double mm = __longlong_as_double((long long)amax[b]);
+    if ((int)ceil(mm) + 1 <= WMAX) return;  // handled by the tiled kernel
+    // sources farther than ceil(max|m|) + 1 cannot land on this pixel
+    const int MR = (int)fmin(ceil(mm) + 1.0, (double)(H > W ? H : W));
+    warp_backward_scan<T>(C, H, W, b, x, y, MR, gout, motion, gprev);
 }
 
 }  // namespace ssb
@@ -315,7 +555,8 @@ int ssb_warp(int dtype, int B, int C, int H, int W, const void* prev, const void
     } else if (dtype == SSB_F32) {
         auto* pr = (const float*)prev;
         auto* mo = (const float*)motion;
-        if (C == 3) SSB_LAUNCH(s, k_warp<float, 3><<<grid, block, 0, s>>>(C, H, W, pr, mo, (float*)out, (float*)validity));
+        dim3 sgrid((W + WF_X - 1) / WF_X, (H + WF_Y - 1) / WF_Y, B);
+        if (C == 3) SSB_LAUNCH(s, k_warp_staged<<<sgrid, 256, 0, s>>>(H, W, pr, mo, (float*)out, (float*)validity));
         else SSB_LAUNCH(s, k_warp<float, 0><<<grid, block, 0, s>>>(C, H, W, pr, mo, (float*)out, (float*)validity));
     } else {
         set_error("ssb_warp: dtype must be f32 or f64");
@@ -343,6 +584,10 @@ int ssb_warp_backward(int dtype, int B, int C, int H, int W, const void* grad_ou
         set_error("ssb_warp_backward: dtype must be f32 or f64");
         return SSB_EUNSUPPORTED;
     }
+    if ((long long)H * W * C >= (1ll << 31)) {
+        set_error("ssb_warp_backward: H*W*C must be < 2^31 per frame");
+        return SSB_EUNSUPPORTED;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* amax = (unsigned long long*)workspace;
     cudaMemsetAsync(amax, 0, (size_t)B * sizeof(unsigned long long), s);
@@ -352,16 +597,23 @@ int ssb_warp_backward(int dtype, int B, int C, int H, int W, const void* grad_ou
     dim3 tgrid((W + WT_X - 1) / WT_X, (H + WT_Y - 1) / WT_Y, B);
     if (dtype == SSB_F64) {
         SSB_LAUNCH(s, k_motion_absmax<double><<<rgrid, 256, 0, s>>>(n, (const double*)motion, amax));
-        SSB_LAUNCH(s, k_warp_backward_tiled<double, true><<<tgrid, dim3(WT_X, WT_Y), 0, s>>>(
+        SSB_LAUNCH(s, k_warp_backward_tiled<double><<<tgrid, dim3(WT_X, WT_Y), 0, s>>>(
                           C, H, W, (const double*)grad_out, (const double*)motion, amax, (double*)grad_prev));
         SSB_LAUNCH(s, k_warp_backward<double><<<grid, block, 0, s>>>(C, H, W, (const double*)grad_out,
                                                                    (const double*)motion, amax, (double*)grad_prev));
     } else {
-        SSB_LAUNCH(s, k_motion_absmax<float><<<rgrid, 256, 0, s>>>(n, (const float*)motion, amax));
-        SSB_LAUNCH(s, k_warp_backward_tiled<float, false><<<tgrid, dim3(WT_X, WT_Y), 0, s>>>(
-                          C, H, W, (const float*)grad_out, (const float*)motion, amax, (float*)grad_prev));
-        SSB_LAUNCH(s, k_warp_backward<float><<<grid, block, 0, s>>>(C, H, W, (const float*)grad_out,
-                                                                  (const float*)motion, amax, (float*)grad_prev));
+        const long long b4 = (2 * n + 1023) / 1024;
+        SSB_LAUNCH(s, k_motion_absmax_f32<<<dim3((unsigned)(b4 < 296 ? b4 : 296), B), 256, 0, s>>>(
+                          2 * n, (const float*)motion, amax));
+        dim3 mgrid((W + WM_X - 1) / WM_X, (H + WM_Y - 1) / WM_Y, B);
+        static bool attr = false;  // (idempotent; races only repeat the call)
+        if (!attr) {
+            cudaFuncSetAttribute(k_warp_backward_mask, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(MaskSmem));
+            attr = true;
+        }
+        SSB_LAUNCH(s, k_warp_backward_mask<<<mgrid, 256, sizeof(MaskSmem), s>>>(C, H, W, (const float*)grad_out,
+                                                                 (const float*)motion, amax, (float*)grad_prev));
     }
     return cuda_check("ssb_warp_backward");
 }

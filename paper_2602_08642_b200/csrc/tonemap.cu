@@ -99,6 +99,112 @@ __global__ void k_tonemap_backward(long long n, Tmo p, const T* __restrict__ rad
     }
 }
 
+// ---- float32, four pixels per thread (16-B loads / streaming stores):
+// branch-free filmic pieces, reciprocals of toe / shoulder precomputed, MUFU
+// log2 / exp2 (relative error ~1e-6, inside the fp32 tolerance)
+struct TmoF {
+    float exposure, contrast, saturation, toe, shoulder, itoe, ish;
+};
+
+__device__ __forceinline__ void filmic_f(float x, const TmoF& p, float& y, float& dy) {  // tonemap.py:45-69
+    const bool lo = x < p.toe - 1.f, hi = x >= 1.f - p.shoulder;
+    const float z = lo ? (x + 1.f - p.toe) * p.itoe : -(x + p.shoulder - 1.f) * p.ish;
+    const float e = exp2f(fminf(z, 0.f) * 1.4426950408889634f);
+    y = lo ? 0.5f * p.toe * e : (hi ? 1.f - 0.5f * p.shoulder * e : 0.5f * (1.f + x));
+    dy = (lo || hi) ? 0.5f * e : 0.5f;
+}
+
+__device__ __forceinline__ void log_augment_f(const float rad[3], const TmoF& p, float x[3]) {
+    float c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c[k] = __log2f(fmaxf(rad[k], (float)kLogFloor)) * 0.6931471805599453f;
+    const float m = ((c[0] + c[1]) + c[2]) * (1.f / 3.f);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) x[k] = p.contrast * ((m + p.saturation * (c[k] - m)) + p.exposure);
+}
+
+__device__ __forceinline__ float srgb_f(float v) {  // tonemap.py:72-78
+    return v <= 0.0031308f ? v * 12.92f : 1.055f * exp2f(__log2f(v) * (1.f / 2.4f)) - 0.055f;
+}
+__device__ __forceinline__ float srgb_d_f(float v) {  // tonemap.py:81-84
+    return v <= 0.0031308f ? 12.92f : (1.055f / 2.4f) * exp2f(__log2f(v) * (1.f / 2.4f - 1.f));
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, const float v[4]) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void unpack4(const float4 v, float o[4]) {
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+}
+
+// n4 = H * W / 4 quads per plane; 32-bit offsets inside a frame (3 n < 2^31)
+__global__ void __launch_bounds__(256) k_tonemap_f32v4(unsigned n4, TmoF p, const float* __restrict__ rad,
+                                                       float* __restrict__ ldr) {
+    const int b = blockIdx.y;
+    const unsigned n = 4u * n4;
+    const float* rb = rad + (size_t)b * 3 * n;
+    float* lb = ldr + (size_t)b * 3 * n;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        float r[3][4], y[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) unpack4(ld4(rb + c * n + 4 * i), r[c]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float v[3] = {r[0][j], r[1][j], r[2][j]};
+            float x[3];
+            log_augment_f(v, p, x);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float f, df;
+                filmic_f(x[c], p, f, df);
+                y[c][j] = srgb_f(f);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) st4(lb + c * n + 4 * i, y[c]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tonemap_backward_f32v4(unsigned n4, TmoF p, const float* __restrict__ rad,
+                                                                const float* __restrict__ up,
+                                                                float* __restrict__ grad) {
+    const int b = blockIdx.y;
+    const unsigned n = 4u * n4;
+    const size_t fo = (size_t)b * 3 * n;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        float r[3][4], u[3][4], g[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            unpack4(ld4(rad + fo + c * n + 4 * i), r[c]);
+            unpack4(ld4(up + fo + c * n + 4 * i), u[c]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float v[3] = {r[0][j], r[1][j], r[2][j]};
+            float x[3], gx[3];
+            log_augment_f(v, p, x);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float f, df;
+                filmic_f(x[c], p, f, df);
+                gx[c] = u[c][j] * srgb_d_f(f) * df;
+            }
+            const float gs = (gx[0] + gx[1]) + gx[2];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float gc = p.contrast * (p.saturation * gx[c] + (1.f - p.saturation) * (1.f / 3.f) * gs);
+                g[c][j] = v[c] > (float)kLogFloor ? __fdividef(gc, v[c]) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) st4(grad + fo + c * n + 4 * i, g[c]);
+    }
+}
+
 __device__ __forceinline__ double lr_block_sum(double v) {
     __shared__ double sh[8];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -113,53 +219,6 @@ __device__ __forceinline__ double lr_block_sum(double v) {
 }
 
 constexpr int kLossBlocks = 512;
-
-// per-pixel maps (spatial / temporal / combined) and per-block partials of
-// their sums (+ the valid count): losses.py:58-91
-template <typename T>
-__global__ void __launch_bounds__(256) k_loss_maps(long long n, const T* __restrict__ out1, const T* __restrict__ ref,
-                                                   const T* __restrict__ out0w, const T* __restrict__ refw,
-                                                   const T* __restrict__ validity, const T* __restrict__ mask,
-                                                   T* sp_map, T* tm_map, T* cb_map, double* part) {
-    const int b = blockIdx.y;
-    double ssp = 0.0, stm = 0.0, scb = 0.0, scnt = 0.0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const long long o = (long long)b * 3 * n + i, pm = (long long)b * n + i;
-        T sp = (T)0, tm = (T)0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sp = sp + fabs(out1[o + k * n] - ref[o + k * n]);
-        sp = sp / (T)3 * (mask ? mask[pm] : (T)1);
-        if (out0w) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                tm = tm + fabs((out1[o + k * n] - out0w[o + k * n]) - (ref[o + k * n] - refw[o + k * n]));
-            tm = tm / (T)3;
-            if (validity) {
-                const bool valid = validity[pm] >= (T)1;
-                tm = valid ? tm : (T)0;
-                scnt += valid ? 1.0 : 0.0;
-            }
-        }
-        const T cb = fmax((T)kTemporalWeight * tm, sp);
-        if (sp_map) sp_map[pm] = sp;
-        if (tm_map) tm_map[pm] = tm;
-        if (cb_map) cb_map[pm] = cb;
-        ssp += (double)sp;
-        stm += (double)tm;
-        scb += (double)cb;
-    }
-    ssp = lr_block_sum(ssp);
-    stm = lr_block_sum(stm);
-    scb = lr_block_sum(scb);
-    scnt = lr_block_sum(scnt);
-    if (threadIdx.x == 0) {
-        double* q = part + ((long long)b * kLossBlocks + blockIdx.x) * 4;
-        q[0] = ssp;
-        q[1] = stm;
-        q[2] = scb;
-        q[3] = scnt;
-    }
-}
 
 // losses[b] = (spatial, temporal, combined) means
 __global__ void k_loss_reduce(long long n, int has_temporal, int has_validity, const double* __restrict__ part,
@@ -178,42 +237,123 @@ __global__ void k_loss_reduce(long long n, int has_temporal, int has_validity, c
 
 template <typename T>
 __device__ __forceinline__ T sgn(T v) { return v > (T)0 ? (T)1 : (v < (T)0 ? (T)-1 : (T)0); }
+// x / 3: IEEE division in float64 (bit-exact with numpy); float32 multiplies
+// by the rounded reciprocal (<= 1 ulp, inside the fp32 tolerance)
+__device__ __forceinline__ double div3(double x) { return x / 3.0; }
+__device__ __forceinline__ float div3(float x) { return x * (1.f / 3.f); }
 
-// gradients of the combined loss w.r.t. ldr1 and the warped ldr0
-// (optimize.py:219-231)
+// Per-pixel maps (spatial / temporal / combined, losses.py:58-91),
+// per-block partials of their sums (+ the valid count) and the gradients of
+// the combined loss w.r.t. ldr1 and the warped ldr0 (optimize.py:219-231) in
+// ONE pass over the inputs; V = 4
+// pixels per iteration with 16-B loads (float32, n % 4 == 0, aligned planes)
+template <typename T, int V>
+struct Vec;
+template <>
+struct Vec<float, 4> {
+    static __device__ __forceinline__ void ld(const float* p, float o[4]) { unpack4(ld4(p), o); }
+    static __device__ __forceinline__ void st(float* p, const float v[4]) { st4(p, v); }
+};
 template <typename T>
-__global__ void k_loss_grads(long long n, const T* __restrict__ out1, const T* __restrict__ ref,
-                             const T* __restrict__ out0w, const T* __restrict__ refw,
-                             const T* __restrict__ validity, const T* __restrict__ mask, T* __restrict__ g1,
-                             T* __restrict__ g0w) {
+struct Vec<T, 1> {
+    static __device__ __forceinline__ void ld(const T* p, T o[1]) { o[0] = *p; }
+    static __device__ __forceinline__ void st(T* p, const T v[1]) { *p = v[0]; }
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 2) k_loss_fused(long long n, const T* __restrict__ out1, const T* __restrict__ ref,
+                                                    const T* __restrict__ out0w, const T* __restrict__ refw,
+                                                    const T* __restrict__ validity, const T* __restrict__ mask,
+                                                    T* sp_map, T* tm_map, T* cb_map, double* part,
+                                                    T* __restrict__ g1, T* __restrict__ g0w) {
+    using VL = Vec<T, V>;
     const int b = blockIdx.y;
     const T inv_n = (T)1 / (T)n;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const long long o = (long long)b * 3 * n + i, pm = (long long)b * n + i;
-        const T w = mask ? mask[pm] : (T)1;
-        T sp = (T)0, tm = (T)0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sp = sp + fabs(out1[o + k * n] - ref[o + k * n]);
-        sp = sp / (T)3 * w;
-        if (out0w) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                tm = tm + fabs((out1[o + k * n] - out0w[o + k * n]) - (ref[o + k * n] - refw[o + k * n]));
-            tm = tm / (T)3;
-            if (validity && !(validity[pm] >= (T)1)) tm = (T)0;
-        }
-        const bool twins = (T)kTemporalWeight * tm > sp;  // ties to the spatial term
-        const T gsp = twins ? (T)0 : inv_n, gtm = twins ? (T)kTemporalWeight / (T)n : (T)0;
+    double ssp = 0.0, stm = 0.0, scb = 0.0, scnt = 0.0;
+    const long long nv = n / V;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+        const long long o = (long long)b * 3 * n + V * i, pm = (long long)b * n + V * i;
+        T a1[3][V], rf[3][V], a0[3][V], rw[3][V], val[V], w[V];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            const T s1 = sgn(out1[o + k * n] - ref[o + k * n]);
-            T v = s1 * (gsp * w) / (T)3;
+            VL::ld(out1 + o + k * n, a1[k]);
+            VL::ld(ref + o + k * n, rf[k]);
             if (out0w) {
-                const T st = sgn((out1[o + k * n] - out0w[o + k * n]) - (ref[o + k * n] - refw[o + k * n]));
-                v = v + st * gtm / (T)3;
-                if (g0w) g0w[o + k * n] = -st * gtm / (T)3;
+                VL::ld(out0w + o + k * n, a0[k]);
+                VL::ld(refw + o + k * n, rw[k]);
             }
-            g1[o + k * n] = v;
+        }
+        if (validity) VL::ld(validity + pm, val);
+        if (mask) VL::ld(mask + pm, w);
+        else
+#pragma unroll
+            for (int j = 0; j < V; ++j) w[j] = (T)1;
+        T spv[V], tmv[V], cbv[V], cs[V], ct[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            T sp = (T)0, tm = (T)0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) sp = sp + fabs(a1[k][j] - rf[k][j]);
+            sp = div3(sp) * w[j];
+            if (out0w) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tm = tm + fabs((a1[k][j] - a0[k][j]) - (rf[k][j] - rw[k][j]));
+                tm = div3(tm);
+                if (validity) {
+                    const bool valid = val[j] >= (T)1;
+                    tm = valid ? tm : (T)0;
+                    scnt += valid ? 1.0 : 0.0;
+                }
+            }
+            const T cb = fmax((T)kTemporalWeight * tm, sp);
+            spv[j] = sp;
+            tmv[j] = tm;
+            cbv[j] = cb;
+            ssp += (double)sp;
+            stm += (double)tm;
+            scb += (double)cb;
+            // optimize.py:219-231 (ties to the spatial term); s * x / 3 ==
+            // s * (x / 3) exactly for a sign s, so the /3 is hoisted
+            const bool twins = (T)kTemporalWeight * tm > sp;
+            const T gsp = twins ? (T)0 : inv_n, gtm = twins ? (T)kTemporalWeight / (T)n : (T)0;
+            cs[j] = div3(gsp * w[j]);
+            ct[j] = div3(gtm);
+        }
+        if (sp_map) VL::st(sp_map + pm, spv);
+        if (tm_map) VL::st(tm_map + pm, tmv);
+        if (cb_map) VL::st(cb_map + pm, cbv);
+        if (g1) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                T gv1[V], gv0[V];
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    T v = sgn(a1[k][j] - rf[k][j]) * cs[j];
+                    if (out0w) {
+                        const T st = sgn((a1[k][j] - a0[k][j]) - (rf[k][j] - rw[k][j]));
+                        v = v + st * ct[j];
+                        gv0[j] = -st * ct[j];
+                    }
+                    gv1[j] = v;
+                }
+                VL::st(g1 + o + k * n, gv1);
+                if (g0w) VL::st(g0w + o + k * n, gv0);
+            }
+        }
+    }
+    // (reduced unconditionally: a shuffle under a branch the compiler cannot
+    // prove uniform is emulated per active subset)
+    ssp = lr_block_sum(ssp);
+    stm = lr_block_sum(stm);
+    scb = lr_block_sum(scb);
+    scnt = lr_block_sum(scnt);
+    {
+        if (part && threadIdx.x == 0) {
+            double* q = part + ((long long)b * kLossBlocks + blockIdx.x) * 4;
+            q[0] = ssp;
+            q[1] = stm;
+            q[2] = scb;
+            q[3] = scnt;
         }
     }
 }
@@ -229,6 +369,24 @@ dim3 grid_for(long long n, int B) {
 using namespace ssb;
 
 extern "C" {
+
+static TmoF tmo_f(const Tmo& p) {
+    return TmoF{(float)p.exposure, (float)p.contrast, (float)p.saturation, (float)p.toe, (float)p.shoulder,
+                (float)(1.0 / p.toe), (float)(1.0 / p.shoulder)};
+}
+
+// the float32 vector kernels: whole quads per plane, 16-B aligned planes,
+// 32-bit offsets inside a frame
+static bool vec4_ok(long long n, int B, const void* a, const void* b = nullptr, const void* c = nullptr,
+                    const void* d = nullptr, const void* e = nullptr, const void* f = nullptr,
+                    const void* g = nullptr, const void* h = nullptr, const void* i = nullptr,
+                    const void* j = nullptr) {
+    (void)B;
+    if (n % 4 != 0 || 3 * n >= (1ll << 31)) return false;
+    for (const void* q : {a, b, c, d, e, f, g, h, i, j})
+        if (q && (reinterpret_cast<size_t>(q) & 15)) return false;
+    return true;
+}
 
 static int tmo_check(const double* tmo, Tmo* p) {
     if (!tmo) return SSB_EINVAL;
@@ -249,6 +407,9 @@ int ssb_tonemap(int dtype, int B, int H, int W, const double* tmo, const void* r
     cudaStream_t s = (cudaStream_t)stream;
     const long long n = (long long)H * W;
     if (dtype == SSB_F64) SSB_LAUNCH(s, k_tonemap<double><<<grid_for<double>(n, B), 256, 0, s>>>(n, p, (const double*)radiance, (double*)ldr));
+    else if (dtype == SSB_F32 && vec4_ok(n, B, radiance, ldr))
+        SSB_LAUNCH(s, k_tonemap_f32v4<<<grid_for<float>(n / 4, B), 256, 0, s>>>((unsigned)(n / 4), tmo_f(p),
+                                                                               (const float*)radiance, (float*)ldr));
     else if (dtype == SSB_F32) SSB_LAUNCH(s, k_tonemap<float><<<grid_for<float>(n, B), 256, 0, s>>>(n, p, (const float*)radiance, (float*)ldr));
     else {
         set_error("ssb_tonemap: dtype must be f32 or f64");
@@ -269,6 +430,9 @@ int ssb_tonemap_backward(int dtype, int B, int H, int W, const double* tmo, cons
     if (dtype == SSB_F64)
         SSB_LAUNCH(s, k_tonemap_backward<double><<<grid_for<double>(n, B), 256, 0, s>>>(
                           n, p, (const double*)radiance, (const double*)upstream, (double*)grad));
+    else if (dtype == SSB_F32 && vec4_ok(n, B, radiance, upstream, grad))
+        SSB_LAUNCH(s, k_tonemap_backward_f32v4<<<grid_for<float>(n / 4, B), 256, 0, s>>>(
+                          (unsigned)(n / 4), tmo_f(p), (const float*)radiance, (const float*)upstream, (float*)grad));
     else if (dtype == SSB_F32)
         SSB_LAUNCH(s, k_tonemap_backward<float><<<grid_for<float>(n, B), 256, 0, s>>>(
                           n, p, (const float*)radiance, (const float*)upstream, (float*)grad));
@@ -303,20 +467,21 @@ int ssb_losses(int dtype, int B, int H, int W, const void* ldr1, const void* ref
     }
     cudaStream_t s = (cudaStream_t)stream;
     const long long n = (long long)H * W;
+    const bool sums = losses != nullptr;
     auto run = [&](auto tag) {
         using T = decltype(tag);
-        if (losses || sp_map || tm_map || cb_map) {
-            SSB_LAUNCH(s, k_loss_maps<T><<<dim3(kLossBlocks, B), 256, 0, s>>>(
-                              n, (const T*)ldr1, (const T*)ref, (const T*)ldr0_w, (const T*)ref_w, (const T*)validity,
-                              (const T*)mask, (T*)sp_map, (T*)tm_map, (T*)cb_map, (double*)workspace));
-            if (losses)
-                SSB_LAUNCH(s, k_loss_reduce<<<B, 256, 0, s>>>(n, ldr0_w != nullptr, validity != nullptr,
-                                                              (const double*)workspace, losses));
-        }
-        if (g_ldr1)
-            SSB_LAUNCH(s, k_loss_grads<T><<<grid_for<T>(n, B), 256, 0, s>>>(
-                              n, (const T*)ldr1, (const T*)ref, (const T*)ldr0_w, (const T*)ref_w, (const T*)validity,
-                              (const T*)mask, (T*)g_ldr1, (T*)g_ldr0_w));
+        if (!(sums || sp_map || tm_map || cb_map || g_ldr1)) return;
+        const bool v4 = sizeof(T) == 4 && vec4_ok(n, B, ldr1, ref, ldr0_w, ref_w, validity, mask, sp_map, tm_map,
+                                                   cb_map, g_ldr1) &&
+                        vec4_ok(n, B, g_ldr0_w);
+        auto kern = v4 ? k_loss_fused<T, sizeof(T) == 4 ? 4 : 1> : k_loss_fused<T, 1>;
+        SSB_LAUNCH(s, kern<<<dim3(kLossBlocks, B), 256, 0, s>>>(
+                          n, (const T*)ldr1, (const T*)ref, (const T*)ldr0_w, (const T*)ref_w, (const T*)validity,
+                          (const T*)mask, (T*)sp_map, (T*)tm_map, (T*)cb_map, sums ? (double*)workspace : nullptr,
+                          (T*)g_ldr1, (T*)g_ldr0_w));
+        if (sums)
+            SSB_LAUNCH(s, k_loss_reduce<<<B, 256, 0, s>>>(n, ldr0_w != nullptr, validity != nullptr,
+                                                          (const double*)workspace, losses));
     };
     if (dtype == SSB_F64) run(0.0);
     else run(0.0f);

@@ -56,6 +56,39 @@ def test_warp_f32_vs_oracle(ops):
     np.testing.assert_allclose(hwc(gp), gp_r, rtol=1e-5, atol=1e-5 * np.abs(gp_r).max())
 
 
+@pytest.mark.parametrize("amp,c,h,w", [(0.4, 3, 45, 77), (2.0, 3, 67, 131), (3.0, 3, 40, 33),
+                                       (2.0, 4, 37, 70), (1.5, 1, 19, 200), (3.0, 3, 1, 9)])
+def test_warp_f32_small_motion_vs_oracle(ops, amp, c, h, w):
+    """max|motion| <= 3: the staged forward gather and the landing-mask
+    transpose (temporal.cu), incl. channel counts other than 3 and borders."""
+    rng = np.random.default_rng(int(amp * 10) + c + h)
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    prev = f32(rng.lognormal(-1, 1.5, (h, w, c)))
+    g = f32(rng.normal(size=(h, w, c)))
+    m = f32(rng.uniform(-amp, amp, (h, w, 2)))
+    m[0, 0] = (amp, -amp)  # the extreme offsets
+    out_r, val_r = ot.warp_array(prev, m)
+    gp_r = ot.warp_backward(g, m)
+    out, val = ops.warp(planar(prev, torch.float32), planar(m, torch.float32))
+    gp = ops.warp_backward(planar(g, torch.float32), planar(m, torch.float32))
+    np.testing.assert_allclose(hwc(out), out_r, rtol=1e-5, atol=1e-5 * np.abs(out_r).max())
+    np.testing.assert_allclose(val[0].double().cpu().numpy(), val_r, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(hwc(gp), gp_r, rtol=1e-5, atol=1e-5 * np.abs(gp_r).max())
+
+
+def test_warp_f32_deterministic_and_adjoint_1080p(ops):
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn((2, 3, 1080, 1920), device="cuda", generator=gen)
+    g = torch.randn((2, 3, 1080, 1920), device="cuda", generator=gen)
+    m = (torch.rand((2, 2, 1080, 1920), device="cuda", generator=gen) - 0.5) * 4
+    y, _ = ops.warp(x, m)
+    gt1 = ops.warp_backward(g, m)
+    gt2 = ops.warp_backward(g, m)
+    assert torch.equal(gt1, gt2)
+    lhs, rhs = (y.double() * g.double()).sum().item(), (x.double() * gt1.double()).sum().item()
+    assert abs(lhs - rhs) <= 1e-5 * (y.double().abs() * g.double().abs()).sum().item()
+
+
 def test_warp_backward_deterministic_and_adjoint_1080p(ops):
     """Size-independent properties at 1080p: bitwise run-to-run determinism of
     the gather-transpose and <warp(x), g> = <x, warp^T(g)>."""
@@ -107,6 +140,23 @@ def test_score_grad_f32_vs_oracle(ops):
     s_t, gi_t, gd_t = _score_inputs(d, "x", torch.float32)
     r = ops.score_grad(s_t, gi_t, gd_t, 0.25, 1.5)[0].double().cpu().numpy()
     np.testing.assert_allclose(r, ref, rtol=1e-5, atol=1e-5 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("sigma,h,w,f,c", [(0.0, 64, 96, 1, 3), (0.6, 37, 53, 2, 3), (1.5, 64, 100, 3, 1),
+                                           (3.9, 70, 44, 2, 3), (1.5, 1, 257, 2, 3)])
+def test_score_grad_f32_configs_vs_oracle(ops, sigma, h, w, f, c):
+    """float32 estimator backward across blur radii 0..16 (the radius-templated
+    tiles), frame / channel counts, quad-vector and scalar shapes, B = 2."""
+    rng = np.random.default_rng(int(sigma * 10) + h + w)
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    cases = [(f32(rng.normal(size=(h, w))), f32(rng.normal(size=(f, h, w, c))), f32(rng.normal(size=(f, h, w, c))))
+             for _ in range(2)]
+    refs = [osc.score_grad(sc, 0.25, list(gi), list(gd), sigma) for sc, gi, gd in cases]
+    ins = [_score_inputs({"x_gin": gi, "x_gd": gd, "x_scores": sc}, "x", torch.float32) for sc, gi, gd in cases]
+    r = ops.score_grad(torch.cat([i[0] for i in ins]), torch.cat([i[1] for i in ins]),
+                       torch.cat([i[2] for i in ins]), 0.25, sigma).double().cpu().numpy()
+    for k in range(2):
+        np.testing.assert_allclose(r[k], refs[k], rtol=1e-5, atol=1e-5 * np.abs(refs[k]).max())
 
 
 def test_score_grad_sums_to_zero(ops):

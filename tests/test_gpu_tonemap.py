@@ -75,6 +75,45 @@ def test_tonemap_and_losses_f32_vs_oracle(ops):
     np.testing.assert_allclose(hwc(r["g_ldr1"]), g1, rtol=1e-6, atol=1e-12)
 
 
+@pytest.mark.parametrize("h,w", [(64, 96), (33, 51)])  # quad-vector kernels / scalar fallback
+def test_tonemap_and_full_losses_f32_vs_oracle(ops, h, w):
+    """float32: tonemap (all three filmic pieces), tonemap backward, and the
+    single-pass loss kernel with the warped history, validity and a mask:
+    maps, per-frame losses and both gradients."""
+    rng = np.random.default_rng(h + w)
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    B = 2
+    t = (0.2, 1.3, 0.8, 0.35, 0.45)
+    rad = [f32(rng.lognormal(-0.5, 2.5, (h, w, 3))) for _ in range(B)]
+    up = [f32(rng.normal(size=(h, w, 3))) for _ in range(B)]
+    stack = lambda xs: torch.cat([planar(x, torch.float32) for x in xs])  # noqa: E731
+    ldr = ops.tonemap(stack(rad), t)
+    g = ops.tonemap_backward(stack(rad), t, stack(up))
+    for i in range(B):
+        np.testing.assert_allclose(ldr[i].permute(1, 2, 0).double().cpu().numpy(), otm.tonemap(rad[i], t),
+                                   rtol=1e-5, atol=1e-6)
+        gr = otm.tonemap_backward(rad[i], t, up[i])
+        np.testing.assert_allclose(g[i].permute(1, 2, 0).double().cpu().numpy(), gr, rtol=1e-4,
+                                   atol=1e-5 * np.abs(gr).max())
+    img = lambda: [f32(rng.uniform(0, 1, (h, w, 3))) for _ in range(B)]  # noqa: E731
+    a1, rf, a0, rw = img(), img(), img(), img()
+    val = [(rng.uniform(size=(h, w)) > 0.2).astype(np.float64) for _ in range(B)]
+    msk = [f32(rng.uniform(0, 1, (h, w))) for _ in range(B)]
+    tm = lambda xs: torch.from_numpy(np.stack(xs)).cuda().float()  # noqa: E731
+    r = ops.losses(stack(a1), stack(rf), stack(a0), stack(rw), validity=tm(val), mask=tm(msk), want_grads=True)
+    for i in range(B):
+        sp, tmm, cb, vals = otm.losses(a1[i], rf[i], a0[i], rw[i], val[i], msk[i])
+        for key, ref in (("spatial_map", sp), ("temporal_map", tmm), ("combined_map", cb)):
+            np.testing.assert_allclose(r[key][i].double().cpu().numpy(), ref, rtol=1e-6, atol=1e-7)
+        np.testing.assert_allclose(r["losses"][i].cpu().numpy(), vals, rtol=1e-6)
+        g1, g0 = otm.loss_grads(a1[i], rf[i], a0[i], rw[i], val[i], msk[i])
+        # the branch choice (temporal vs spatial) may flip on float32 near-ties
+        agree = np.isclose(r["g_ldr1"][i].permute(1, 2, 0).double().cpu().numpy(), g1, rtol=1e-6, atol=1e-12)
+        assert agree.mean() > 0.999
+        agree0 = np.isclose(r["g_ldr0_w"][i].permute(1, 2, 0).double().cpu().numpy(), g0, rtol=1e-6, atol=1e-12)
+        assert agree0.mean() > 0.999
+
+
 def test_losses_reject_bad_inputs(ops):
     x = torch.zeros((1, 3, 8, 8), device="cuda", dtype=torch.float64)
     with pytest.raises(ValueError):
