@@ -249,6 +249,17 @@ int ssb_losses(int dtype, int B, int H, int W, const void* ldr1, const void* ref
                void* cb_map, double* losses, void* g_ldr1, void* g_ldr0_w, void* workspace,
                ssb_stream_t stream);
 
+/* The evaluate_step epilogue fused (optimize.py:219-231 over tonemap.py and
+ * losses.py): tonemap(radiance) -> losses vs ref (+ warped history) -> the
+ * loss gradient w.r.t. the LDR frame -> chained through the tonemap, in one
+ * pass.  Equals ssb_tonemap + ssb_losses(g_ldr1, g_ldr0_w) +
+ * ssb_tonemap_backward (float64: bit-identical).  grad_radiance required;
+ * ldr (the tonemapped frame), losses (needs the ssb_losses workspace) and
+ * g_ldr0_w optional; ldr0_w/ref_w/validity/mask as in ssb_losses. */
+int ssb_epilogue(int dtype, int B, int H, int W, const double* tmo, const void* radiance, const void* ref,
+                 const void* ldr0_w, const void* ref_w, const void* validity, const void* mask, void* ldr,
+                 double* losses, void* grad_radiance, void* g_ldr0_w, void* workspace, ssb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,7 @@ EXPORTS = (
     "ssb_allocate", "ssb_stochastic_core", "ssb_estimate", "ssb_place_fused",
     "ssb_warp", "ssb_warp_backward_workspace_bytes", "ssb_warp_backward",
     "ssb_score_grad_workspace_bytes", "ssb_score_grad",
-    "ssb_tonemap", "ssb_tonemap_backward", "ssb_losses_workspace_bytes", "ssb_losses",
+    "ssb_tonemap", "ssb_tonemap_backward", "ssb_losses_workspace_bytes", "ssb_losses", "ssb_epilogue",
 )
 
 vp = C.c_void_p
@@ -133,6 +133,7 @@ def load(build_if_missing: bool = False):
             "ssb_tonemap_backward": (C.c_int, [C.c_int] * 4 + [P(C.c_double)] + [vp] * 4),
             "ssb_losses_workspace_bytes": (C.c_int, [C.c_int, P(C.c_size_t)]),
             "ssb_losses": (C.c_int, [C.c_int] * 4 + [vp] * 14),
+            "ssb_epilogue": (C.c_int, [C.c_int] * 4 + [P(C.c_double)] + [vp] * 12),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(lib, name)

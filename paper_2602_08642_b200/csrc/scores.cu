@@ -279,9 +279,14 @@ __global__ void __launch_bounds__(SG_TX * SG_TY) k_blur_sums(int H, int W, BlurW
     }
 }
 
+// acc + x * y: float64 rounds the product (scipy's order; the file is built
+// with -fmad=false), float32 fuses it
+__device__ __forceinline__ double madd(double x, double y, double acc) { return acc + x * y; }
+__device__ __forceinline__ float madd(float x, float y, float acc) { return __fmaf_rn(x, y, acc); }
+
 // compile-time radius R: 64 x 16 tile per CTA (four outputs per thread),
-// unrolled taps, constant-divisor window indexing -- same sums in the same
-// order as k_blur_sums
+// unrolled taps, constant-divisor window indexing -- the sums of k_blur_sums
+// in the same order
 constexpr int SB_TX = 64, SB_TY = 16;
 
 template <typename T, int R>
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(256) k_blur_sums_r(int H, int W, BlurWeights b
         const A* c = s_in + (ty + R) * NX + tx;
         A a = c[0] * w[0];
 #pragma unroll
-        for (int j = R; j >= 1; --j) a = a + (c[-j * NX] + c[j * NX]) * w[j];
+        for (int j = R; j >= 1; --j) a = madd(c[-j * NX] + c[j * NX], w[j], a);
         s_v[i] = a;
     }
     __syncthreads();
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(256) k_blur_sums_r(int H, int W, BlurWeights b
         const A* c = s_v + ty * NX + lx + R;
         A a = c[0] * w[0];
 #pragma unroll
-        for (int j = R; j >= 1; --j) a = a + (c[-j] + c[j]) * w[j];
+        for (int j = R; j >= 1; --j) a = madd(c[-j] + c[j], w[j], a);
         const size_t o = (size_t)b * H * W + (size_t)y * W + x;
         g1[o] = a;
         const double e = sg_exp(scores[o], m);
@@ -457,7 +462,7 @@ int score_grad_fused(int B, int F, int C, int H, int W, const T* gin, const T* g
     else
         SSB_LAUNCH(s, k_score_dot_max<T><<<dim3(kDotBlocks, B), kSgThreads, 0, s>>>(F, C, n, gin, gd, sc, g0, pmax));
     SSB_LAUNCH(s, k_max_reduce<<<B, kSgThreads, 0, s>>>(pmax, fmx));
-    if (RT) {
+    if constexpr (RT) {
         if (!launch_blur_r<T, 0>(bw.r, tgrid, H, W, bw, g0, sc, fmx, g1, pse, psd, s)) return SSB_EUNSUPPORTED;
     } else {
         SSB_LAUNCH(s, k_blur_sums<T><<<tgrid, dim3(SG_TX, SG_TY), 0, s>>>(H, W, bw, g0, sc, fmx, g1, pse, psd));

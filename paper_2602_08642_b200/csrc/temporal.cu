@@ -142,17 +142,35 @@ __global__ void __launch_bounds__(256) k_warp_staged(int H, int W, const float* 
         if (x >= W || y >= H) continue;
         const unsigned p = (unsigned)y * (unsigned)W + (unsigned)x;
         const float mx = __ldg(mb + p), my = __ldg(mb + hw + p);
+        // warp_tap's four taps, sharing the floor / fraction / clamp work:
+        // x0 = x + floor(mx) (float32 split, images.py:101-117), taps x0 and
+        // x0 + 1, weight 0 outside the frame, clamped source indices
+        const float fmx = floorf(mx), fmy = floorf(my);
+        const float fx = mx - fmx, fy = my - fmy;
+        const float tx = (float)x + fmx, ty = (float)y + fmy;
+        float wxs[2], wys[2];
+        int ixs[2], iys[2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            const float ux = tx + (float)d, uy = ty + (float)d;
+            wxs[d] = (ux >= 0.f && ux < (float)W) ? (d ? fx : 1.f - fx) : 0.f;
+            wys[d] = (uy >= 0.f && uy < (float)H) ? (d ? fy : 1.f - fy) : 0.f;
+            ixs[d] = (int)fminf(fmaxf(ux, 0.f), (float)(W - 1));
+            iys[d] = (int)fminf(fmaxf(uy, 0.f), (float)(H - 1));
+        }
         float w[4], v[4][3];
+        const bool inwin = ixs[0] - wx0 >= 0 && ixs[1] - wx0 < WF_WX && iys[0] - wy0 >= 0 && iys[1] - wy0 < WF_WY;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            int ix, iy;
-            warp_tap(k, x, y, W, H, mx, my, w[k], ix, iy);
-            const int li = ix - wx0, lj = iy - wy0;
-            if ((unsigned)li < (unsigned)WF_WX && (unsigned)lj < (unsigned)WF_WY) {
+            const int dx = k & 1, dy = k >> 1;
+            // (NaN motion: both tap weights of an axis are 0 -- the
+            // comparisons fail -- and the clamped index is 0)
+            w[k] = wxs[dx] * wys[dy];
+            if (inwin) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) v[k][c] = s_p[c][lj * WF_WX + li];
+                for (int c = 0; c < 3; ++c) v[k][c] = s_p[c][(iys[dy] - wy0) * WF_WX + ixs[dx] - wx0];
             } else {
-                const unsigned src = (unsigned)iy * (unsigned)W + (unsigned)ix;
+                const unsigned src = (unsigned)iys[dy] * (unsigned)W + (unsigned)ixs[dx];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) v[k][c] = __ldg(pb + c * hw + src);
             }
@@ -162,7 +180,7 @@ __global__ void __launch_bounds__(256) k_warp_staged(int H, int W, const float* 
         for (int c = 0; c < 3; ++c) {
             float acc = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc = acc + w[k] * v[k][c];
+            for (int k = 0; k < 4; ++k) acc = __fmaf_rn(w[k], v[k][c], acc);
             __stcs(ob + c * hw + p, acc);
         }
         if (validity) {

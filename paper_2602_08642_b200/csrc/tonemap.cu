@@ -101,33 +101,41 @@ __global__ void k_tonemap_backward(long long n, Tmo p, const T* __restrict__ rad
 
 // ---- float32, four pixels per thread (16-B loads / streaming stores):
 // branch-free filmic pieces, reciprocals of toe / shoulder precomputed, MUFU
-// log2 / exp2 (relative error ~1e-6, inside the fp32 tolerance)
+// log2 / exp2 (approx.ftz: relative error ~1e-6, inside the fp32 tolerance;
+// inputs are >= the 1e-8 log floor, no denormals), explicit FMAs (the file is
+// built with -fmad=false for the float64 parity kernels)
 struct TmoF {
     float exposure, contrast, saturation, toe, shoulder, itoe, ish;
 };
 
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ void filmic_f(float x, const TmoF& p, float& y, float& dy) {  // tonemap.py:45-69
     const bool lo = x < p.toe - 1.f, hi = x >= 1.f - p.shoulder;
     const float z = lo ? (x + 1.f - p.toe) * p.itoe : -(x + p.shoulder - 1.f) * p.ish;
-    const float e = exp2f(fminf(z, 0.f) * 1.4426950408889634f);
-    y = lo ? 0.5f * p.toe * e : (hi ? 1.f - 0.5f * p.shoulder * e : 0.5f * (1.f + x));
+    const float e = ex2_ftz(fminf(z, 0.f) * 1.4426950408889634f);
+    y = lo ? 0.5f * p.toe * e : (hi ? __fmaf_rn(-0.5f * p.shoulder, e, 1.f) : __fmaf_rn(0.5f, x, 0.5f));
     dy = (lo || hi) ? 0.5f * e : 0.5f;
 }
 
 __device__ __forceinline__ void log_augment_f(const float rad[3], const TmoF& p, float x[3]) {
     float c[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) c[k] = __log2f(fmaxf(rad[k], (float)kLogFloor)) * 0.6931471805599453f;
+    for (int k = 0; k < 3; ++k) c[k] = lg2_ftz(fmaxf(rad[k], (float)kLogFloor)) * 0.6931471805599453f;
     const float m = ((c[0] + c[1]) + c[2]) * (1.f / 3.f);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) x[k] = p.contrast * ((m + p.saturation * (c[k] - m)) + p.exposure);
+    for (int k = 0; k < 3; ++k) x[k] = p.contrast * (__fmaf_rn(p.saturation, c[k] - m, m) + p.exposure);
 }
 
 __device__ __forceinline__ float srgb_f(float v) {  // tonemap.py:72-78
-    return v <= 0.0031308f ? v * 12.92f : 1.055f * exp2f(__log2f(v) * (1.f / 2.4f)) - 0.055f;
+    return v <= 0.0031308f ? v * 12.92f : __fmaf_rn(1.055f, ex2_ftz(lg2_ftz(v) * (1.f / 2.4f)), -0.055f);
 }
 __device__ __forceinline__ float srgb_d_f(float v) {  // tonemap.py:81-84
-    return v <= 0.0031308f ? 12.92f : (1.055f / 2.4f) * exp2f(__log2f(v) * (1.f / 2.4f - 1.f));
+    return v <= 0.0031308f ? 12.92f : (1.055f / 2.4f) * ex2_ftz(lg2_ftz(v) * (1.f / 2.4f - 1.f));
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(256) k_tonemap_backward_f32v4(unsigned n4, Tmo
             const float gs = (gx[0] + gx[1]) + gx[2];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float gc = p.contrast * (p.saturation * gx[c] + (1.f - p.saturation) * (1.f / 3.f) * gs);
+                const float gc = p.contrast * __fmaf_rn(p.saturation, gx[c], (1.f - p.saturation) * (1.f / 3.f) * gs);
                 g[c][j] = v[c] > (float)kLogFloor ? __fdividef(gc, v[c]) : 0.f;
             }
         }
@@ -358,6 +366,131 @@ __global__ void __launch_bounds__(256, 2) k_loss_fused(long long n, const T* __r
     }
 }
 
+// The whole evaluate_step epilogue in ONE pass (optimize.py:219-231 with
+// tonemap.py:36-118): tonemap the radiance, the three losses against the
+// reference (+ the warped history), their gradient w.r.t. the LDR frame, and
+// its chain through the tonemap to the radiance -- per pixel, so nothing but
+// the inputs and the two gradients (and optionally the LDR frame) touches
+// HBM.  float64 evaluates exactly the expressions of k_tonemap, k_loss_fused
+// and k_tonemap_backward (bit-identical to the three-launch composition);
+// float32 uses the fast pieces of the vector kernels.
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 2) k_epilogue(long long n, Tmo p, TmoF pf, const T* __restrict__ rad,
+                                                     const T* __restrict__ ref, const T* __restrict__ out0w,
+                                                     const T* __restrict__ refw, const T* __restrict__ validity,
+                                                     const T* __restrict__ mask, T* __restrict__ ldr_out,
+                                                     double* part, T* __restrict__ grad, T* __restrict__ g0w) {
+    using VL = Vec<T, V>;
+    constexpr bool F32 = sizeof(T) == 4;
+    const int b = blockIdx.y;
+    const T inv_n = (T)1 / (T)n;
+    double ssp = 0.0, stm = 0.0, scb = 0.0, scnt = 0.0;
+    const long long nv = n / V;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+        const long long o = (long long)b * 3 * n + V * i, pm = (long long)b * n + V * i;
+        T rv[3][V], rf[3][V], a0[3][V], rw[3][V], val[V], w[V];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            VL::ld(rad + o + k * n, rv[k]);
+            VL::ld(ref + o + k * n, rf[k]);
+            if (out0w) {
+                VL::ld(out0w + o + k * n, a0[k]);
+                VL::ld(refw + o + k * n, rw[k]);
+            }
+        }
+        if (validity) VL::ld(validity + pm, val);
+        if (mask) VL::ld(mask + pm, w);
+        else
+#pragma unroll
+            for (int j = 0; j < V; ++j) w[j] = (T)1;
+        T a1[3][V], dfy[3][V], gout[3][V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            // tonemap (k_tonemap): x, filmic y, ldr = srgb(y); keep d ldr / dx
+            const T v[3] = {rv[0][j], rv[1][j], rv[2][j]};
+            T x[3];
+            if constexpr (F32) log_augment_f(v, pf, x);
+            else log_augment(v, p, x);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                if constexpr (F32) {
+                    float f, df;
+                    filmic_f(x[k], pf, f, df);
+                    a1[k][j] = srgb_f(f);
+                    dfy[k][j] = srgb_d_f(f) * df;
+                } else {
+                    const T y = filmic(x[k], (T)p.toe, (T)p.shoulder);
+                    a1[k][j] = srgb(y);
+                    dfy[k][j] = srgb_d(y);  // (times filmic_d below, in k_tonemap_backward's order)
+                }
+            }
+            // losses + their LDR gradient (k_loss_fused)
+            T sp = (T)0, tm = (T)0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) sp = sp + fabs(a1[k][j] - rf[k][j]);
+            sp = div3(sp) * w[j];
+            if (out0w) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) tm = tm + fabs((a1[k][j] - a0[k][j]) - (rf[k][j] - rw[k][j]));
+                tm = div3(tm);
+                if (validity) {
+                    const bool valid = val[j] >= (T)1;
+                    tm = valid ? tm : (T)0;
+                    scnt += valid ? 1.0 : 0.0;
+                }
+            }
+            const T cb = fmax((T)kTemporalWeight * tm, sp);
+            ssp += (double)sp;
+            stm += (double)tm;
+            scb += (double)cb;
+            const bool twins = (T)kTemporalWeight * tm > sp;
+            const T gsp = twins ? (T)0 : inv_n, gtm = twins ? (T)kTemporalWeight / (T)n : (T)0;
+            const T cs = div3(gsp * w[j]), ct = div3(gtm);
+            T gx[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                T g1 = sgn(a1[k][j] - rf[k][j]) * cs;
+                if (out0w) {
+                    const T st = sgn((a1[k][j] - a0[k][j]) - (rf[k][j] - rw[k][j]));
+                    g1 = g1 + st * ct;
+                    gout[k][j] = -st * ct;
+                }
+                // tonemap backward (k_tonemap_backward)
+                if constexpr (F32) gx[k] = g1 * dfy[k][j];
+                else gx[k] = g1 * dfy[k][j] * filmic_d(x[k], (T)p.toe, (T)p.shoulder);
+            }
+            const T gs = (gx[0] + gx[1]) + gx[2];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                if constexpr (F32) {
+                    const float gc = pf.contrast * __fmaf_rn(pf.saturation, gx[k], (1.f - pf.saturation) * (1.f / 3.f) * gs);
+                    dfy[k][j] = v[k] > (float)kLogFloor ? __fdividef(gc, v[k]) : 0.f;
+                } else {
+                    const T gc = (T)p.contrast * ((T)p.saturation * gx[k] + ((T)1 - (T)p.saturation) / (T)3 * gs);
+                    dfy[k][j] = v[k] > (T)kLogFloor ? gc / fmax(v[k], (T)kLogFloor) : (T)0;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            VL::st(grad + o + k * n, dfy[k]);
+            if (g0w) VL::st(g0w + o + k * n, gout[k]);
+            if (ldr_out) VL::st(ldr_out + o + k * n, a1[k]);
+        }
+    }
+    ssp = lr_block_sum(ssp);
+    stm = lr_block_sum(stm);
+    scb = lr_block_sum(scb);
+    scnt = lr_block_sum(scnt);
+    if (part && threadIdx.x == 0) {
+        double* q = part + ((long long)b * kLossBlocks + blockIdx.x) * 4;
+        q[0] = ssp;
+        q[1] = stm;
+        q[2] = scb;
+        q[3] = scnt;
+    }
+}
+
 template <typename T>
 dim3 grid_for(long long n, int B) {
     long long g = (n + 255) / 256;
@@ -486,6 +619,39 @@ int ssb_losses(int dtype, int B, int H, int W, const void* ldr1, const void* ref
     if (dtype == SSB_F64) run(0.0);
     else run(0.0f);
     return cuda_check("ssb_losses");
+}
+
+int ssb_epilogue(int dtype, int B, int H, int W, const double* tmo, const void* radiance, const void* ref,
+                 const void* ldr0_w, const void* ref_w, const void* validity, const void* mask, void* ldr,
+                 double* losses, void* grad_radiance, void* g_ldr0_w, void* workspace, ssb_stream_t stream) {
+    Tmo p;
+    if (B <= 0 || H <= 0 || W <= 0 || !radiance || !ref || !grad_radiance || (!ldr0_w) != (!ref_w) ||
+        (validity && !ldr0_w) || (losses && !workspace) || (g_ldr0_w && !ldr0_w) || tmo_check(tmo, &p)) {
+        set_error("ssb_epilogue: invalid arguments");
+        return SSB_EINVAL;
+    }
+    if (dtype != SSB_F32 && dtype != SSB_F64) {
+        set_error("ssb_epilogue: dtype must be f32 or f64");
+        return SSB_EUNSUPPORTED;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long n = (long long)H * W;
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        const bool v4 = sizeof(T) == 4 && vec4_ok(n, B, radiance, ref, ldr0_w, ref_w, validity, mask, ldr,
+                                                   grad_radiance, g_ldr0_w);
+        auto kern = v4 ? k_epilogue<T, sizeof(T) == 4 ? 4 : 1> : k_epilogue<T, 1>;
+        SSB_LAUNCH(s, kern<<<dim3(kLossBlocks, B), 256, 0, s>>>(
+                          n, p, tmo_f(p), (const T*)radiance, (const T*)ref, (const T*)ldr0_w, (const T*)ref_w,
+                          (const T*)validity, (const T*)mask, (T*)ldr, losses ? (double*)workspace : nullptr,
+                          (T*)grad_radiance, (T*)g_ldr0_w));
+        if (losses)
+            SSB_LAUNCH(s, k_loss_reduce<<<B, 256, 0, s>>>(n, ldr0_w != nullptr, validity != nullptr,
+                                                          (const double*)workspace, losses));
+    };
+    if (dtype == SSB_F64) run(0.0);
+    else run(0.0f);
+    return cuda_check("ssb_epilogue");
 }
 
 }  // extern "C"

@@ -545,6 +545,59 @@ def tonemap_backward(radiance, tmo, upstream):
     return g
 
 
+def _loss_inputs(img, ref, ldr0_w, ref_w, validity, mask, name):
+    """Shared checks of `losses` / `loss_epilogue` (the reference's
+    ValueErrors, losses.py:58-91)."""
+    _need(img, name)
+    dt = _img_dtype(img, name)
+    dev = img.device
+    _need(ref, "ref", dev, img.dtype)
+    if img.dim() != 4 or img.shape[1] != 3 or ref.shape != img.shape:
+        raise ValueError("loss: image dimensions must match")
+    if (ldr0_w is None) != (ref_w is None):
+        raise ValueError("loss: the warped history needs both ldr0_w and ref_w")
+    B, _, H, W = img.shape
+    for t, nm in ((ldr0_w, "ldr0_w"), (ref_w, "ref_w")):
+        if t is not None:
+            _need(t, nm, dev, img.dtype)
+            if t.shape != img.shape:
+                raise ValueError("temporal loss: image dimensions must match")
+    for t, nm in ((validity, "validity"), (mask, "mask")):
+        if t is not None:
+            _need(t, nm, dev, img.dtype)
+            if tuple(t.shape) != (B, H, W):
+                raise ValueError(f"{nm} must be (B, H, W)")
+    if validity is not None and ldr0_w is None:
+        raise ValueError("validity needs the warped history")
+    return dt, dev, B, H, W
+
+
+def loss_epilogue(radiance, ref, tmo, ldr0_w=None, ref_w=None, validity=None, mask=None, want_ldr=False,
+                  want_losses=True):
+    """The evaluate_step epilogue in one kernel (optimize.py:219-231 over
+    tonemap.py / losses.py): tonemap(radiance), the spatial / temporal /
+    combined losses against `ref` (and the warped history), and the gradient
+    of the combined loss chained through the tonemap to the radiance.  Equals
+    tonemap -> losses(want_grads=True) -> tonemap_backward (float64:
+    bit-identical).  Returns a dict: 'grad_radiance', 'g_ldr0_w' (with a
+    history), 'losses' (B, 3) float64, 'ldr' (want_ldr)."""
+    lib = _lib.load()
+    dt, dev, B, H, W = _loss_inputs(radiance, ref, ldr0_w, ref_w, validity, mask, "radiance")
+    grad = torch.empty_like(radiance)
+    g0 = torch.empty_like(radiance) if ldr0_w is not None else None
+    ldr = torch.empty_like(radiance) if want_ldr else None
+    vals = torch.empty((B, 3), dtype=torch.float64, device=dev) if want_losses else None
+    wb = C.c_size_t()
+    check(lib.ssb_losses_workspace_bytes(B, C.byref(wb)), "ssb_losses_workspace_bytes")
+    ws = torch.empty(wb.value, dtype=torch.uint8, device=dev)
+    t = _tmo(tmo)
+    with torch.cuda.device(dev):
+        check(lib.ssb_epilogue(dt, B, H, W, t, _ptr(radiance), _ptr(ref), _ptr(ldr0_w), _ptr(ref_w),
+                               _ptr(validity), _ptr(mask), _ptr(ldr), _ptr(vals), _ptr(grad), _ptr(g0), _ptr(ws),
+                               _stream(dev)), "ssb_epilogue")
+    return {"grad_radiance": grad, "g_ldr0_w": g0, "losses": vals, "ldr": ldr}
+
+
 def losses(ldr1, ref, ldr0_w=None, ref_w=None, validity=None, mask=None, want_maps=True,
            want_grads=False):
     """Masked spatial, temporal and max-combined losses (losses.py:58-91) and,
@@ -554,27 +607,7 @@ def losses(ldr1, ref, ldr0_w=None, ref_w=None, validity=None, mask=None, want_ma
     (B, 3) float64 = (spatial, temporal, combined), the maps, 'g_ldr1',
     'g_ldr0_w'."""
     lib = _lib.load()
-    _need(ldr1, "ldr1")
-    dt = _img_dtype(ldr1, "ldr1")
-    dev = ldr1.device
-    _need(ref, "ref", dev, ldr1.dtype)
-    if ldr1.dim() != 4 or ldr1.shape[1] != 3 or ref.shape != ldr1.shape:
-        raise ValueError("loss: image dimensions must match")
-    if (ldr0_w is None) != (ref_w is None):
-        raise ValueError("loss: the warped history needs both ldr0_w and ref_w")
-    B, _, H, W = ldr1.shape
-    for t, nm in ((ldr0_w, "ldr0_w"), (ref_w, "ref_w")):
-        if t is not None:
-            _need(t, nm, dev, ldr1.dtype)
-            if t.shape != ldr1.shape:
-                raise ValueError("temporal loss: image dimensions must match")
-    for t, nm in ((validity, "validity"), (mask, "mask")):
-        if t is not None:
-            _need(t, nm, dev, ldr1.dtype)
-            if tuple(t.shape) != (B, H, W):
-                raise ValueError(f"{nm} must be (B, H, W)")
-    if validity is not None and ldr0_w is None:
-        raise ValueError("validity needs the warped history")
+    dt, dev, B, H, W = _loss_inputs(ldr1, ref, ldr0_w, ref_w, validity, mask, "ldr1")
     maps = [torch.empty((B, H, W), dtype=ldr1.dtype, device=dev) for _ in range(3)] if want_maps else [None] * 3
     vals = torch.empty((B, 3), dtype=torch.float64, device=dev)
     g1 = torch.empty_like(ldr1) if want_grads else None

@@ -114,6 +114,41 @@ def test_tonemap_and_full_losses_f32_vs_oracle(ops, h, w):
         assert agree0.mean() > 0.999
 
 
+@pytest.mark.parametrize("dtype,h,w,hist", [(torch.float64, 37, 53, True), (torch.float64, 16, 24, False),
+                                             (torch.float32, 64, 96, True), (torch.float32, 33, 51, True),
+                                             (torch.float32, 48, 64, False)])
+def test_fused_epilogue_matches_composition(ops, dtype, h, w, hist):
+    """ssb_epilogue == tonemap -> losses(want_grads) -> tonemap_backward:
+    bit-identical in float64, within float32 rounding (and the same
+    temporal/spatial branch on all but near-tie pixels) in float32."""
+    gen = torch.Generator(device="cuda").manual_seed(h * w)
+    B = 2
+    rnd = lambda *s: torch.rand(s, device="cuda", dtype=dtype, generator=gen)  # noqa: E731
+    rad = torch.exp(torch.randn((B, 3, h, w), device="cuda", dtype=dtype, generator=gen) * 2.0 - 0.5)
+    ref = rnd(B, 3, h, w)
+    l0w, rw = (rnd(B, 3, h, w), rnd(B, 3, h, w)) if hist else (None, None)
+    val = (rnd(B, h, w) > 0.2).to(dtype) if hist else None
+    msk = rnd(B, h, w)
+    t = (0.2, 1.3, 0.8, 0.35, 0.45)
+    f = ops.loss_epilogue(rad, ref, t, l0w, rw, validity=val, mask=msk, want_ldr=True)
+    ldr = ops.tonemap(rad, t)
+    r = ops.losses(ldr, ref, l0w, rw, validity=val, mask=msk, want_maps=False, want_grads=True)
+    g = ops.tonemap_backward(rad, t, r["g_ldr1"])
+    if dtype == torch.float64:
+        assert torch.equal(f["ldr"], ldr)
+        assert torch.equal(f["grad_radiance"], g)
+        assert torch.equal(f["losses"], r["losses"])
+        if hist:
+            assert torch.equal(f["g_ldr0_w"], r["g_ldr0_w"])
+    else:
+        torch.testing.assert_close(f["ldr"], ldr, rtol=1e-5, atol=1e-6)
+        torch.testing.assert_close(f["losses"], r["losses"], rtol=1e-5, atol=1e-9)
+        close = torch.isclose(f["grad_radiance"], g, rtol=1e-4, atol=1e-5 * g.abs().max().item())
+        assert close.float().mean().item() > 0.999
+        if hist:
+            assert torch.isclose(f["g_ldr0_w"], r["g_ldr0_w"]).float().mean().item() > 0.999
+
+
 def test_losses_reject_bad_inputs(ops):
     x = torch.zeros((1, 3, 8, 8), device="cuda", dtype=torch.float64)
     with pytest.raises(ValueError):
