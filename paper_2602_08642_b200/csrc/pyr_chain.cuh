@@ -30,9 +30,11 @@ struct UpTransposeArgs {
 };
 
 // two horizontally adjacent values of a plane (x even, W even: 8-B / 4-B aligned)
-__device__ __forceinline__ float2 ld_pair_lg(const float* p) { return __ldcs(reinterpret_cast<const float2*>(p)); }
+// (default caching: the neighbouring coarse pixels' threads re-read edge
+// rows / columns -- an evict-first load would send those back to DRAM)
+__device__ __forceinline__ float2 ld_pair_lg(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
 __device__ __forceinline__ float2 ld_pair_lg(const __nv_bfloat16* p) {
-    const unsigned w = __ldcs(reinterpret_cast<const unsigned*>(p));
+    const unsigned w = __ldg(reinterpret_cast<const unsigned*>(p));
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(256) k_up_transpose(const UpTransposeArgs a) {
         if (y >= a.H) break;
         const bool i1 = r == 0 || lastY;
         const unsigned p = (unsigned)y * (unsigned)a.W + (unsigned)x0;
-        const float2 l2 = __ldcs(reinterpret_cast<const float2*>(lse + p));
+        const float2 l2 = __ldg(reinterpret_cast<const float2*>(lse + p));
         float2 z[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) z[t] = ld_pair_lg(lg + (size_t)(TIED ? NT : NT + t) * hw + p);
@@ -78,8 +80,8 @@ __global__ void __launch_bounds__(256) k_up_transpose(const UpTransposeArgs a) {
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float2 u = __ldcs(reinterpret_cast<const float2*>(up + c * hw + p));
-            const float2 d = __ldcs(reinterpret_cast<const float2*>(dm + c * hw + p));
+            const float2 u = __ldg(reinterpret_cast<const float2*>(up + c * hw + p));
+            const float2 d = __ldg(reinterpret_cast<const float2*>(dm + c * hw + p));
             acc[c] = fmaf(ws0, u.x * demod_clamp(d.x), acc[c]);
             acc[c] = fmaf(ws1, u.y * demod_clamp(d.y), acc[c]);
         }
