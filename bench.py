@@ -561,6 +561,7 @@ def gpu_arm(args, rank, world, local_rank, dist):
         "step_roofline": {"achieved": round(step_gbs, 1), "peak": peak, "unit": "GB/s",
                           "frac": round(step_gbs / peak, 4),
                           "bytes_per_frame": {"fwd": fwd_b, "bwd": 0 if fwd_only else bwd_b}},
+        "step_dram": None if fwd_only else step_dram(args.workload, value / max(world, 1), peak),
         "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -648,6 +649,21 @@ def main():
         dist.destroy_process_group()
 
 
+def step_dram(workload, mpix_s, peak):
+    """Achieved DRAM bandwidth of the whole step: the DRAM bytes per pixel
+    that ncu measured for every kernel of one step of this workload
+    (tools/gpu_step_traffic.sh -> profiles/step_traffic.json; cold,
+    serialized launches) times the live pixel rate.  Supplementary to the
+    algorithmic-bytes step_roofline (which counts only the minimum bytes)."""
+    try:
+        ent = json.load(open(os.path.join(ROOT, "profiles", "step_traffic.json")))[workload]
+    except (OSError, ValueError, KeyError):
+        return None
+    gbs = ent["dram_bytes_per_px"] * mpix_s / 1e3
+    return {"dram_bytes_per_px": ent["dram_bytes_per_px"], "achieved": round(gbs, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(gbs / peak, 4), "source": ent.get("source", "")}
+
+
 def also_measurements():
     """The other BASELINE configs on the same box: c3 (4K, L4, k7, bf16
     logits), c4b (8K fwd), and the 8(f) rows (temporal warp, score gradient)."""
@@ -667,6 +683,7 @@ def also_measurements():
                  "ms_per_step": round(ms, 4),
                  "step_frac_of_hbm": round((fwd_b + bwd_b) / (ms * 1e-3) / 1e9 / peak, 4),
                  "bwd_l0_frac_of_hbm": round(dom_b / (kern["bwd_l0"] * 1e-3) / 1e9 / peak, 4),
+                 "step_dram": step_dram("c3", H * W / (ms * 1e-3) / 1e6, peak),
                  "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
     del noisy, demod, logits, up, r
     torch.cuda.empty_cache()
