@@ -429,9 +429,11 @@ def time_e2e(dev, frames, steps, k, H, W, L, ldt, chunk=4, pool_frames=16):
     h_glg = [host((pool_frames, logit_channels(l, L, k), h, w), lt) for l, (h, w) in enumerate(lvl)]
     for t in list(h_in.values()) + h_lg:
         t.uniform_(0.05, 1.0)
-    # two device chunk buffers (double buffering)
+    # NBUF device chunk buffers: the H2D of chunk i + NBUF waits only for the
+    # D2H of chunk i (3 measured no better than 2)
+    NBUF = 2
     bufs = []
-    for _ in range(2):
+    for _ in range(NBUF):
         d_n = torch.empty(chunk, 3, H, W, device=dev)
         d_d = torch.empty_like(d_n)
         d_u = torch.empty_like(d_n)
@@ -444,27 +446,27 @@ def time_e2e(dev, frames, steps, k, H, W, L, ldt, chunk=4, pool_frames=16):
     out_bytes = sum(t[0:1].numel() * t.element_size() for t in list(h_out.values()) + h_glg) * frames
 
     def one_step():
-        ev_h2d = [torch.cuda.Event() for _ in range(2)]
-        ev_comp = [torch.cuda.Event() for _ in range(2)]
-        ev_d2h = [None, None]
+        ev_h2d = [torch.cuda.Event() for _ in range(NBUF)]
+        ev_comp = [torch.cuda.Event() for _ in range(NBUF)]
+        ev_d2h = [None] * NBUF
         for ci, f0 in enumerate(range(0, frames, chunk)):
-            r = bufs[ci % 2]
+            r = bufs[ci % NBUF]
             p0 = f0 % pool_frames
             sl = slice(p0, p0 + chunk)
             with torch.cuda.stream(s_h2d):
-                if ev_d2h[ci % 2] is not None:
-                    s_h2d.wait_event(ev_d2h[ci % 2])
+                if ev_d2h[ci % NBUF] is not None:
+                    s_h2d.wait_event(ev_d2h[ci % NBUF])
                 r.noisy.copy_(h_in["noisy"][sl], non_blocking=True)
                 r.demod.copy_(h_in["demod"][sl], non_blocking=True)
                 r.up.copy_(h_in["up"][sl], non_blocking=True)
                 for z, hz in zip(r.logits, h_lg):
                     z.copy_(hz[sl], non_blocking=True)
-                ev_h2d[ci % 2].record(s_h2d)
-            s_comp.wait_event(ev_h2d[ci % 2])
+                ev_h2d[ci % NBUF].record(s_h2d)
+            s_comp.wait_event(ev_h2d[ci % NBUF])
             r.step(s_comp.cuda_stream)
-            ev_comp[ci % 2].record(s_comp)
+            ev_comp[ci % NBUF].record(s_comp)
             with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev_comp[ci % 2])
+                s_d2h.wait_event(ev_comp[ci % NBUF])
                 h_out["out"][sl].copy_(r.out, non_blocking=True)
                 h_out["g_noisy"][sl].copy_(r.g_noisy, non_blocking=True)
                 h_out["g_demod"][sl].copy_(r.g_demod, non_blocking=True)
@@ -472,7 +474,7 @@ def time_e2e(dev, frames, steps, k, H, W, L, ldt, chunk=4, pool_frames=16):
                     hz[sl].copy_(gz, non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(s_d2h)
-                ev_d2h[ci % 2] = e
+                ev_d2h[ci % NBUF] = e
         torch.cuda.synchronize()
 
     one_step()
@@ -481,6 +483,42 @@ def time_e2e(dev, frames, steps, k, H, W, L, ldt, chunk=4, pool_frames=16):
         one_step()
     dt = (time.perf_counter() - t0) / steps
     return dt, in_bytes, out_bytes
+
+
+def pcie_gbs(dev, nbytes=1 << 30):
+    """Pinned host <-> device copy bandwidth of this box: one 1 GiB copy each
+    way, then both at once on two streams (aggregate), after a warm-up -- the
+    ceiling of the e2e number."""
+    import torch
+    h, h2 = (torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2))
+    d, d2 = (torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2))
+    out = []
+    for src, dst in ((h, d), (d, h)):  # best of 3 (one-off hiccups)
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out.append(best)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    bidir = 0.0
+    for _ in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        bidir = max(bidir, 2 * nbytes / (time.perf_counter() - t0) / 1e9)
+    out.append(bidir)
+    del h, h2, d, d2
+    return out
 
 
 def gpu_arm(args, rank, world, local_rank, dist):
@@ -630,9 +668,17 @@ def main():
             tt = torch.tensor([dt], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = tt.item()
+        h2d, d2h, bidir = pcie_gbs(torch.device("cuda", local_rank))
+        # copies overlap each other and the compute: the PCIe ceiling is the
+        # step's bytes at the measured aggregate (both directions at once) rate
+        ceil = B * H * W / max((ib + ob) / (bidir * 1e9), ib / (h2d * 1e9), ob / (d2h * 1e9)) / 1e6
         res["e2e"] = {"value": round(B * world * H * W / dt / 1e6, 3), "unit": "Mpix/s",
                       "h2d_bytes_per_step": ib * world, "d2h_bytes_per_step": ob * world,
-                      "path": "ops C-ABI from pinned host buffers, chunked H2D/compute/D2H overlap"}
+                      "path": "ops C-ABI from pinned host buffers, chunked H2D/compute/D2H overlap",
+                      "pcie_gbs_measured": {"h2d": round(h2d, 1), "d2h": round(d2h, 1),
+                                            "both_directions": round(bidir, 1)},
+                      "pcie_ceiling_mpix_s": round(ceil * world, 3),
+                      "frac_of_pcie_ceiling": round(B * H * W / dt / 1e6 / ceil, 4)}
     else:
         res["e2e"] = None
 
