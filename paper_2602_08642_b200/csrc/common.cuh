@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/ssb_api.h"
 
 namespace ssb {
@@ -108,6 +110,20 @@ __device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); 
 
 template <typename T>
 __device__ __forceinline__ T demod_clamp(T d) { return d > (T)kDemodFloor ? d : (T)kDemodFloor; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and
+// device (the attribute lives in the current device's context): `mask` is
+// the call site's static, one bit per device; a race only repeats the
+// idempotent call
+inline void smem_attr_once(std::atomic<unsigned long long>& mask, const void* kern, int bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(mask.load(std::memory_order_relaxed) & bit)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        mask.fetch_or(bit);
+    }
+}
 
 // launch accounting (pyr_api.cu): every kernel launch is wrapped in
 // SSB_LAUNCH(stream, kernel<<<...>>>(...)) so the bench can count launches and

@@ -67,11 +67,8 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
     if (!ok) return false;
     auto kern = k_pyr_fwd_tma<K, TL, L0, UP, TIED>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_mask{0};
+    smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     FwdLevel a = a0;
     const int strips = (a.W + SH::TXF - 1) / SH::TXF;
     a.seg_h = pick_segment(strips, a.H, a.batch);
@@ -142,11 +139,8 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
     TmaMaps mp;
     if (!prepare_bwd_tma<K, TL, L0, UP, TIED, CH>(a0, mp)) return false;
     auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED, CH>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_mask{0};
+    smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     BwdLevel a = a0;
     const int strips = (a.W + SH::TXB - 1) / SH::TXB;
     a.seg_h = pick_segment(strips, a.H, a.batch);
@@ -162,11 +156,8 @@ void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
     }
     using SH = BwdShape<K, UP, PREV, T>;
     auto kern = k_pyr_bwd<K, TL, T, L0, UP, TIED, PREV>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_mask{0};
+    smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     BwdLevel a = a0;
     const int strips = (a.W + SH::TXB - 1) / SH::TXB;
     a.seg_h = pick_segment(strips, a.H, B);
@@ -393,11 +384,8 @@ int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bw
     }
     using SH = TmaShape<K, TL, true, true, TIED, true>;
     auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SH::SMEM);
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_mask{0};
+    smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     const int strips = (a0.W + SH::TXB - 1) / SH::TXB;
     a0.seg_h = pick_segment(strips, a0.H, a0.batch);
     dim3 grid(strips, (a0.H + a0.seg_h - 1) / a0.seg_h, a0.batch);

@@ -421,12 +421,8 @@ bool launch_blur_r(int r, dim3 grid, int H, int W, const BlurWeights& bw, const 
         return false;
     } else {
         if (r != R) return launch_blur_r<T, R + 1>(r, grid, H, W, bw, g0, sc, fmx, g1, pse, psd, s);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_blur_sums_r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)blur_r_smem<T, R>());
-            attr = true;
-        }
+        static std::atomic<unsigned long long> attr_mask{0};
+        smem_attr_once(attr_mask, (const void*)k_blur_sums_r<T, R>, (int)blur_r_smem<T, R>());
         SSB_LAUNCH(s, k_blur_sums_r<T, R><<<grid, 256, blur_r_smem<T, R>(), s>>>(H, W, bw, g0, sc, fmx, g1, pse, psd));
         return true;
     }

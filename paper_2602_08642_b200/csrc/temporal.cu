@@ -624,12 +624,8 @@ int ssb_warp_backward(int dtype, int B, int C, int H, int W, const void* grad_ou
         SSB_LAUNCH(s, k_motion_absmax_f32<<<dim3((unsigned)(b4 < 296 ? b4 : 296), B), 256, 0, s>>>(
                           2 * n, (const float*)motion, amax));
         dim3 mgrid((W + WM_X - 1) / WM_X, (H + WM_Y - 1) / WM_Y, B);
-        static bool attr = false;  // (idempotent; races only repeat the call)
-        if (!attr) {
-            cudaFuncSetAttribute(k_warp_backward_mask, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(MaskSmem));
-            attr = true;
-        }
+        static std::atomic<unsigned long long> attr_mask{0};
+        smem_attr_once(attr_mask, (const void*)k_warp_backward_mask, (int)sizeof(MaskSmem));
         SSB_LAUNCH(s, k_warp_backward_mask<<<mgrid, 256, sizeof(MaskSmem), s>>>(C, H, W, (const float*)grad_out,
                                                                  (const float*)motion, amax, (float*)grad_prev));
     }
