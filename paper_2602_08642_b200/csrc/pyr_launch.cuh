@@ -88,10 +88,20 @@ void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
 }
 
 inline int pick_segment(int strips, int H, int B) {
-    // keep >= ~8 CTAs per SM of work, amortise the halo rows
-    int seg = 128;
-    while (seg > 16 && (long long)strips * ((H + seg - 1) / seg) * B < 148 * 8) seg >>= 1;
-    return seg;
+    // balanced row segments of <= SSB_SEG_ROWS (default 128) rows, a multiple
+    // of 4, keeping >= ~8 CTAs per SM of work.  Measured (tools/seg_sweep.sh,
+    // c4a): 48 -> 7719, 96 -> 7798, 128 -> 7886, 192 -> 7630, 256 -> 7250
+    // Mpix/s -- longer walks amortise the prologue but spread the co-resident
+    // CTAs over more rows of every logit plane
+    static const int target = [] {
+        const char* e = getenv("SSB_SEG_ROWS");
+        const int v = e ? atoi(e) : 128;
+        return v >= 16 ? v : 128;
+    }();
+    int nseg = (H + target - 1) / target;
+    while ((long long)strips * nseg * B < 148 * 8 && (H + nseg - 1) / nseg > 16) nseg *= 2;
+    const int seg = (H + nseg - 1) / nseg;
+    return (seg + 3) & ~3;
 }
 
 // TMA-pipelined level backward (fp32 images, fp32/bf16 logits, no temporal

@@ -1,7 +1,7 @@
 """Per-source-line instruction / stall attribution for one kernel of an ncu
 report (needs -lineinfo builds and --import-source on).
 
-    python tools/ncu_lines.py REPORT KERNEL_REGEX [TOP] [PIXELS]
+    python tools/ncu_lines.py REPORT KERNEL_REGEX [TOP] [PIXELS] [--by-stall]
 """
 import collections
 import csv
@@ -51,7 +51,8 @@ def main():
     tot = sum(v[0] for v in per.values()) or 1
     tots = sum(v[1] for v in per.values()) or 1
     print(f"total warp-instructions {tot}" + (f"  ({tot * 32 / pixels:.0f} thread-instr/px)" if pixels else ""))
-    for k, v in sorted(per.items(), key=lambda kv: -kv[1][0])[:top]:
+    key = (lambda kv: -kv[1][1]) if "--by-stall" in sys.argv else (lambda kv: -kv[1][0])
+    for k, v in sorted(per.items(), key=key)[:top]:
         extra = f" {v[0] * 32 / pixels:6.1f}/px" if pixels else ""
         print(f"{k[0][:16]:16s}:{k[1]:<5d} {100 * v[0] / tot:5.1f}%{extra} st {100 * v[1] / tots:5.1f}%  {v[2].strip()[:80]}")
 
