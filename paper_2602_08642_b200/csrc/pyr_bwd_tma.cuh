@@ -610,6 +610,7 @@ __global__ void __launch_bounds__(256, 2)
             }
 
         } else {
+            // -------------------------------------------- B2: gather-transpose (warps 4-7)
             // taps of tap column dx for every source row of the step: window row
             // k = s + d (compile-time), smem column rj = ri - dx (runtime)
             auto gather_dx = [&](int rj, int dx) {

@@ -32,5 +32,6 @@ for _ in range(2):
     ldr = ops.tonemap(rad, tmo)
     r = ops.losses(ldr, ref, l0w, rw, validity=val, mask=msk, want_maps=False, want_grads=True)
     ops.tonemap_backward(rad, tmo, r["g_ldr1"])
+    ops.loss_epilogue(rad, ref, tmo, l0w, rw, validity=val, mask=msk)
 torch.cuda.synchronize()
 print("ok")
