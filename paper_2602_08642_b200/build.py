@@ -27,6 +27,8 @@ LIB = os.path.join(LIBDIR, "libssb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
+# experiments only (e.g. SSB_NVCC_FLAGS=-DSSB_ROLE_TIMING; delete lib/obj first)
+COMMON += os.environ.get("SSB_NVCC_FLAGS", "").split()
 # per-file extra flags: placement decisions must round exactly like numpy
 EXTRA = {"place.cu": ["-fmad=false"], "temporal.cu": ["-fmad=false"], "scores.cu": ["-fmad=false"], "tonemap.cu": ["-fmad=false"]}
 

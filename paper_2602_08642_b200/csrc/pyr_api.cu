@@ -369,4 +369,11 @@ int ssb_pyr_backward(const ssb_pyr_desc* d, const ssb_pyr_bwd_io* io, const void
     return by_types(d, c);
 }
 
+
+#ifdef SSB_ROLE_TIMING
+// experiment build only (not in ssb_api.h): this TU's copy of the backward
+// kernel's per-role cycle counters (tools/role_timing.py sums every TU)
+int ssb_debug_role_cycles0(unsigned long long* out8) { return ssb::role_cycles_read(out8); }
+#endif
+
 }  // extern "C"

@@ -189,6 +189,24 @@ __device__ __forceinline__ float rcp_fast(float x) {  // MUFU.RCP (x >= 1e-3 her
 }
 __device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0, 256;" ::: "memory"); }
 
+#ifdef SSB_ROLE_TIMING
+// experiment build only: per role (warps 0-3 / 4-7) cycles spent waiting for
+// the step's TMA, in phase A (incl. its barrier), in the role's B work, and at
+// the end-of-step barrier (tools/role_timing.py)
+// (internal linkage: one copy per translation unit -- read through the
+// per-k entry points in pyr_k{3,5,7}.cu)
+static __device__ unsigned long long g_role_cycles[8];
+static inline int role_cycles_read(unsigned long long* out8) {
+    if (cudaMemcpyFromSymbol(out8, g_role_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess) return -2;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_role_cycles, z, sizeof(z));
+    return 0;
+}
+#define SSB_RT(...) __VA_ARGS__
+#else
+#define SSB_RT(...)
+#endif
+
 template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
 __global__ void __launch_bounds__(256, 2)
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
@@ -330,6 +348,7 @@ __global__ void __launch_bounds__(256, 2)
     const int ri_a = RA - R + rw_a;                     // smem column of this thread's region pixel
     const bool act_a = tid < S * RW;
 
+    SSB_RT(long long rt_tw = 0; unsigned long long rt_acc[4] = {0, 0, 0, 0};)
     // ------------------------------------------------ A: softmax, G, inner'
     // (every thread; ends with the CTA barrier, the next prefetch and the
     // clamp patch of the image rows that arrived with this step)
@@ -343,6 +362,7 @@ __global__ void __launch_bounds__(256, 2)
             }
         }
         mbar_wait(&bars[i & 1], (i >> 1) & 1);
+        SSB_RT(rt_tw = clock64();)
         if (act_a) {
             float e[NLOG];
 #pragma unroll
@@ -433,8 +453,10 @@ __global__ void __launch_bounds__(256, 2)
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = qstart + i * S;
         float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
+        SSB_RT(const long long rt_t0 = clock64();)
         phase_a(i, qs, lgb,
                 reinterpret_cast<const TL*>(SEP ? s_lg + LGF + (SH::EARLY ? (i & 1) * LGS1 : 0) : lgb));
+        SSB_RT(const long long rt_t1 = clock64(); rt_acc[0] += rt_tw - rt_t0; rt_acc[1] += rt_t1 - rt_tw;)
         if (tid < 128) {
             // -------------------------------------------- B1: logit gradients
             const int qy = qs + s, gx = x0 + xi;
@@ -797,7 +819,9 @@ __global__ void __launch_bounds__(256, 2)
                 for (int c = 0; c < 3; ++c)
                     win[p][c] = p + S / 2 < NPW ? win[p + S / 2][c] : make_float2(0.f, 0.f);
         }
+        SSB_RT(const long long rt_t2 = clock64();)
         cta_sync();  // end of step
+        SSB_RT(const long long rt_t3 = clock64(); rt_acc[2] += rt_t2 - rt_t1; rt_acc[3] += rt_t3 - rt_t2;)
         if (B3ON && tid < 128) {
             // coarse ghat rows finished by this step (all B3 items are in)
             const bool bottom = qs + S >= H;
@@ -822,6 +846,10 @@ __global__ void __launch_bounds__(256, 2)
             cnext = cend;
         }
     }
+#ifdef SSB_ROLE_TIMING
+    if ((tid & 31) == 0)
+        for (int k = 0; k < 4; ++k) atomicAdd(&g_role_cycles[(tid < 128 ? 0 : 4) + k], rt_acc[k]);
+#endif
 }
 
 }  // namespace ssb
