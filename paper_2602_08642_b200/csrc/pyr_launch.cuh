@@ -92,14 +92,20 @@ inline int pick_segment(int strips, int H, int B) {
     // of 4, keeping >= ~8 CTAs per SM of work.  Measured (tools/seg_sweep.sh,
     // c4a): 48 -> 7719, 96 -> 7798, 128 -> 7886, 192 -> 7630, 256 -> 7250
     // Mpix/s -- longer walks amortise the prologue but spread the co-resident
-    // CTAs over more rows of every logit plane
+    // CTAs over more rows of every logit plane.  SSB_MIN_CTAS (default 8 per
+    // SM): c3 296 -> 4282, 592 -> 4371, 1184 -> 4413, 2368 -> 4342 Mpix/s
     static const int target = [] {
         const char* e = getenv("SSB_SEG_ROWS");
         const int v = e ? atoi(e) : 128;
         return v >= 16 ? v : 128;
     }();
+    static const long long min_ctas = [] {
+        const char* e = getenv("SSB_MIN_CTAS");
+        const long long v = e ? atoll(e) : 148 * 8;
+        return v >= 1 ? v : 148 * 8;
+    }();
     int nseg = (H + target - 1) / target;
-    while ((long long)strips * nseg * B < 148 * 8 && (H + nseg - 1) / nseg > 16) nseg *= 2;
+    while ((long long)strips * nseg * B < min_ctas && (H + nseg - 1) / nseg > 16) nseg *= 2;
     const int seg = (H + nseg - 1) / nseg;
     return (seg + 3) & ~3;
 }
