@@ -284,65 +284,113 @@ __global__ void __launch_bounds__(SG_TX * SG_TY) k_blur_sums(int H, int W, BlurW
 __device__ __forceinline__ double madd(double x, double y, double acc) { return acc + x * y; }
 __device__ __forceinline__ float madd(float x, float y, float acc) { return __fmaf_rn(x, y, acc); }
 
-// compile-time radius R: 64 x 16 tile per CTA (four outputs per thread),
-// unrolled taps, constant-divisor window indexing -- the sums of k_blur_sums
-// in the same order
+// compile-time radius R, float32: 64 x 16 tile per CTA, register-blocked --
+// the vertical pass gives each thread 4 consecutive rows of one column (4 + 2R
+// shared loads for 4 outputs), the horizontal pass 4 consecutive columns of
+// one row (16-B shared loads); every output keeps scipy's sum order
+// (x_i w0 + sum_{j = R..1} (x_{i-j} + x_{i+j}) w_j)
 constexpr int SB_TX = 64, SB_TY = 16;
+
+template <int R>
+struct BlurTile {
+    static constexpr int NX = SB_TX + 2 * R, NY = SB_TY + 2 * R, NWIN = NX * NY;
+    static constexpr int NXP = (NX + 3) & ~3;      // 16-B row pitch of the vertical-pass output
+    static constexpr int VOFF = (NWIN + 3) & ~3;   // s_v offset (16-B aligned)
+    static constexpr int NB = 4 + 2 * R, NV4 = (NB + 3) / 4;
+    static constexpr size_t BYTES = (size_t)(VOFF + SB_TY * NXP) * sizeof(float);
+};
 
 template <typename T, int R>
 __global__ void __launch_bounds__(256) k_blur_sums_r(int H, int W, BlurWeights bw, const acc_t<T>* __restrict__ g0,
                                                      const T* __restrict__ scores, const double* __restrict__ pmax,
                                                      acc_t<T>* __restrict__ g1, double* __restrict__ pse,
                                                      double* __restrict__ psd) {
-    using A = acc_t<T>;
-    constexpr int NX = SB_TX + 2 * R, NY = SB_TY + 2 * R, NWIN = NX * NY;
+    static_assert(sizeof(T) == 4, "float32 path");
+    using TT = BlurTile<R>;
+    constexpr int NX = TT::NX, NWIN = TT::NWIN, NXP = TT::NXP, NB = TT::NB;
     extern __shared__ __align__(16) unsigned char smem_blur[];
-    A* s_in = reinterpret_cast<A*>(smem_blur);  // [NY][NX]
-    A* s_v = s_in + NWIN;                        // [SB_TY][NX]
+    float* s_in = reinterpret_cast<float*>(smem_blur);  // [NY][NX]
+    float* s_v = s_in + TT::VOFF;                        // [SB_TY][NXP]
     const int b = blockIdx.z, tid = threadIdx.x;
     const int x0 = blockIdx.x * SB_TX, y0 = blockIdx.y * SB_TY;
-    const A* gb = g0 + (size_t)b * H * W;
-    A w[R + 1];
+    const float* gb = g0 + (size_t)b * H * W;
+    float w[R + 1];
 #pragma unroll
-    for (int j = 0; j <= R; ++j) w[j] = (A)bw.w[j];
+    for (int j = 0; j <= R; ++j) w[j] = (float)bw.w[j];
     const double m = pmax[b];
     constexpr int NIT = (NWIN + 255) / 256;
-    A v[NIT];
+    float v[NIT];
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {  // every load issued before the stores
         const int i = tid + it * 256;
         const int wy = i / NX, wx = i - wy * NX;
         const int yy = clampi(y0 - R + wy, 0, H - 1), xx = clampi(x0 - R + wx, 0, W - 1);
-        v[it] = i < NWIN ? gb[(size_t)yy * W + xx] : (A)0;
+        v[it] = i < NWIN ? gb[(size_t)yy * W + xx] : 0.f;
     }
 #pragma unroll
     for (int it = 0; it < NIT; ++it)
         if (tid + it * 256 < NWIN) s_in[tid + it * 256] = v[it];
     __syncthreads();
-    for (int i = tid; i < SB_TY * NX; i += 256) {  // axis 0
-        const int ty = i / NX, tx = i - ty * NX;
-        const A* c = s_in + (ty + R) * NX + tx;
-        A a = c[0] * w[0];
+    for (int i = tid; i < (SB_TY / 4) * NX; i += 256) {  // axis 0: rows 4 q4 .. 4 q4 + 3 of column tx
+        const int q4 = i / NX, tx = i - q4 * NX;
+        const float* c = s_in + 4 * q4 * NX + tx;  // window row 0 = output row 4 q4 - R
+        float col[NB];
 #pragma unroll
-        for (int j = R; j >= 1; --j) a = madd(c[-j * NX] + c[j * NX], w[j], a);
-        s_v[i] = a;
+        for (int k = 0; k < NB; ++k) col[k] = c[k * NX];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float a = col[q + R] * w[0];
+#pragma unroll
+            for (int j = R; j >= 1; --j) a = madd(col[q + R - j] + col[q + R + j], w[j], a);
+            s_v[(4 * q4 + q) * NXP + tx] = a;
+        }
     }
     __syncthreads();
+    // axis 1: row ty, columns 4 lq .. 4 lq + 3
+    const int ty = tid >> 4, lq = tid & 15, y = y0 + ty, xq = x0 + 4 * lq;
     double se = 0.0, sd = 0.0;
-    const int lx = tid & 63, ly = tid >> 6;
+    if (y < H && xq < W) {
+        float row[4 * TT::NV4];
+        const float4* r4 = reinterpret_cast<const float4*>(s_v + ty * NXP + 4 * lq);
 #pragma unroll
-    for (int h = 0; h < SB_TY / 4; ++h) {  // axis 1
-        const int ty = ly + 4 * h, x = x0 + lx, y = y0 + ty;
-        if (x >= W || y >= H) continue;
-        const A* c = s_v + ty * NX + lx + R;
-        A a = c[0] * w[0];
+        for (int k = 0; k < TT::NV4; ++k) {
+            const float4 t = r4[k];
+            row[4 * k] = t.x;
+            row[4 * k + 1] = t.y;
+            row[4 * k + 2] = t.z;
+            row[4 * k + 3] = t.w;
+        }
+        float out[4];
 #pragma unroll
-        for (int j = R; j >= 1; --j) a = madd(c[-j] + c[j], w[j], a);
-        const size_t o = (size_t)b * H * W + (size_t)y * W + x;
-        g1[o] = a;
-        const double e = sg_exp(scores[o], m);
-        se += e;
-        sd += e * (double)a;
+        for (int q = 0; q < 4; ++q) {
+            float a = row[q + R] * w[0];
+#pragma unroll
+            for (int j = R; j >= 1; --j) a = madd(row[q + R - j] + row[q + R + j], w[j], a);
+            out[q] = a;
+        }
+        const size_t o = (size_t)b * H * W + (size_t)y * W + xq;
+        float sc[4];
+        const bool vec = (W & 3) == 0 && xq + 3 < W && (reinterpret_cast<size_t>(scores) & 15) == 0 &&
+                         (reinterpret_cast<size_t>(g1) & 15) == 0;
+        if (vec) {
+            const float4 s4 = __ldg(reinterpret_cast<const float4*>(scores + o));
+            sc[0] = s4.x;
+            sc[1] = s4.y;
+            sc[2] = s4.z;
+            sc[3] = s4.w;
+            *reinterpret_cast<float4*>(g1 + o) = make_float4(out[0], out[1], out[2], out[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (xq + q >= W) break;
+            if (!vec) {
+                sc[q] = scores[o + q];
+                g1[o + q] = out[q];
+            }
+            const double e = sg_exp(sc[q], m);
+            se += e;
+            sd += e * (double)out[q];
+        }
     }
     se = sg_block_reduce(se, false);
     sd = sg_block_reduce(sd, false);
@@ -355,7 +403,7 @@ __global__ void __launch_bounds__(256) k_blur_sums_r(int H, int W, BlurWeights b
 
 template <typename T, int R>
 size_t blur_r_smem() {
-    return (size_t)((SB_TX + 2 * R) * (SB_TY + 2 * R) + SB_TY * (SB_TX + 2 * R)) * sizeof(acc_t<T>);
+    return BlurTile<R>::BYTES;
 }
 
 // per-frame totals of the tile partials (fixed order: deterministic)
