@@ -44,16 +44,23 @@ struct FwdTmaShape {
     static constexpr size_t SMEM = FLOATS * 4 + 32;
     static constexpr int MINB_SMEM = (int)((227 * 1024) / (SMEM + 1024));
     static constexpr int MINB = MINB_SMEM > 4 ? 4 : (MINB_SMEM < 1 ? 1 : MINB_SMEM);
+    // PAIR (bf16 logits, k = 7: instruction bound): 128 threads, each two
+    // horizontally adjacent pixels -- 32-bit logit loads carry both pixels,
+    // FFMA2 / FADD2 over the pair, one 8-B shared load per two window values
+    static constexpr bool PAIR = LGE == 2 && K == 7;
+    static constexpr int NTH = PAIR ? 128 : 256;
 };
 
 template <int K, typename TL, bool L0, bool UP, bool TIED>
-__global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
+__global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
     k_pyr_fwd_tma(const FwdLevel a, const __grid_constant__ FwdTmaMaps mp) {
     using SH = FwdTmaShape<K, TL, L0, UP, TIED>;
     constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S;
     constexpr int TXF = SH::TXF, RA = SH::RA, RX = SH::RX, NPRO = SH::NPRO, NBL = SH::NBL;
     constexpr int NI = SH::NI, CB = SH::CB, CROWS = SH::CROWS, LGF = SH::LGF, BLKF = SH::BLKF;
     constexpr int DEMOFF = SH::DEMOFF, PL = S * RX, LPL = S * TXF;
+    constexpr bool PAIR = SH::PAIR;
+    constexpr int NTH = SH::NTH;
 
     extern __shared__ __align__(128) unsigned char smem_ftma[];
     const TL* s_lg = reinterpret_cast<const TL*>(smem_ftma);  // [NLOG][S][TXF]
@@ -68,7 +75,8 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
     const int cxs = (x0 >> 1) & ~3;
     const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
     const int nsteps = (y1 - y0 + S - 1) / S;
-    const int s_t = tid >> 6, xi = tid & 63;  // own pixel of this thread in a step
+    // own pixel (PAIR: pixels xi, xi + 1) of this thread in a step
+    const int s_t = PAIR ? tid >> 5 : tid >> 6, xi = PAIR ? 2 * (tid & 31) : tid & 63;
 
     auto lin_block = [&](int j) { return s_lin + ((j + 64 * NBL) % NBL) * BLKF; };
     int sl_i = 0;  // slot of the current step's image block
@@ -92,7 +100,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
     // clamp-to-edge patch of image rows [r0, r1) of the ring (after conversion)
     auto patch_rows = [&](int qs, int r0, int r1) {
         if (col_border) {
-            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
+            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += NTH) {
                 const int ri = i % RX, rest = i / RX;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
                 const int src = clampi(xs0 + ri, 0, W - 1) - xs0;
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
             __syncthreads();
         }
         if (r0 < 0 || r1 > H) {
-            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
+            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += NTH) {
                 const int ri = i % RX, rest = i / RX;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
                 const int src = clampi(r, 0, H - 1);
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
     };
     auto convert_rows = [&](float* blk) {  // x0 = noisy / max(d, floor), in place
         if constexpr (L0) {
-            for (int i = tid; i < S * RX; i += 256) {
+            for (int i = tid; i < S * RX; i += NTH) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
                     blk[c * PL + i] *= frcp(demod_clamp(blk[DEMOFF + c * PL + i]));
@@ -149,6 +157,131 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = y0 + i * S;
         mbar_wait(&bars[0], i & 1);
+        if constexpr (PAIR) {
+            // softmax of the thread's two pixels (one 32-bit load per channel)
+            float2 e2[NW];
+            float2 mk2;
+            {
+                float2 z2[NLOG];
+#pragma unroll
+                for (int t = 0; t < NLOG; ++t) {
+                    const unsigned wv = *reinterpret_cast<const unsigned*>(s_lg + t * LPL + s_t * TXF + xi);
+                    z2[t] = make_float2(__uint_as_float(wv << 16), __uint_as_float(wv & 0xffff0000u));
+                }
+                float m0 = z2[0].x, m1 = z2[0].y;
+#pragma unroll
+                for (int t = 1; t < NLOG; ++t) {
+                    m0 = fmaxf(m0, z2[t].x);
+                    m1 = fmaxf(m1, z2[t].y);
+                }
+                mk2 = make_float2(m0 * kLog2e, m1 * kLog2e);
+                const float2 nm = make_float2(-mk2.x, -mk2.y);
+                auto ex = [&](float2 z) {
+                    const float2 q = ffma2(z, bcast2(kLog2e), nm);
+                    return make_float2(ex2_ftz(q.x), ex2_ftz(q.y));
+                };
+#pragma unroll
+                for (int t = 0; t < NT; ++t) e2[t] = ex(z2[t]);
+                if constexpr (UP) {
+                    if constexpr (TIED) {
+                        const float2 eb = ex(z2[NT]);
+#pragma unroll
+                        for (int t = NT; t < NW; ++t) e2[t] = eb;
+                    } else {
+#pragma unroll
+                        for (int t = NT; t < NW; ++t) e2[t] = ex(z2[t]);
+                    }
+                }
+            }
+            convert_rows(lin_block(i));
+            __syncthreads();  // logits consumed, new image rows converted
+            if (tid == 0 && i + 1 < nsteps) {
+                fence_proxy_async();
+                issue_step(i + 1);
+            }
+            if (col_border || qs + R + S > H) patch_rows(qs, qs + R, qs + R + S);
+
+            const int qy = qs + s_t, gx = x0 + xi;
+            if (qy < y1 && gx < W) {
+                float2 sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < NW; ++t) sum2 = fadd2(sum2, e2[t]);
+                const float inv0 = frcp(sum2.x), inv1 = frcp(sum2.y);
+                const bool two = gx + 1 < W;
+                if constexpr (L0) {  // base-2 log-sum-exp for the backward's upsample-transpose pre-pass
+                    if (a.lse) {
+                        float* lp = (float*)a.lse + (size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx;
+                        lp[0] = mk2.x + __log2f(sum2.x);
+                        if (two) lp[1] = mk2.y + __log2f(sum2.y);
+                    }
+                }
+                float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                // window of the pair: smem columns xi + RA - R .. xi + RA + R + 1,
+                // read as 8-B pairs from the even column below (PAR = 1 here)
+                constexpr int PAR = (RA - R) & 1, NV = (2 * R + 2 + PAR + 1) / 2;
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) {
+                    const float* lb = lin_row_step(qs, qy + dy, 0) + xi + RA - R - PAR;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        float v[2 * NV];
+#pragma unroll
+                        for (int k2 = 0; k2 < NV; ++k2) {
+                            const float2 t2 = *reinterpret_cast<const float2*>(lb + c * PL + 2 * k2);
+                            v[2 * k2] = t2.x;
+                            v[2 * k2 + 1] = t2.y;
+                        }
+#pragma unroll
+                        for (int dx = -R; dx <= R; ++dx) {
+                            const int j = dx + R + PAR;  // pixel 0's window value; pixel 1 takes j + 1
+                            const float2 wv = e2[(dy + R) * K + dx + R];
+                            if ((j & 1) == 0) {
+                                acc[c] = ffma2(wv, make_float2(v[j], v[j + 1]), acc[c]);
+                            } else {
+                                acc[c].x = fmaf(wv.x, v[j], acc[c].x);
+                                acc[c].y = fmaf(wv.y, v[j + 1], acc[c].y);
+                            }
+                        }
+                    }
+                }
+                if constexpr (UP) {
+                    const float* lh = s_lhc + (i & 1) * SH::LHF;
+                    const int cyb = qs >> 1;
+#pragma unroll
+                    for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj) {
+                            const int cy = min((qy + ii) >> 1, a.Hc - 1) - cyb;
+                            const int cx0 = min((gx + jj) >> 1, a.Wc - 1) - cxs;
+                            const int cx1 = min((gx + 1 + jj) >> 1, a.Wc - 1) - cxs;
+                            const float2 wv = e2[NT + 2 * ii + jj];
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                acc[c].x = fmaf(wv.x, lh[(c * CROWS + cy) * CB + cx0], acc[c].x);
+                                acc[c].y = fmaf(wv.y, lh[(c * CROWS + cy) * CB + cx1], acc[c].y);
+                            }
+                        }
+                }
+                const unsigned po = (unsigned)qy * (unsigned)W + (unsigned)gx;
+                const float* dr = L0 ? lin_row_step(qs, qy, 1) + xi + RA : nullptr;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (c >= nc) break;
+                    float v0 = acc[c].x * inv0, v1 = acc[c].y * inv1;
+                    if constexpr (L0) {
+                        v0 *= demod_clamp(dr[c * PL]);
+                        v1 *= demod_clamp(dr[c * PL + 1]);
+                    }
+                    float* op = ofb + po + c * hw32;
+                    if (two && ((po & 1) == 0)) {
+                        *reinterpret_cast<float2*>(op) = make_float2(v0, v1);
+                    } else {
+                        op[0] = v0;
+                        if (two) op[1] = v1;
+                    }
+                }
+            }
+        } else {
         // softmax of this thread's own pixel, from smem into registers
         float e[NW];
         float mk;
@@ -224,6 +357,7 @@ __global__ void __launch_bounds__(256, (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
                 if constexpr (L0) v *= demod_clamp(dr[c * PL]);
                 ofb[po + c * hw32] = v;
             }
+        }
         }
     }
 }

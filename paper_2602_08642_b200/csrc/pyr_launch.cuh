@@ -73,7 +73,7 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
     const int strips = (a.W + SH::TXF - 1) / SH::TXF;
     a.seg_h = pick_segment(strips, a.H, a.batch);
     dim3 grid(strips, (a.H + a.seg_h - 1) / a.seg_h, a.batch);
-    SSB_LAUNCH(s, kern<<<grid, 256, SH::SMEM, s>>>(a, mp));
+    SSB_LAUNCH(s, kern<<<grid, SH::NTH, SH::SMEM, s>>>(a, mp));
     return true;
 }
 

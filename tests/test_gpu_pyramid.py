@@ -160,11 +160,12 @@ def test_oracle_cases(ops, h, w, L, k, prev, blend, precision):
         assert_close(planar_to_hwc(g.prev), ref["g_prev"], rtol, "g_prev")
 
 
-@pytest.mark.parametrize("k,L", [(5, 3), (7, 4)])
-def test_bf16_logits(ops, k, L):
+@pytest.mark.parametrize("k,L,h,w", [(5, 3, 90, 132), (7, 4, 90, 132), (7, 4, 72, 128), (5, 3, 64, 96)])
+def test_bf16_logits(ops, k, L, h, w):
     """bf16 logits, fp32 radiance and accumulation: within 2e-2 of the oracle
-    fed the bf16-rounded logits."""
-    h, w = 90, 132
+    fed the bf16-rounded logits.  W % 8 == 0 at every level (72 x 128, 64 x
+    96) runs the TMA level kernels (bf16 rows must be 16-B multiples; k = 7:
+    the pixel-pair forward), the other sizes the generic kernels."""
     rng = np.random.default_rng(7)
     lg32 = [torch.from_numpy(z.astype(np.float32)) for z in
             op.random_logits(h, w, L, k, rng, temporal=False)]
