@@ -80,6 +80,25 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 bcast2(float s) { return make_float2(s, s); }
 
+// max / sum of a per-pixel register array as 4 independent chains (dependency
+// depth N/4 + 2 instead of N: the softmax's serial tails)
+template <int N>
+__device__ __forceinline__ float max4(const float (&e)[N]) {
+    float m[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = e[j < N ? j : N - 1];
+#pragma unroll
+    for (int t = 4; t < N; ++t) m[t & 3] = fmaxf(m[t & 3], e[t]);
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+template <int N>
+__device__ __forceinline__ float sum4(const float (&e)[N]) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < N; ++t) s[t & 3] += e[t];
+    return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
 // ---- exponentials ---------------------------------------------------------
 // fp32: MUFU.EX2 with flush-to-zero (arguments are <= 0 after the max
 // subtraction; weights below 2^-126 are irrelevant), the max subtraction folded

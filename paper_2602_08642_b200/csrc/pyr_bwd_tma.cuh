@@ -367,20 +367,19 @@ __global__ void __launch_bounds__(256, 2)
             float e[NLOG];
 #pragma unroll
             for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PL + s_a * RX + ri_a]);
-            float m = e[0];
-#pragma unroll
-            for (int t = 1; t < NLOG; ++t) m = fmaxf(m, e[t]);
+            const float m = max4(e);
             const float2 mk2 = bcast2(-m * kLog2e);
-            float2 sum2 = make_float2(0.f, 0.f);
+            float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 chains
 #pragma unroll
             for (int t = 0; t + 1 < NLOG; t += 2) {
                 const float2 z2 = ffma2(make_float2(e[t], e[t + 1]), bcast2(kLog2e), mk2);
                 e[t] = ex2_ftz(z2.x);
                 e[t + 1] = ex2_ftz(z2.y);
-                sum2 = fadd2(sum2, make_float2((TIED && t == NT) ? 4.f * e[t] : e[t],
-                                               (TIED && t + 1 == NT) ? 4.f * e[t + 1] : e[t + 1]));
+                sum2[(t >> 1) & 1] = fadd2(sum2[(t >> 1) & 1],
+                                           make_float2((TIED && t == NT) ? 4.f * e[t] : e[t],
+                                                       (TIED && t + 1 == NT) ? 4.f * e[t + 1] : e[t + 1]));
             }
-            float sum = sum2.x + sum2.y;
+            float sum = (sum2[0].x + sum2[1].x) + (sum2[0].y + sum2[1].y);
             if constexpr (NLOG & 1) {
                 e[NLOG - 1] = ex2_ftz(fmaf(e[NLOG - 1], kLog2e, mk2.x));
                 sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];

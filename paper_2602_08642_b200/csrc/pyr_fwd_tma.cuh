@@ -168,12 +168,13 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
                     const unsigned wv = *reinterpret_cast<const unsigned*>(s_lg + t * LPL + s_t * TXF + xi);
                     z2[t] = make_float2(__uint_as_float(wv << 16), __uint_as_float(wv & 0xffff0000u));
                 }
-                float m0 = z2[0].x, m1 = z2[0].y;
+                float ma[2][2] = {{z2[0].x, z2[0].y}, {z2[NLOG - 1].x, z2[NLOG - 1].y}};  // 2 chains per pixel
 #pragma unroll
-                for (int t = 1; t < NLOG; ++t) {
-                    m0 = fmaxf(m0, z2[t].x);
-                    m1 = fmaxf(m1, z2[t].y);
+                for (int t = 1; t < NLOG - 1; ++t) {
+                    ma[t & 1][0] = fmaxf(ma[t & 1][0], z2[t].x);
+                    ma[t & 1][1] = fmaxf(ma[t & 1][1], z2[t].y);
                 }
+                const float m0 = fmaxf(ma[0][0], ma[1][0]), m1 = fmaxf(ma[0][1], ma[1][1]);
                 mk2 = make_float2(m0 * kLog2e, m1 * kLog2e);
                 const float2 nm = make_float2(-mk2.x, -mk2.y);
                 auto ex = [&](float2 z) {
@@ -203,9 +204,10 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
 
             const int qy = qs + s_t, gx = x0 + xi;
             if (qy < y1 && gx < W) {
-                float2 sum2 = make_float2(0.f, 0.f);
+                float2 sa[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-                for (int t = 0; t < NW; ++t) sum2 = fadd2(sum2, e2[t]);
+                for (int t = 0; t < NW; ++t) sa[t & 1] = fadd2(sa[t & 1], e2[t]);
+                const float2 sum2 = fadd2(sa[0], sa[1]);
                 const float inv0 = frcp(sum2.x), inv1 = frcp(sum2.y);
                 const bool two = gx + 1 < W;
                 if constexpr (L0) {  // base-2 log-sum-exp for the backward's upsample-transpose pre-pass
@@ -289,10 +291,7 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
             float z[NLOG];
 #pragma unroll
             for (int t = 0; t < NLOG; ++t) z[t] = to_f32(s_lg[t * LPL + s_t * TXF + xi]);
-            float m = z[0];
-#pragma unroll
-            for (int t = 1; t < NLOG; ++t) m = fmaxf(m, z[t]);
-            mk = m * kLog2e;
+            mk = max4(z) * kLog2e;
 #pragma unroll
             for (int t = 0; t < NT; ++t) e[t] = ex2_ftz(fmaf(z[t], kLog2e, -mk));
             if constexpr (UP) {
@@ -316,9 +315,7 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
 
         const int qy = qs + s_t, gx = x0 + xi;
         if (qy < y1 && gx < W) {
-            float sum = 0.f;
-#pragma unroll
-            for (int t = 0; t < NW; ++t) sum += e[t];
+            const float sum = sum4(e);
             const float inv = frcp(sum);
             if constexpr (L0) {  // base-2 log-sum-exp for the backward's upsample-transpose pre-pass
                 if (a.lse) ((float*)a.lse)[(size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx] = mk + __log2f(sum);
