@@ -380,3 +380,35 @@ def test_level0_last_order_matches_general_order(H, W, L, k, ldt, monkeypatch):
         a, b = a.double(), b.double()
         tol = 2e-2 if ldt == "bf16" else 1e-5
         assert torch.allclose(a, b, rtol=tol, atol=tol * b.abs().max().item()), (a - b).abs().max().item()
+
+
+@pytest.mark.parametrize("k,ldt,blend,C", [(7, torch.bfloat16, "native", 3), (7, torch.bfloat16, "tied", 6),
+                                           (5, torch.float32, "tied", 6), (3, torch.float32, "native", 3)])
+def test_tma_and_generic_forward_backward_agree(ops, monkeypatch, k, ldt, blend, C):
+    """The TMA level kernels (incl. the bf16 k = 7 pixel-pair forward and the
+    level-0-last backward) against the generic kernels (SSB_NO_TMA=1) on the
+    same inputs: forward outputs and every gradient to fp32 rounding; tied
+    blend and C = 6 (two channel groups) included."""
+    g = torch.Generator(device="cuda").manual_seed(k * 10 + C)
+    H, W, L = 72, 128, 4
+    noisy = torch.rand((2, C, H, W), device="cuda", generator=g) * 2
+    dm = torch.rand((2, C, H, W), device="cuda", generator=g) * 0.9 + 0.05
+    lg = [torch.randn((2, ops.logit_channels(l, L, k, blend=blend), h, w), device="cuda", generator=g).to(ldt)
+          for l, (h, w) in enumerate(ops.level_shapes(H, W, L))]
+    up = torch.randn((2, C, H, W), device="cuda", generator=g)
+    res = []
+    for mode in ("tma", "generic"):
+        if mode == "generic":
+            monkeypatch.setenv("SSB_NO_TMA", "1")
+        out, t = ops.pyramid_forward(noisy, lg, dm, ksize=k, blend=blend)
+        res.append((out, ops.pyramid_backward(t, up)))
+        monkeypatch.delenv("SSB_NO_TMA", raising=False)
+    (o1, g1), (o2, g2) = res
+    assert (o1 - o2).abs().max().item() <= 2e-5 * o2.abs().max().item()
+    tol = 2e-2 if ldt == torch.bfloat16 else 2e-5  # bf16 logit gradients round differently
+    for a_, b_ in [(g1.input, g2.input), (g1.demod, g2.demod)]:
+        assert (a_ - b_).abs().max().item() <= 2e-5 * b_.abs().max().item()
+    for a_, b_ in zip(g1.logits, g2.logits):
+        a_, b_ = a_.float(), b_.float()
+        assert (a_ - b_).abs().max().item() <= tol * b_.abs().max().item()
+
