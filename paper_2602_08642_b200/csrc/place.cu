@@ -232,30 +232,17 @@ __global__ void k_partial_max(long long n, const TS* scores, double* pmax) {
     if (threadIdx.x == 0) pmax[b * kRedBlocks + blockIdx.x] = m;
 }
 
-__device__ __forceinline__ double frame_max(const double* pmax, int b, int nblk = kRedBlocks) {
-    double m = -INFINITY;
-    for (int k = 0; k < nblk; ++k) m = fmax(m, pmax[b * kRedBlocks + k]);
-    return m;
-}
-
-__device__ __forceinline__ double frame_sum(const double* psum, int b, int nblk = kRedBlocks) {
-    double s = 0.0;
-    for (int k = 0; k < nblk; ++k) s += psum[b * kRedBlocks + k];
-    return s;
-}
-
-// the frame's max / sum of the partials, once per frame (same serial order as
-// frame_max / frame_sum): out[2b] = max, out[2b+1] = sum (when psum given)
+// the frame's max / sum of the block partials, once per frame: out[2b] = max,
+// out[2b+1] = sum (when psum given).  Each thread folds a strided subset in
+// order, then a fixed shuffle tree (deterministic; launched with kRedThreads)
 __global__ void k_frame_stats(const double* pmax, const double* psum, double* out, int nblk) {
-    __shared__ double sh[kRedBlocks];
     const int b = blockIdx.x;
-    const double* src = psum ? psum : pmax;
-    for (int k = threadIdx.x; k < nblk; k += blockDim.x) sh[k] = src[b * kRedBlocks + k];
-    __syncthreads();
-    if (threadIdx.x == 0) {  // the serial order of frame_max / frame_sum, from shared memory
-        if (psum) out[2 * b + 1] = frame_sum(sh, 0, nblk);
-        else out[2 * b] = frame_max(sh, 0, nblk);
-    }
+    const bool is_max = psum == nullptr;
+    const double* src = (is_max ? pmax : psum) + (size_t)b * kRedBlocks;
+    double v = is_max ? -INFINITY : 0.0;
+    for (int k = threadIdx.x; k < nblk; k += blockDim.x) v = is_max ? fmax(v, src[k]) : v + src[k];
+    v = block_reduce(v, is_max);
+    if (threadIdx.x == 0) out[2 * b + (is_max ? 0 : 1)] = v;
 }
 
 template <typename TS>
@@ -264,6 +251,7 @@ __global__ void k_partial_sum(long long n, const TS* scores, const double* fstat
     const double m = fstat[2 * b];
     const TS* p = scores + (long long)b * n;
     double s = 0.0;
+#pragma unroll 4
     for (long long i = (long long)blockIdx.x * kRedThreads + threadIdx.x; i < n;
          i += (long long)gridDim.x * kRedThreads)
         s += exp((double)p[i] - m);
@@ -327,9 +315,9 @@ static void launch_reductions(int B, long long n, const TS* scores, double* pmax
     nb = nb < 1 ? 1 : (nb > kRedBlocks ? kRedBlocks : nb);
     dim3 grid((unsigned)nb, B), sgrid(B, (unsigned)nb);  // (k_frame_stats reads nb from gridDim.y)
     SSB_LAUNCH(s, k_partial_max<TS><<<grid, kRedThreads, 0, s>>>(n, scores, pmax));
-    SSB_LAUNCH(s, k_frame_stats<<<dim3(B, 1), 256, 0, s>>>(pmax, nullptr, fstat, (int)nb));
+    SSB_LAUNCH(s, k_frame_stats<<<dim3(B, 1), kRedThreads, 0, s>>>(pmax, nullptr, fstat, (int)nb));
     SSB_LAUNCH(s, k_partial_sum<TS><<<grid, kRedThreads, 0, s>>>(n, scores, fstat, psum));
-    SSB_LAUNCH(s, k_frame_stats<<<dim3(B, 1), 256, 0, s>>>(pmax, psum, fstat, (int)nb));
+    SSB_LAUNCH(s, k_frame_stats<<<dim3(B, 1), kRedThreads, 0, s>>>(pmax, psum, fstat, (int)nb));
     (void)sgrid;
 }
 
