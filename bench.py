@@ -1,7 +1,7 @@
 """Benchmark of the B200 hot path: gather-pyramid filter fwd+bwd (BASELINE metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c4a|c3|c2|c1] [--no-e2e] [--no-cpu] [--no-also]
+                    [--workload c4a|c3|c2|c4b] [--no-e2e] [--no-cpu] [--no-also]
 
 Default workload (BASELINE.json configs[4a], the metric's 1080p multi-GPU
 config): 64 frames of 1920x1080, 3-level 5x5 pyramid, fp32, forward + backward
@@ -54,7 +54,11 @@ WORKLOADS = {
             "row bands with a one-round NVLink halo exchange (bands.py)"),
 }
 FWD_ONLY = {"c4b"}
-CPU_SAMPLE = (540, 960, 3, 5)  # per-worker sample of the c4a workload (H, W, L, k)
+# per-worker samples of each workload for the reference arm (H, W, L, k, with
+# backward): a 960x540 crop at the workload's pyramid depth and kernel size
+# (c2: one of its 256^2 frames; c4b: forward only, like the workload)
+CPU_SAMPLES = {"c4a": (540, 960, 3, 5, True), "c3": (540, 960, 4, 7, True), "c2": (256, 256, 4, 5, True),
+               "c4b": (540, 960, 4, 7, False)}
 
 
 # ---------------------------------------------------------------------------
@@ -91,12 +95,12 @@ def algorithmic_bytes(h, w, L, k, sl, sg, channels=3):
 # CPU legs: the reference algorithm (oracle port, float64) on host cores
 
 
-def _cpu_worker(seed):
+def _cpu_worker(arg):
+    seed, (h, w, L, k, bwd) = arg
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     import numpy as np
 
     from oracle import pyramid as op
-    h, w, L, k = CPU_SAMPLE
     rng = np.random.default_rng(seed)
     logits = op.random_logits(h, w, L, k, rng, temporal=True)
     noisy = rng.lognormal(-1.0, 1.5, (h, w, 3)) * (rng.uniform(size=(h, w, 1)) < 0.25)
@@ -104,18 +108,22 @@ def _cpu_worker(seed):
     up = rng.normal(size=(h, w, 3))
     t0 = time.perf_counter()
     out, tape = op.forward(noisy, logits, None, demod, k=k)
-    op.backward(tape, up)
+    if bwd:
+        op.backward(tape, up)
     return time.perf_counter() - t0
 
 
-def cpu_pool_size():
+def cpu_pool_size(sample=None):
+    h, w, L, k, _ = sample or CPU_SAMPLES["c4a"]
     cores = len(os.sched_getaffinity(0))
     try:
         import psutil
         ram = psutil.virtual_memory().available
     except Exception:
         ram = 8 << 30
-    per_proc = 2.2 * (1 << 30)  # measured ~1.7 GB RSS for one 960x540 L3 fwd+bwd
+    # measured ~1.7 GB RSS for one 960x540 L3 k5 fwd+bwd; scales with pixels
+    # and logit channels
+    per_proc = 2.2 * (1 << 30) * (h * w) / (540 * 960) * (2 * k * k + 4) / 54
     return max(1, min(cores, int(ram // per_proc)))
 
 
@@ -131,9 +139,9 @@ class CpuPool:
         else:
             os.environ["OMP_NUM_THREADS"] = env_threads
 
-    def step(self, seed):
+    def step(self, seed, sample):
         t0 = time.perf_counter()
-        self.pool.map(_cpu_worker, [seed * 1000 + i for i in range(self.procs)])
+        self.pool.map(_cpu_worker, [(seed * 1000 + i, sample) for i in range(self.procs)])
         return time.perf_counter() - t0
 
     def close(self):
@@ -151,22 +159,23 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_sample_desc(procs):
-    h, w, L, k = CPU_SAMPLE
-    return (f"{procs} worker processes x one {w}x{h} L{L} k{k} fwd+bwd (float64 numpy oracle "
-            f"port of the reference, OMP_NUM_THREADS=1 each) per step; CPU {cpu_model()}")
+def cpu_sample_desc(procs, workload="c4a"):
+    h, w, L, k, bwd = CPU_SAMPLES[workload]
+    return (f"{procs} worker processes x one {w}x{h} L{L} k{k} {'fwd+bwd' if bwd else 'fwd'} (float64 "
+            f"numpy oracle port of the reference, OMP_NUM_THREADS=1 each) per step; CPU {cpu_model()}")
 
 
-def run_cpu(steps, warmup):
-    procs = cpu_pool_size()
+def run_cpu(steps, warmup, workload="c4a"):
+    sample = CPU_SAMPLES[workload]
+    procs = cpu_pool_size(sample)
     pool = CpuPool(procs)
     try:
         for i in range(warmup):
-            pool.step(100 + i)
-        times = [pool.step(i) for i in range(steps)]
+            pool.step(100 + i, sample)
+        times = [pool.step(i, sample) for i in range(steps)]
     finally:
         pool.close()
-    h, w, _, _ = CPU_SAMPLE
+    h, w = sample[0], sample[1]
     t = sum(times) / len(times)
     return {"value": procs * h * w / t / 1e6, "procs": procs, "sec_per_step": t}
 
@@ -631,17 +640,19 @@ def main():
         # the reference CPU path is float64 numpy; bounded samples per step
         steps = args.steps
         warm = min(args.warmup, 1)
-        r = run_cpu(steps, warm)
-        h, w, _, _ = CPU_SAMPLE
-        res = {"impl": "reference", "metric": f"pyramidal filter fwd+bwd throughput ({args.workload})",
+        r = run_cpu(steps, warm, args.workload)
+        fwd_only = args.workload in FWD_ONLY
+        res = {"impl": "reference",
+               "metric": f"pyramidal filter {'fwd' if fwd_only else 'fwd+bwd'} throughput ({args.workload})",
                "value": round(r["value"], 4), "unit": "Mpix/s", "n_gpus": world, "steps": steps,
                "warmup": warm, "ms_per_step": round(r["sec_per_step"] * 1e3, 1),
-               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "higher_is_better": True, "scaling": "strong" if frames_total > 1 else "weak",
+               "vs_baseline": None,
                "dtype": "f64", "data": "synthetic, BASELINE config distributions (seeded)",
-               "config": {"workload": desc, "sample": cpu_sample_desc(r["procs"])},
+               "config": {"workload": desc, "sample": cpu_sample_desc(r["procs"], args.workload)},
                "cpu_baseline": {"value": round(r["value"], 4), "unit": "Mpix/s",
                                 "cores": r["procs"], "kind": "port",
-                                "sample": cpu_sample_desc(r["procs"])},
+                                "sample": cpu_sample_desc(r["procs"], args.workload)},
                "e2e": {"value": round(r["value"], 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
         print(json.dumps(res), flush=True)
@@ -683,9 +694,9 @@ def main():
         res["e2e"] = None
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = run_cpu(1, 0)
+        r = run_cpu(1, 0, args.workload)
         res["cpu_baseline"] = {"value": round(r["value"], 4), "unit": "Mpix/s", "cores": r["procs"],
-                               "kind": "port", "sample": cpu_sample_desc(r["procs"])}
+                               "kind": "port", "sample": cpu_sample_desc(r["procs"], args.workload)}
     if rank == 0 and world == 1 and not args.no_also and args.workload == "c4a":
         res["also"] = also_measurements()
     if rank == 0:
