@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) k_warp_staged(int H, int W, const float* 
                                                      const float* __restrict__ motion, float* __restrict__ out,
                                                      float* __restrict__ validity) {
     constexpr int NWIN = WF_WY * WF_WX;
-    __shared__ float s_p[3][NWIN];
+    __shared__ float4 s_p[NWIN];  // channel-interleaved: one 16-B load per tap
     const int b = blockIdx.z, tid = threadIdx.x;
     const int tx0 = blockIdx.x * WF_X, ty0 = blockIdx.y * WF_Y;
     const int wx0 = tx0 - 4, wy0 = ty0 - 4;
@@ -130,9 +130,7 @@ __global__ void __launch_bounds__(256) k_warp_staged(int H, int W, const float* 
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
         const int i = tid + it * 256;
-        if (i < NWIN)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) s_p[c][i] = pv[it][c];
+        if (i < NWIN) s_p[i] = make_float4(pv[it][0], pv[it][1], pv[it][2], 0.f);
     }
     __syncthreads();
     const int lx = tid & 31;
@@ -167,8 +165,10 @@ __global__ void __launch_bounds__(256) k_warp_staged(int H, int W, const float* 
             // comparisons fail -- and the clamped index is 0)
             w[k] = wxs[dx] * wys[dy];
             if (inwin) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) v[k][c] = s_p[c][(iys[dy] - wy0) * WF_WX + ixs[dx] - wx0];
+                const float4 t = s_p[(iys[dy] - wy0) * WF_WX + ixs[dx] - wx0];
+                v[k][0] = t.x;
+                v[k][1] = t.y;
+                v[k][2] = t.z;
             } else {
                 const unsigned src = (unsigned)iys[dy] * (unsigned)W + (unsigned)ixs[dx];
 #pragma unroll
