@@ -377,22 +377,28 @@ __device__ void warp_backward_scan(int C, int H, int W, int b, int x, int y, int
                                    const T* __restrict__ motion, T* __restrict__ gprev);
 
 struct MaskSmem {
-    static constexpr int NWIN = WM_WY * WM_WX;
-    float4 wg[4][NWIN];  // per source and tap: w_k * g_c (c < 3), w_k = wx * wy (images.py:101-117)
-    unsigned m[2][WM_MY * WM_MX];
-    int lut[64];         // bit -> window offset of the source from its cell
+    static constexpr int NWIN = WM_WY * WM_WX, NCELL = WM_MY * WM_MX;
+    float4 src[NWIN];      // per window source: fx, fy, g0, g1
+    float src2[NWIN];      //                    g2
+    float4 acc[4][NCELL];  // per landing cell and tap k: sum over its sources of w_k * g
+    unsigned m[2][NCELL];
+    int lut[64];           // bit -> window offset of the source from its cell
 };
 
+// Two gathers instead of one scatter: (1) every landing cell sums, per tap k,
+// w_k * g over the sources that land on it (its mask bits, ascending); (2)
+// every target adds the 4 cells p - k.  The cell walk is the only
+// data-dependent loop, once per cell instead of once per (target, tap).
 template <int NWD>
 __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, int W, int b, int tx0, int ty0,
                                                    const float* __restrict__ gout, const float* __restrict__ motion,
                                                    float* __restrict__ gprev) {
-    constexpr int NWIN = MaskSmem::NWIN, OB = NWD == 1 ? 2 : 3;  // |o| bound
+    constexpr int NWIN = MaskSmem::NWIN, NCELL = MaskSmem::NCELL, OB = NWD == 1 ? 2 : 3;  // |o| bound
     const int tid = threadIdx.x, lx = tid & 31, ly0 = tid >> 5;
     const int wx0 = tx0 - 4, wy0 = ty0 - 4;  // window origin; cell origin is tile - 1
     const unsigned hw = (unsigned)H * (unsigned)W;
     const float* mb = motion + (size_t)b * 2 * hw;
-    for (int i = tid; i < NWD * WM_MY * WM_MX; i += 256) (&sm.m[0][0])[i] = 0u;
+    for (int i = tid; i < NWD * NCELL; i += 256) (&sm.m[0][0])[i] = 0u;
     if (tid < 32 * NWD) {
         int oy, ox;
         if (NWD == 1) {
@@ -408,7 +414,7 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
     for (int c0 = 0; c0 < C; c0 += 3) {
         const int nc = min(3, C - c0);
         if (c0 > 0) __syncthreads();
-        // stage: landing masks (first group), tap weights times the gradient;
+        // (0) stage the window: landing masks (first group), fractions, gradient;
         // every load of the thread's window items is issued before any use
         constexpr int NIT = (NWIN + 255) / 256;
         const float* gp = gout + ((size_t)b * C + c0) * hw;  // 32-bit offsets below (C*H*W < 2^31)
@@ -433,7 +439,6 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
             const int wj = i / WM_WX, wi = i - wj * WM_WX;
             const float mx = mv[it][0], my = mv[it][1];
             const float fmx = floorf(mx), fmy = floorf(my);
-            const float fx = mx - fmx, fy = my - fmy;
             if (c0 == 0 && fmx >= (float)-OB && fmx <= (float)OB && fmy >= (float)-OB && fmy <= (float)OB) {
                 const int ox = (int)fmx, oy = (int)fmy;  // (false for NaN motion)
                 const int u = wi - 3 + ox, v = wj - 3 + oy;  // cell of t0 = q + o
@@ -442,12 +447,41 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
                     else atomicOr(&sm.m[oy > 0][v * WM_MX + u], 1u << (((oy + 3) & 3) * 8 + ox + 3));
                 }
             }
-            const float wk[4] = {(1.f - fx) * (1.f - fy), fx * (1.f - fy), (1.f - fx) * fy, fx * fy};
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                sm.wg[k][i] = make_float4(wk[k] * gv[it][0], wk[k] * gv[it][1], wk[k] * gv[it][2], 0.f);
+            sm.src[i] = make_float4(mx - fmx, my - fmy, gv[it][0], gv[it][1]);
+            sm.src2[i] = gv[it][2];
         }
         __syncthreads();
+        // (1) per landing cell and tap: sum of w_k * g over its sources, in bit order
+        for (int cell = tid; cell < NCELL; cell += 256) {
+            const int v = cell / WM_MX, u = cell - v * WM_MX;
+            const int wc = v * WM_WX + u;
+            float a[4][3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) a[k][c] = 0.f;
+#pragma unroll
+            for (int wd = 0; wd < NWD; ++wd) {
+                unsigned m = sm.m[wd][cell];
+                while (m) {
+                    const int bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int li = wc + sm.lut[wd * 32 + bit];  // source q = t0 - o
+                    const float4 t = sm.src[li];
+                    const float g[3] = {t.z, t.w, sm.src2[li]};
+                    // images.py:101-117: w = wx * wy per tap (dx, dy)
+                    const float wk[4] = {(1.f - t.x) * (1.f - t.y), t.x * (1.f - t.y), (1.f - t.x) * t.y, t.x * t.y};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) a[k][c] = a[k][c] + wk[k] * g[c];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sm.acc[k][cell] = make_float4(a[k][0], a[k][1], a[k][2], 0.f);
+        }
+        __syncthreads();
+        // (2) targets: the 4 cells p - k, tap-major
 #pragma unroll
         for (int h = 0; h < WM_Y / 8; ++h) {
             const int ly = ly0 + 8 * h, x = tx0 + lx, y = ty0 + ly;
@@ -455,20 +489,10 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
             float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const int cell = (ly + 1 - (k >> 1)) * WM_MX + lx + 1 - (k & 1);  // t0 = p - k
-                const float4* wgk = sm.wg[k] + (ly + 1 - (k >> 1)) * WM_WX + lx + 1 - (k & 1);
-#pragma unroll
-                for (int wd = 0; wd < NWD; ++wd) {
-                    unsigned m = sm.m[wd][cell];
-                    while (m) {
-                        const int bit = __ffs(m) - 1;
-                        m &= m - 1;
-                        const float4 t = wgk[sm.lut[wd * 32 + bit]];  // source q = t0 - o
-                        acc[0] = acc[0] + t.x;
-                        acc[1] = acc[1] + t.y;
-                        acc[2] = acc[2] + t.z;
-                    }
-                }
+                const float4 t = sm.acc[k][(ly + 1 - (k >> 1)) * WM_MX + lx + 1 - (k & 1)];
+                acc[0] = acc[0] + t.x;
+                acc[1] = acc[1] + t.y;
+                acc[2] = acc[2] + t.z;
             }
             float* op = gprev + ((size_t)b * C + c0) * hw + ((unsigned)y * (unsigned)W + x);
             for (int c = 0; c < nc; ++c) __stcs(op + c * hw, acc[c]);
