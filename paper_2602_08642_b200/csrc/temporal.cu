@@ -420,10 +420,24 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
         const float* gp = gout + ((size_t)b * C + c0) * hw;  // 32-bit offsets below (C*H*W < 2^31)
         float mv[NIT][2], gv[NIT][3];
         bool inw[NIT];
+        // window coordinates of item tid + 256 it, advanced incrementally
+        constexpr int DJ = 256 / WM_WX, DI = 256 - DJ * WM_WX;
+        int wjs[NIT], wis[NIT];
+        wjs[0] = tid / WM_WX;
+        wis[0] = tid - wjs[0] * WM_WX;
+#pragma unroll
+        for (int it = 1; it < NIT; ++it) {
+            wjs[it] = wjs[it - 1] + DJ;
+            wis[it] = wis[it - 1] + DI;
+            if (wis[it] >= WM_WX) {
+                wis[it] -= WM_WX;
+                ++wjs[it];
+            }
+        }
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
             const int i = tid + it * 256;
-            const int wj = i / WM_WX, wi = i - wj * WM_WX;
+            const int wj = wjs[it], wi = wis[it];
             const int qx = wx0 + wi, qy = wy0 + wj;
             inw[it] = i < NWIN && qx >= 0 && qx < W && qy >= 0 && qy < H;  // others never land
             const unsigned q = inw[it] ? (unsigned)qy * (unsigned)W + (unsigned)qx : 0u;
@@ -436,7 +450,7 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
         for (int it = 0; it < NIT; ++it) {
             if (!inw[it]) continue;
             const int i = tid + it * 256;
-            const int wj = i / WM_WX, wi = i - wj * WM_WX;
+            const int wj = wjs[it], wi = wis[it];
             const float mx = mv[it][0], my = mv[it][1];
             const float fmx = floorf(mx), fmy = floorf(my);
             if (c0 == 0 && fmx >= (float)-OB && fmx <= (float)OB && fmy >= (float)-OB && fmy <= (float)OB) {
@@ -474,7 +488,7 @@ __device__ __forceinline__ void warp_bwd_mask_body(MaskSmem& sm, int C, int H, i
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) a[k][c] = a[k][c] + wk[k] * g[c];
+                        for (int c = 0; c < 3; ++c) a[k][c] = __fmaf_rn(wk[k], g[c], a[k][c]);  // (float32 path)
                 }
             }
 #pragma unroll
