@@ -846,7 +846,10 @@ __global__ void __launch_bounds__(256, 2)
         }
     }
 #ifdef SSB_ROLE_TIMING
-    if ((tid & 31) == 0)
+#ifndef SSB_ROLE_TIMING_L0
+#define SSB_ROLE_TIMING_L0 -1  // -1: every level; 1: level 0 only; 0: levels >= 1 only
+#endif
+    if ((tid & 31) == 0 && (SSB_ROLE_TIMING_L0 < 0 || (SSB_ROLE_TIMING_L0 == 1) == L0))
         for (int k = 0; k < 4; ++k) atomicAdd(&g_role_cycles[(tid < 128 ? 0 : 4) + k], rt_acc[k]);
 #endif
 }
