@@ -694,7 +694,7 @@ def main():
         res["e2e"] = None
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = run_cpu(1, 0, args.workload)
+        r = run_cpu(1, 1, args.workload)  # (one warm-up step: worker imports out of the timing)
         res["cpu_baseline"] = {"value": round(r["value"], 4), "unit": "Mpix/s", "cores": r["procs"],
                                "kind": "port", "sample": cpu_sample_desc(r["procs"], args.workload)}
     if rank == 0 and world == 1 and not args.no_also and args.workload == "c4a":
