@@ -383,7 +383,8 @@ def test_level0_last_order_matches_general_order(H, W, L, k, ldt, monkeypatch):
 
 
 @pytest.mark.parametrize("k,ldt,blend,C", [(7, torch.bfloat16, "native", 3), (7, torch.bfloat16, "tied", 6),
-                                           (5, torch.float32, "tied", 6), (3, torch.float32, "native", 3)])
+                                           (7, torch.bfloat16, "native", 4), (5, torch.float32, "tied", 6),
+                                           (5, torch.float32, "native", 4), (3, torch.float32, "native", 3)])
 def test_tma_and_generic_forward_backward_agree(ops, monkeypatch, k, ldt, blend, C):
     """The TMA level kernels (incl. the bf16 k = 7 pixel-pair forward and the
     level-0-last backward) against the generic kernels (SSB_NO_TMA=1) on the
