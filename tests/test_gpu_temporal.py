@@ -76,6 +76,26 @@ def test_warp_f32_small_motion_vs_oracle(ops, amp, c, h, w):
     np.testing.assert_allclose(hwc(gp), gp_r, rtol=1e-5, atol=1e-5 * np.abs(gp_r).max())
 
 
+def test_warp_f32_integer_motion_vs_oracle(ops):
+    """Integer-valued motion (fractions 0: one tap weight 1, three 0) through
+    the staged warp and the landing-mask transpose, incl. the |o| = 2 and
+    |o| = 3 mask layouts."""
+    rng = np.random.default_rng(5)
+    h, w = 41, 72
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    for amp in (2, 3):
+        prev = f32(rng.lognormal(-1, 1.0, (h, w, 3)))
+        g = f32(rng.normal(size=(h, w, 3)))
+        m = rng.integers(-amp, amp + 1, (h, w, 2)).astype(np.float64)
+        out_r, val_r = ot.warp_array(prev, m)
+        gp_r = ot.warp_backward(g, m)
+        out, val = ops.warp(planar(prev, torch.float32), planar(m, torch.float32))
+        gp = ops.warp_backward(planar(g, torch.float32), planar(m, torch.float32))
+        np.testing.assert_allclose(hwc(out), out_r, rtol=1e-5, atol=1e-5 * np.abs(out_r).max())
+        np.testing.assert_allclose(val[0].double().cpu().numpy(), val_r, rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(hwc(gp), gp_r, rtol=1e-5, atol=1e-5 * np.abs(gp_r).max())
+
+
 def test_warp_f32_deterministic_and_adjoint_1080p(ops):
     gen = torch.Generator(device="cuda").manual_seed(1)
     x = torch.randn((2, 3, 1080, 1920), device="cuda", generator=gen)
