@@ -2,14 +2,15 @@
 // previous frame and its transpose, planar on device.
 //   warp_array    images.py:88-119   out(p) = sum_k w_k(p) prev(tap_k(p)), validity = sum_k w_k
 //   warp_backward images.py:122-147  grad_prev = transpose (np.add.at scatter)
-// The transpose is computed as a deterministic GATHER: every target pixel
-// scans the sources that can reach it (|q - p| <= ceil(max|motion|) + 1,
-// staged in shared memory per tile when max|motion| <= 5; float32 with
-// max|motion| <= 3 through per-cell landing masks), in float64 in the
-// reference's own order (tap-major, then sources in raster order) so the
-// result reproduces np.add.at bit for bit; float32 in a fixed order.  No
-// floating-point atomics: results are run-to-run identical.
-// Compiled with -fmad=false (products and sums rounded like numpy).
+// The transpose is computed as a deterministic GATHER.  float64: every target
+// pixel scans the sources that can reach it (|q - p| <= ceil(max|motion|) + 1,
+// staged in shared memory per tile when max|motion| <= 5) in the reference's
+// own order (tap-major, then sources in raster order), so the result
+// reproduces np.add.at bit for bit.  float32 with max|motion| <= 3: per-cell
+// landing bit masks, per-cell tap sums, then 4 cells per target, in a fixed
+// order (general scan beyond).  No floating-point atomics: results are
+// run-to-run identical.  Compiled with -fmad=false (products and sums rounded
+// like numpy; the float32 kernels use explicit FMAs where they want them).
 #include <math.h>
 #include <string>
 

@@ -7,7 +7,10 @@
 //   (optimize.py:219-231): the per-pixel max picks the branch (ties to the
 //   spatial term), g_sp = [spatial wins] / N, g_tm = [temporal wins] * 1.25 / N.
 // Images (B, 3, H, W); maps (B, H, W); per-frame loss scalars reduced in a
-// fixed order (deterministic).  Compiled with -fmad=false.
+// fixed order (deterministic).  ssb_losses runs maps, sums and gradients in
+// one pass; ssb_epilogue fuses tonemap -> losses -> gradient -> tonemap
+// backward per pixel.  Compiled with -fmad=false (float64 parity; the float32
+// vector kernels use explicit FMAs).
 #include <math.h>
 #include <string>
 
