@@ -10,7 +10,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 [-DPS=4 -DNST=2 -DMINB=2] \
 //        pattern_probe.cu -o pattern_probe -lcuda
 //   ./pattern_probe [frames]
-// PS = rows per step, NST = TMA stages (prefetch NST - 1 steps ahead), MINB = CTAs per SM
+// PS = rows per step, NST = TMA stages (prefetch NST - 1 steps ahead), MINB = CTAs per SM,
+// NTHR = threads per CTA (the store stream's issuers)
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -30,6 +31,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 #endif
 #ifndef MINB
 #define MINB 2
+#endif
+#ifndef NTHR
+#define NTHR 256
 #endif
 constexpr int NLOG = 29, S = PS, TXB = 60, RX = 68, RA = 4, SEG = 120, CB = 36, CT = S;
 constexpr int al32(int n) { return (n + 31) & ~31; }  // TMA destinations 128-B aligned
@@ -56,7 +60,7 @@ __device__ __forceinline__ void wait(uint64_t* bar, int parity) {
                  : "memory");
 }
 
-__global__ void __launch_bounds__(256, MINB) k_probe(const __grid_constant__ Maps mp, int H, int W, float* gl, float* gx) {
+__global__ void __launch_bounds__(NTHR, MINB) k_probe(const __grid_constant__ Maps mp, int H, int W, float* gl, float* gx) {
     extern __shared__ __align__(128) float sm[];
     __shared__ __align__(8) uint64_t bars[NST];
     const int tid = threadIdx.x, b = blockIdx.z;
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(const __grid_constant__ Map
         const float* st = sm + (i % NST) * STAGE;
         const int qs = y0 + i * S;
         // writes: 29 + 6 planes x S rows x 60 own columns as float4 (15 quads per row)
-        for (int it = tid; it < (NLOG + 6) * S * 15; it += 256) {  // (S rows)
+        for (int it = tid; it < (NLOG + 6) * S * 15; it += NTHR) {  // (S rows)
             const int q = it % 15, r = (it / 15) % S, pl = it / (15 * S);
             const int y = qs + r, x = x0 + 4 * q;
             if (y >= y1 || x >= W) continue;
@@ -131,13 +135,13 @@ int main(int argc, char** argv) {
     const int smem = NST * STAGE * 4;
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     dim3 grid(W / TXB, (H + SEG - 1) / SEG, B);
-    for (int w = 0; w < 3; ++w) k_probe<<<grid, 256, smem>>>(mp, H, W, gl, gx);
+    for (int w = 0; w < 3; ++w) k_probe<<<grid, NTHR, smem>>>(mp, H, W, gl, gx);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int reps = 10;
     cudaEventRecord(e0);
-    for (int r = 0; r < reps; ++r) k_probe<<<grid, 256, smem>>>(mp, H, W, gl, gx);
+    for (int r = 0; r < reps; ++r) k_probe<<<grid, NTHR, smem>>>(mp, H, W, gl, gx);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0.f;
@@ -145,7 +149,7 @@ int main(int argc, char** argv) {
     ms /= reps;
     // algorithmic bytes of the real kernel's pattern (own pixels): reads 29 + 12 planes + T1/4, writes 29 + 6
     const double px = (double)B * hw, bytes = px * (4.0 * (NLOG + 12) + 3.0 + 4.0 * (NLOG + 6));
-    printf("pattern probe S=%d stages=%d minb=%d: %d frames 1080p, smem %d B/CTA, %.3f ms, %.1f B/px -> %.1f GB/s (%s)\n",
-           PS, NST, MINB, B, smem, ms, bytes / px, bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    printf("pattern probe S=%d stages=%d minb=%d threads=%d: %d frames 1080p, smem %d B/CTA, %.3f ms, %.1f B/px -> %.1f GB/s (%s)\n",
+           PS, NST, MINB, NTHR, B, smem, ms, bytes / px, bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
