@@ -48,7 +48,7 @@ struct TmaMaps {
 // CH: level 0 runs after the coarser levels (pyr_chain.cuh): no upsample
 // transpose (ghat^1 comes from k_up_transpose) and the flush adds the pool
 // chain T1(parent) / count, writing the final g_noisy / g_demod
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4>
 struct TmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
@@ -57,7 +57,10 @@ struct TmaShape {
     // wide, TXB a multiple of RA.  k = 7 uses narrower strips (shared memory).
     static constexpr int LGE = (int)sizeof(TL);  // logit element size
     static constexpr bool SEP = LGE != 4;        // bf16: staging box + separate fp32 exponentials
-    static constexpr int RA = 16 / LGE, S = 4;
+    // SS = rows per step: 4 (256 threads, 2 CTAs per SM) or 8 (512 threads, one
+    // CTA per SM: twice the TMA box rows per request)
+    static constexpr int RA = 16 / LGE, S = SS;
+    static constexpr int NTH = 64 * SS, HN = NTH / 2, MINB = SS == 4 ? 2 : 1;
     static constexpr int TXW = ((64 - 2 * R) / RA) * RA;
     static constexpr int TXB = K >= 7 ? 32 : TXW, RX = TXB + 2 * RA, RW = TXB + 2 * R;
     static constexpr int TXC = TXB / 2, NQUAD = TXB / 4;
@@ -69,11 +72,11 @@ struct TmaShape {
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
     // B1: S * NQUAD pixel quads on warps 0-3; tap rows split in B1SPL warp-uniform parts
     static constexpr int NB1 = S * NQUAD;
-    static constexpr int B1SPL = NB1 <= 32 ? 4 : (NB1 <= 64 ? 2 : 1);
-    static constexpr int B1ITEMS = 128 / B1SPL;
+    static constexpr int B1SPL = NB1 <= HN / 4 ? 4 : (NB1 <= HN / 2 ? 2 : 1);
+    static constexpr int B1ITEMS = HN / B1SPL;
     static constexpr int DYS = (K + B1SPL - 1) / B1SPL;  // tap rows per part
     // B2: TXB columns x B2SPL tap-column groups on warps 4-7 (adjacent lanes)
-    static constexpr int B2SPL = TXB * 4 <= 128 ? 4 : (TXB * 2 <= 128 ? 2 : 1);
+    static constexpr int B2SPL = TXB * 4 <= HN ? 4 : (TXB * 2 <= HN ? 2 : 1);
     static constexpr int AW = S + 2 * R, NPW = (AW + 1) / 2;  // output-row window (float2 pairs)
     // coarse box: 16-B aligned start (x0/2 rounded down to 4), TXC + 1 + 3 cols
     static constexpr int CR = 4, CB = ((TXB / 2 + 4 + 3) / 4) * 4, CROWS = S / 2 + 1;
@@ -120,10 +123,11 @@ struct TmaShape {
                                      3 * S * RX + S * RX + (B3ON ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
-    static_assert(TXB * B2SPL <= 128 && 3 * TXC <= 128 && TXB % 4 == 0, "B2/B3 items exceed their warps");
-    static_assert(S * RW <= 256 && RW <= 64, "phase A items exceed the CTA");
-    static_assert(S == 4 && (32 % B2SPL) == 0, "step geometry");
-    static_assert(SMEM + 1024 <= 233472 / 2, "two CTAs per SM");
+    static_assert(TXB * B2SPL <= HN && 3 * TXC <= HN && TXB % 4 == 0, "B2/B3 items exceed their warps");
+    static_assert(S * RW <= NTH && RW <= 64, "phase A items exceed the CTA");
+    static_assert((S == 4 || S == 8) && (32 % B2SPL) == 0, "step geometry");
+    static_assert(!(UP && !CH) || S == 4, "the B3 coarse-row ring (CR = 4) assumes 4-row steps");
+    static_assert(SMEM + 1024 <= 233472 / MINB, "CTAs per SM");
 };
 
 // paired gradient store (two horizontally adjacent pixels, 8-B / 4-B aligned)
@@ -187,7 +191,8 @@ __device__ __forceinline__ float rcp_fast(float x) {  // MUFU.RCP (x >= 1e-3 her
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0, 256;" ::: "memory"); }
+template <int NTH = 256>
+__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0, %0;" ::"n"(NTH) : "memory"); }
 
 #ifdef SSB_ROLE_TIMING
 // experiment build only: per role (warps 0-3 / 4-7) cycles spent waiting for
@@ -207,10 +212,11 @@ static inline int role_cycles_read(unsigned long long* out8) {
 #define SSB_RT(...)
 #endif
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
-__global__ void __launch_bounds__(256, 2)
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4>
+__global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), (TmaShape<K, TL, L0, UP, TIED, CH, SS>::MINB))
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS>;
+    constexpr int NTH = SH::NTH, HN = SH::HN;
     constexpr bool B3ON = SH::B3ON;
     constexpr int CT = SH::CT, T1F = SH::T1F;
     constexpr bool SEP = SH::SEP;
@@ -251,10 +257,10 @@ __global__ void __launch_bounds__(256, 2)
     // image-ring row r for rows of the current step's window [qs - NPRO*S + R, qs + 2S + R)
     auto lin_row_step = [&](int qs, int r, int which) {
         const int rel = r - qs - R + NPRO * S;      // >= 0
-        int slt = sl_i - NPRO + (rel >> 2);         // S == 4
+        int slt = sl_i - NPRO + rel / S;
         slt += slt < 0 ? NBL : 0;
         slt -= slt >= NBL ? NBL : 0;
-        return s_lin + slt * BLKF + which * DEMOFF + (rel & 3) * RX;
+        return s_lin + slt * BLKF + which * DEMOFF + (rel % S) * RX;
     };
     auto ring_block = [&](float* base, int j) { return base + ((j + 64 * NBU) % NBU) * UPF; };
     // image-ring row r (absolute) -> pointer to plane `which` (0: x0/L, 1: demod), channel 0
@@ -283,29 +289,29 @@ __global__ void __launch_bounds__(256, 2)
     };
 
     // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion);
-    // called by all 256 threads with uniform arguments
+    // called by all threads with uniform arguments
     const bool col_border = xs0 < 0 || xs0 + RX > W;
     auto patch_rows = [&](int r0, int r1) {
         if (col_border) {
             // only the columns outside the image: [0, lo) and [hi, RX)
             const int lo = max(0, -xs0), hi = min(RX, W - xs0), nb = lo + (RX - hi);
-            for (int i = tid; i < (r1 - r0) * NI * 3 * nb; i += 256) {
+            for (int i = tid; i < (r1 - r0) * NI * 3 * nb; i += NTH) {
                 const int k = i % nb, rest = i / nb;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
                 const int ri = k < lo ? k : hi + (k - lo), src = k < lo ? lo : hi - 1;
                 float* row = lin_row(r, pc / 3) + (pc % 3) * PL;
                 row[ri] = row[src];
             }
-            cta_sync();
+            cta_sync<NTH>();
         }
         if (r0 < 0 || r1 > H) {
-            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += 256) {
+            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += NTH) {
                 const int ri = i % RX, rest = i / RX;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
                 const int src = clampi(r, 0, H - 1);
                 if (src != r) lin_row(r, pc / 3)[(pc % 3) * PL + ri] = lin_row(src, pc / 3)[(pc % 3) * PL + ri];
             }
-            cta_sync();
+            cta_sync<NTH>();
         }
     };
     // x0 = noisy / max(d, floor) in place (level 0), for ring rows of block j
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(256, 2)
 
     // ---- prologue
     if constexpr (B3ON)
-        for (int i = tid; i < CR * 3 * TXC; i += 256) s_cac[i] = 0.f;
+        for (int i = tid; i < CR * 3 * TXC; i += NTH) s_cac[i] = 0.f;
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(256, 2)
         if (nsteps > 0) issue_step(0);
     }
     mbar_wait(&bars[3], 0);
-    for (int i = tid; i < NPRO * S * RX; i += 256) {
+    for (int i = tid; i < NPRO * S * RX; i += NTH) {
         const int jj = i / (S * RX), rem = i % (S * RX);
         convert_block(jj - NPRO, rem / RX, rem % RX);
     }
@@ -406,7 +412,7 @@ __global__ void __launch_bounds__(256, 2)
             }
             s_inn[s_a * RX + ri_a] = inner * inv;
         }
-        cta_sync();
+        cta_sync<NTH>();
         if constexpr (!SH::EARLY) {
             // every thread has finished the previous step and this step's phase A:
             // the buffers of step i+1 are free
@@ -423,14 +429,14 @@ __global__ void __launch_bounds__(256, 2)
 
     // B1 / B3 role (warps 0-3)
     int cnext = qstart >> 1;
-    const int part = B1SPL == 1 ? 0 : (tid & 127) / SH::B1ITEMS;
-    const int item = (tid & 127) - part * SH::B1ITEMS;
+    const int part = B1SPL == 1 ? 0 : (tid % HN) / SH::B1ITEMS;
+    const int item = (tid % HN) - part * SH::B1ITEMS;
     const int s = item / NQUAD, xi = 4 * (item - s * NQUAD), ri = xi + RA;
     // B2 role (warps 4-7)
-    const int b2 = tid & 127;
+    const int b2 = tid % HN;
     const int col = b2 / B2SPL, part2 = b2 - col * B2SPL;
     const int gx2 = x0 + col, ri2 = col + RA;
-    const bool act2 = tid >= 128 && col < TXB && gx2 < W;
+    const bool act2 = tid >= HN && col < TXB && gx2 < W;
     // the lanes of a column split the tap columns dx (window rows stay compile-time)
     constexpr int DXN = (K + B2SPL - 1) / B2SPL;
     const int dx0 = -R + part2 * DXN, ndx = min(DXN, R + 1 - dx0);
@@ -456,7 +462,7 @@ __global__ void __launch_bounds__(256, 2)
         phase_a(i, qs, lgb,
                 reinterpret_cast<const TL*>(SEP ? s_lg + LGF + (SH::EARLY ? (i & 1) * LGS1 : 0) : lgb));
         SSB_RT(const long long rt_t1 = clock64(); rt_acc[0] += rt_tw - rt_t0; rt_acc[1] += rt_t1 - rt_tw;)
-        if (tid < 128) {
+        if (tid < HN) {
             // -------------------------------------------- B1: logit gradients
             const int qy = qs + s, gx = x0 + xi;
             // W is a multiple of 4 on this path: the quad (gx .. gx + 3) is in
@@ -805,11 +811,13 @@ __global__ void __launch_bounds__(256, 2)
                     }
                 }
             };
+            // the step's S finished rows, four per block
             flush_block(std::integral_constant<int, 0>{});
+            if constexpr (S > 4) flush_block(std::integral_constant<int, 4>{});
             if (bottom) {
                 // the image's last rows: the whole window is final
                 if constexpr (AW > S) flush_block(std::integral_constant<int, (AW > S ? S : 0)>{});
-                if constexpr (AW > 2 * S) flush_block(std::integral_constant<int, (AW > 2 * S ? 2 * S : 0)>{});
+                if constexpr (AW > S + 4) flush_block(std::integral_constant<int, (AW > S + 4 ? S + 4 : 0)>{});
             }
             // slide the window by S rows
 #pragma unroll
@@ -819,14 +827,14 @@ __global__ void __launch_bounds__(256, 2)
                     win[p][c] = p + S / 2 < NPW ? win[p + S / 2][c] : make_float2(0.f, 0.f);
         }
         SSB_RT(const long long rt_t2 = clock64();)
-        cta_sync();  // end of step
+        cta_sync<NTH>();  // end of step
         SSB_RT(const long long rt_t3 = clock64(); rt_acc[2] += rt_t2 - rt_t1; rt_acc[3] += rt_t3 - rt_t2;)
-        if (B3ON && tid < 128) {
+        if (B3ON && tid < HN) {
             // coarse ghat rows finished by this step (all B3 items are in)
             const bool bottom = qs + S >= H;
             const int cend = bottom ? a.Hc : (qs + S) >> 1;
             const int own0 = y0 >> 1, own1 = (y1 + 1) >> 1;
-            for (int k2 = tid; k2 < (cend - cnext) * TXC; k2 += 128) {
+            for (int k2 = tid; k2 < (cend - cnext) * TXC; k2 += HN) {
                 const int rr = k2 / TXC, cxi = k2 - rr * TXC;
                 const int Y = cnext + rr, X = (x0 >> 1) + cxi;
                 float v[3];
@@ -850,7 +858,7 @@ __global__ void __launch_bounds__(256, 2)
 #define SSB_ROLE_TIMING_L0 -1  // -1: every level; 1: level 0 only; 0: levels >= 1 only
 #endif
     if ((tid & 31) == 0 && (SSB_ROLE_TIMING_L0 < 0 || (SSB_ROLE_TIMING_L0 == 1) == L0))
-        for (int k = 0; k < 4; ++k) atomicAdd(&g_role_cycles[(tid < 128 ? 0 : 4) + k], rt_acc[k]);
+        for (int k = 0; k < 4; ++k) atomicAdd(&g_role_cycles[(tid < HN ? 0 : 4) + k], rt_acc[k]);
 #endif
 }
 

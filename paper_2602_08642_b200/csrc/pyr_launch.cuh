@@ -118,9 +118,9 @@ inline bool tma_disabled() {
     return e && e[0] == '1';
 }
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4>
 bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS>;
     // needs the forward output (level 0) / Lhat^l for the softmax-backward inner product
     if ((L0 && !a0.demod) || !a0.outp || tma_disabled()) return false;
     const long long plane = (long long)a0.H * a0.W;
@@ -356,9 +356,18 @@ BwdLevel bwd_level(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io
 // pre-pass, levels 1..L-1, the level-1 pool chain, then level 0 writing the
 // final g_noisy / g_demod (no coarse->fine sweep kernel).  Returns 1 without
 // launching anything if level 0 is not TMA-addressable.
-template <int K, typename TL, bool TIED>
-int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
-                       void* ws, cudaStream_t s) {
+// SSB_BWD_S8=1 (experiment): the level-0 kernel with 8-row steps, 512 threads
+inline bool bwd_s8() {
+    static const bool on = [] {
+        const char* e = getenv("SSB_BWD_S8");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+template <int K, typename TL, bool TIED, int SS>
+int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
+                          void* ws, cudaStream_t s) {
     const char* tp = (const char*)tape;
     char* wp = (char*)ws;
     const bool want = io->g_logits[0] != nullptr;
@@ -366,7 +375,7 @@ int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bw
     BwdLevel a0 = bwd_level<float>(d, p, io, tp, wp, 0, want, accum);
     a0.t1 = wp + p.gl_off[1];
     TmaMaps mp0;
-    if (!prepare_bwd_tma<K, TL, true, true, TIED, true>(a0, mp0)) return 1;
+    if (!prepare_bwd_tma<K, TL, true, true, TIED, true, SS>(a0, mp0)) return 1;
     {
         UpTransposeArgs u{};
         u.H = p.H;
@@ -398,15 +407,23 @@ int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bw
         dim3 grid((p.wl[1] + 127) / 128, (p.hl[1] + 7) / 8, p.B);
         SSB_LAUNCH(s, k_pool_chain<<<grid, dim3(32, 8), 0, s>>>(c));
     }
-    using SH = TmaShape<K, TL, true, true, TIED, true>;
-    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true>;
+    using SH = TmaShape<K, TL, true, true, TIED, true, SS>;
+    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true, SS>;
     static std::atomic<unsigned long long> attr_mask{0};
     smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     const int strips = (a0.W + SH::TXB - 1) / SH::TXB;
     a0.seg_h = pick_segment(strips, a0.H, a0.batch);
     dim3 grid(strips, (a0.H + a0.seg_h - 1) / a0.seg_h, a0.batch);
-    SSB_LAUNCH(s, kern<<<grid, 256, SH::SMEM, s>>>(a0, mp0));
+    SSB_LAUNCH(s, kern<<<grid, SH::NTH, SH::SMEM, s>>>(a0, mp0));
     return cuda_check("ssb_pyr_backward");
+}
+
+template <int K, typename TL, bool TIED>
+int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
+                       void* ws, cudaStream_t s) {
+    if constexpr (K == 5 && std::is_same<TL, float>::value)
+        if (bwd_s8()) return run_backward_chain_ss<K, TL, TIED, 8>(d, p, io, tape, ws, s);
+    return run_backward_chain_ss<K, TL, TIED, 4>(d, p, io, tape, ws, s);
 }
 
 template <int K, typename TL, typename T>
