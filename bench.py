@@ -578,6 +578,10 @@ def gpu_arm(args, rank, world, local_rank, dist):
     except (OSError, ValueError, KeyError):
         pass
     dom_gbs = dom_b * B / (dom_ms * 1e-3) / 1e9 if dom_ms else None
+    # per-GPU step bytes: c4b at N > 1 splits ONE frame into N row bands, so
+    # each rank moves ~1/N of the frame's bytes (band halos are not algorithmic)
+    if fwd_only and world > 1:
+        step_bytes = step_bytes / world
     step_gbs = step_bytes * B / (ms * 1e-3) / 1e9
     res = {
         "metric": f"pyramidal filter {'fwd' if fwd_only else 'fwd+bwd'} throughput ({args.workload})",

@@ -297,6 +297,10 @@ class Grads:
     demod: np.ndarray | None
     input: np.ndarray
     prev: np.ndarray | None
+    # per level: max |w * gw| and |w * sum(w gw)| -- the magnitude of the two
+    # softmax-backward operands whose difference the logit gradient is (test
+    # comparators use it as the cancellation-aware atol scale)
+    operand_scale: list | None = None
 
 
 def forward(noisy, logits, prev=None, demod=None, k: int | None = None,
@@ -401,15 +405,21 @@ def backward(tape: Tape, upstream, want_param_grads: bool = True) -> Grads:
     glogits = None
     if want_param_grads:
         glogits = []
+        scales = []
         for l in range(levels):
-            if l == 0 and not tape.temporal and w[0].shape[-1] > t0:
+            n = t0 if (l == 0 and not tape.temporal and w[0].shape[-1] > t0) else w[l].shape[-1]
+            if n < w[l].shape[-1]:
                 gz = np.zeros_like(gw[0])
                 gz[:, :, :t0] = softmax_channels_backward(w[0][:, :, :t0], gw[0][:, :, :t0])
             else:
                 gz = softmax_channels_backward(w[l], gw[l])
             glogits.append(gz)
+            wg = w[l][:, :, :n] * gw[l][:, :, :n]
+            dot = np.abs(wg.sum(axis=-1, keepdims=True)) * w[l][:, :, :n]
+            scales.append(max(float(np.abs(wg).max(initial=0.0)), float(dot.max(initial=0.0))))
         if tape.extra.get("blend") == "tied":
             glogits = collapse_blend_grads(glogits, k)
+            scales = [4.0 * x for x in scales]  # the blend gradient sums 4 taps
 
     gdemod = None
     if tape.demod is not None:
@@ -423,7 +433,8 @@ def backward(tape: Tape, upstream, want_param_grads: bool = True) -> Grads:
             gdemod = np.where(tape.demod > DEMOD_FLOOR, gdc, 0.0)
     else:
         gnoisy = gx0
-    return Grads(logits=glogits, demod=gdemod, input=gnoisy, prev=gprev)
+    return Grads(logits=glogits, demod=gdemod, input=gnoisy, prev=gprev,
+                 operand_scale=scales if want_param_grads else None)
 
 
 # ---------------------------------------------------------------------------

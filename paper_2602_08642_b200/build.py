@@ -29,6 +29,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I", os.path.join(ROOT, "include")]
 # experiments only (e.g. SSB_NVCC_FLAGS=-DSSB_ROLE_TIMING; delete lib/obj first)
 COMMON += os.environ.get("SSB_NVCC_FLAGS", "").split()
+# (experiments: -DSSB_BWD_VARIANTS adds the level-0 backward ring-depth /
+# strip-width variants selectable with SSB_BWD0, see pyr_launch.cuh)
 # per-file extra flags: placement decisions must round exactly like numpy
 EXTRA = {"place.cu": ["-fmad=false"], "temporal.cu": ["-fmad=false"], "scores.cu": ["-fmad=false"], "tonemap.cu": ["-fmad=false"]}
 

@@ -21,6 +21,10 @@ import torch
 
 _PRECISION = os.environ.get("SSB_COMPAT_PRECISION", "f64")
 _DEVICE = os.environ.get("SSB_COMPAT_DEVICE", "cuda")
+# number of compat calls that reached the device (every compat op resolves its
+# device through device()); the reference-suite test reads it to prove the
+# patched path ran
+device_calls = 0
 
 
 def set_precision(p: str) -> None:
@@ -39,6 +43,8 @@ def dtype() -> torch.dtype:
 
 
 def device() -> torch.device:
+    global device_calls
+    device_calls += 1
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2602_08642_b200.compat needs a CUDA device (no CPU fallback)")
     return torch.device(_DEVICE)

@@ -258,11 +258,15 @@ int ssb_pyr_workspace_bytes(const ssb_pyr_desc* d, size_t* bytes) {
 }  // extern "C"
 
 namespace ssb {
-template <int K, typename TL, typename T>
-int run_forward(const ssb_pyr_desc*, const PyrPlan&, const ssb_pyr_fwd_io*, void*, cudaStream_t);
-template <int K, typename TL, typename T>
-int run_backward(const ssb_pyr_desc*, const PyrPlan&, const ssb_pyr_bwd_io*, const void*, void*,
-                 cudaStream_t);
+SSB_EXTERN_PYR(3, float, float)
+SSB_EXTERN_PYR(3, __nv_bfloat16, float)
+SSB_EXTERN_PYR(3, double, double)
+SSB_EXTERN_PYR(5, float, float)
+SSB_EXTERN_PYR(5, __nv_bfloat16, float)
+SSB_EXTERN_PYR(5, double, double)
+SSB_EXTERN_PYR(7, float, float)
+SSB_EXTERN_PYR(7, __nv_bfloat16, float)
+SSB_EXTERN_PYR(7, double, double)
 
 template <typename Fn>
 static int by_types(const ssb_pyr_desc* d, Fn&& fn) {

@@ -48,7 +48,11 @@ struct TmaMaps {
 // CH: level 0 runs after the coarser levels (pyr_chain.cuh): no upsample
 // transpose (ghat^1 comes from k_up_transpose) and the flush adds the pool
 // chain T1(parent) / count, writing the final g_noisy / g_demod
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4>
+// NST = TMA ring depth: step j's boxes land in slot j % NST and are issued
+// NST - 1 steps ahead (at the top of step j - NST + 1, right after the end
+// barrier of step j - NST, whose slot it reuses).  TXO != 0 overrides the
+// strip's own-column count (a multiple of RA).
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0>
 struct TmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
@@ -60,15 +64,15 @@ struct TmaShape {
     // SS = rows per step: 4 (256 threads, 2 CTAs per SM) or 8 (512 threads, one
     // CTA per SM: twice the TMA box rows per request)
     static constexpr int RA = 16 / LGE, S = SS;
-    static constexpr int NTH = 64 * SS, HN = NTH / 2, MINB = SS == 4 ? 2 : 1;
+    static constexpr int NTH = 64 * SS, HN = NTH / 2;
     static constexpr int TXW = ((64 - 2 * R) / RA) * RA;
-    static constexpr int TXB = K >= 7 ? 32 : TXW, RX = TXB + 2 * RA, RW = TXB + 2 * R;
+    static constexpr int TXB = TXO ? TXO : (K >= 7 ? 32 : TXW), RX = TXB + 2 * RA, RW = TXB + 2 * R;
     static constexpr int TXC = TXB / 2, NQUAD = TXB / 4;
     static constexpr int NPRO = (2 * R + S - 1) / S;  // image-ring blocks above step 0
-    static constexpr int NBL = NPRO + 2;               // image-ring blocks (incl. prefetch)
+    static constexpr int NBL = NPRO + NST;             // image-ring blocks (incl. prefetch)
     // upstream ring (level 0: the flush needs u * out, R rows behind); other
     // levels and the forward output / Lhat^l: one block (read in phase A only)
-    static constexpr int NBU0 = L0 ? (R + S - 1) / S + 2 : 2;  // gradient-input ring (2 at l >= 1 with early issue)
+    static constexpr int NBU0 = L0 ? (R + S - 1) / S + NST : NST;  // gradient-input ring (NST at l >= 1 with early issue)
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
     // B1: S * NQUAD pixel quads on warps 0-3; tap rows split in B1SPL warp-uniform parts
     static constexpr int NB1 = S * NQUAD;
@@ -105,27 +109,29 @@ struct TmaShape {
     // the previous step's end barrier) instead of after phase A -- every
     // buffer it overwrites belongs to step i-1; needs a second output block,
     // and for fp32 logits only (bf16 would need a second staging box)
-    static constexpr size_t FL_BASE = (size_t)NBL * BLKF + 2 * LHF + 2 * T1F + 3 * S * RX + S * RX +
-                                      (B3ON ? CR * 3 * TXC : 0);
-    // (bf16: measured no gain at k = 7 with the second staging box -- kept off)
-    static constexpr bool EARLY_FITS = ((size_t)LGF + 2 * LGS1 + FL_BASE + (NBU0 + 2) * UPF) * 4 + 64 <= 113 * 1024;
-    static constexpr bool EARLY = !SEP;
-    static constexpr int NOB = EARLY ? 2 : 1;
-    static constexpr int LGS = EARLY ? 2 * LGS1 : LGS1;  // staging floats (both boxes)
-    static constexpr int LGBUF = SEP ? LGF + LGS : 2 * LGF;
+    // (bf16 at NST = 2: measured no gain at k = 7 with the second staging box
+    // -- issued after phase A instead; NST >= 3 always issues early)
+    static constexpr bool EARLY = !SEP || NST > 2;
+    static constexpr int NOB = EARLY ? NST : 1;
+    static constexpr int LGS = EARLY ? NST * LGS1 : LGS1;  // staging floats (all boxes)
+    static constexpr int LGBUF = SEP ? LGF + LGS : NST * LGF;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
     static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
                                         (CH ? 3 * CT * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr int NBU = L0 ? NBU0 : (EARLY ? 2 : 1);
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + 2 * LHF + 2 * T1F +
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F +
                                      3 * S * RX + S * RX + (B3ON ? CR * 3 * TXC : 0);
     static constexpr size_t SMEM = FLOATS * 4 + 64;
+    // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
+    static constexpr int MINB = (SS == 4 && 2 * (SMEM + 1024) <= 233472) ? 2 : 1;
     static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
+    // the upsample-tap gradients follow the last part's tap rows (t = NT)
+    static_assert(!UP || (B1SPL - 1) * DYS < K, "last B1 part must own the last tap row");
     static_assert(TXB * B2SPL <= HN && 3 * TXC <= HN && TXB % 4 == 0, "B2/B3 items exceed their warps");
     static_assert(S * RW <= NTH && RW <= 64, "phase A items exceed the CTA");
-    static_assert((S == 4 || S == 8) && (32 % B2SPL) == 0, "step geometry");
+    static_assert((S == 4 || S == 8) && (32 % B2SPL) == 0 && NST >= 2 && NST <= 4 && TXB % RA == 0, "step geometry");
     static_assert(!(UP && !CH) || S == 4, "the B3 coarse-row ring (CR = 4) assumes 4-row steps");
     static_assert(SMEM + 1024 <= 233472 / MINB, "CTAs per SM");
 };
@@ -212,10 +218,11 @@ static inline int role_cycles_read(unsigned long long* out8) {
 #define SSB_RT(...)
 #endif
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4>
-__global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), (TmaShape<K, TL, L0, UP, TIED, CH, SS>::MINB))
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0>
+__global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>::NTH),
+                                  (TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>::MINB))
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>;
     constexpr int NTH = SH::NTH, HN = SH::HN;
     constexpr bool B3ON = SH::B3ON;
     constexpr int CT = SH::CT, T1F = SH::T1F;
@@ -231,13 +238,13 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
     constexpr int RUP = (R + 1) & ~1;
 
     extern __shared__ __align__(128) unsigned char smem_tma[];
-    float* s_lg = reinterpret_cast<float*>(smem_tma);  // [2][NLOG][S][RX] | [NLOG][S][RX] + staging
+    float* s_lg = reinterpret_cast<float*>(smem_tma);  // [NST][NLOG][S][RX] | [NLOG][S][RX] + staging
     float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RX]
     float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]  (level 0: u * out after A)
     float* s_ob = s_up + NBU * UPF;                    // [NOB][3][S][RX]  forward output / Lhat^l
-    float* s_lhc = s_ob + SH::NOB * UPF;               // [2][3][CROWS][CB]
-    float* s_t1 = s_lhc + 2 * SH::LHF;                 // [2][3][CT][CB]   (CH)
-    float* s_g = s_t1 + 2 * T1F;                       // [3][S][RX]  G = gout / sum
+    float* s_lhc = s_ob + SH::NOB * UPF;               // [NST][3][CROWS][CB]
+    float* s_t1 = s_lhc + NST * SH::LHF;               // [NST][3][CT][CB]   (CH)
+    float* s_g = s_t1 + NST * T1F;                     // [3][S][RX]  G = gout / sum
     float* s_inn = s_g + 3 * PL;                       // [S][RX]     inner' = sum_c gin_c out_c / sum
     float* s_cac = s_inn + PL;                         // [CR][3][TXC] coarse ghat accumulators
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
@@ -275,18 +282,19 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
 
     // ---- TMA issue (thread 0)
     auto issue_step = [&](int j) {
-        uint64_t* bar = &bars[j & 1];
+        const int js = j % NST;
+        uint64_t* bar = &bars[js];
         const int qs = qstart + j * S;
         mbar_expect_tx(bar, SH::TX_STEP);
-        tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? (j & 1) * LGS1 : 0) : s_lg + (j & 1) * LGF, &mp.lg, xs0, qs,
-                    0, b, bar);
+        tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? js * LGS1 : 0) : s_lg + js * LGF, &mp.lg, xs0, qs, 0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
         tma_load_4d(ring_block(s_up, j), &mp.up, xs0, qs, c0, b, bar);
-        tma_load_4d(s_ob + (SH::EARLY ? (j & 1) * UPF : 0), &mp.out, xs0, qs, c0, b, bar);
-        if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
-        if constexpr (CH) tma_load_4d(s_t1 + (j & 1) * T1F, &mp.t1, cxs, (qs - R) >> 1, c0, b, bar);
+        tma_load_4d(s_ob + (SH::EARLY ? js * UPF : 0), &mp.out, xs0, qs, c0, b, bar);
+        if constexpr (UP) tma_load_4d(s_lhc + js * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
+        if constexpr (CH) tma_load_4d(s_t1 + js * T1F, &mp.t1, cxs, (qs - R) >> 1, c0, b, bar);
     };
+    constexpr int PBAR = 7;  // prologue barrier (step barriers: 0 .. NST-1)
 
     // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion);
     // called by all threads with uniform arguments
@@ -330,19 +338,20 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
     if constexpr (B3ON)
         for (int i = tid; i < CR * 3 * TXC; i += NTH) s_cac[i] = 0.f;
     if (tid == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0) {
-        mbar_expect_tx(&bars[3], SH::TX_PRO);
+        mbar_expect_tx(&bars[PBAR], SH::TX_PRO);
         for (int j = -NPRO; j < 0; ++j) {
-            tma_load_4d(lin_block(j), &mp.lin, xs0, qstart + R + j * S, c0, b, &bars[3]);
-            if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qstart + R + j * S, c0, b, &bars[3]);
+            tma_load_4d(lin_block(j), &mp.lin, xs0, qstart + R + j * S, c0, b, &bars[PBAR]);
+            if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qstart + R + j * S, c0, b, &bars[PBAR]);
         }
-        if (nsteps > 0) issue_step(0);
+        // the first steps: NST - 1 ahead when issuing early, else one
+        for (int j = 0; j < (SH::EARLY ? NST - 1 : 1) && j < nsteps; ++j) issue_step(j);
     }
-    mbar_wait(&bars[3], 0);
+    mbar_wait(&bars[PBAR], 0);
     for (int i = tid; i < NPRO * S * RX; i += NTH) {
         const int jj = i / (S * RX), rem = i % (S * RX);
         convert_block(jj - NPRO, rem / RX, rem % RX);
@@ -361,13 +370,13 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
     auto phase_a = [&](int i, int qs, float* lgb, const TL* lgs) {
         if constexpr (SH::EARLY) {
             // every thread passed step i-1's end barrier: the buffers of step
-            // i+1 (those of step i-1) are free -- prefetch a full step ahead
-            if (tid == 0 && i + 1 < nsteps) {
+            // i+NST-1 (those of step i-1) are free -- prefetch NST-1 steps ahead
+            if (tid == 0 && i + NST - 1 < nsteps) {
                 fence_proxy_async();
-                issue_step(i + 1);
+                issue_step(i + NST - 1);
             }
         }
-        mbar_wait(&bars[i & 1], (i >> 1) & 1);
+        mbar_wait(&bars[i % NST], (i / NST) & 1);
         SSB_RT(rt_tw = clock64();)
         if (act_a) {
             float e[NLOG];
@@ -395,7 +404,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
             const float inv = rcp_fast(sum);
             convert_block(i, s_a, ri_a);  // (block i = slot sl_i)
             float* ub = ring_block(s_up, i) + s_a * RX + ri_a;
-            const float* ob = s_ob + (SH::EARLY ? (i & 1) * UPF : 0) + s_a * RX + ri_a;
+            const float* ob = s_ob + (SH::EARLY ? (i % NST) * UPF : 0) + s_a * RX + ri_a;
             float dq[3] = {1.f, 1.f, 1.f};
             if constexpr (L0) {
                 const float* dr = lin_row_step(qs, qs + s_a, 1) + ri_a;
@@ -457,10 +466,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
 
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
         const int qs = qstart + i * S;
-        float* lgb = SEP ? s_lg : s_lg + (i & 1) * LGF;  // exponentials of this step
+        float* lgb = SEP ? s_lg : s_lg + (i % NST) * LGF;  // exponentials of this step
         SSB_RT(const long long rt_t0 = clock64();)
         phase_a(i, qs, lgb,
-                reinterpret_cast<const TL*>(SEP ? s_lg + LGF + (SH::EARLY ? (i & 1) * LGS1 : 0) : lgb));
+                reinterpret_cast<const TL*>(SEP ? s_lg + LGF + (SH::EARLY ? (i % NST) * LGS1 : 0) : lgb));
         SSB_RT(const long long rt_t1 = clock64(); rt_acc[0] += rt_tw - rt_t0; rt_acc[1] += rt_t1 - rt_tw;)
         if (tid < HN) {
             // -------------------------------------------- B1: logit gradients
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
                         if (part == B1SPL - 1) {
                             // parents: pixel p takes column (gx + p + jj) / 2 (clamped): the
                             // quad reads coarse columns gx/2, gx/2 + 1, gx/2 + 2 (clamped)
-                            const float* lh = s_lhc + (i & 1) * SH::LHF;
+                            const float* lh = s_lhc + (i % NST) * SH::LHF;
                             const int cyb = qs >> 1;
                             int Xc[3];
 #pragma unroll
@@ -776,7 +785,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS>::NTH), 
                         const int Yp = P >> 1, Xp = gx2 >> 1;
                         const bool hy = 2 * Yp + 1 < H, hx = 2 * Xp + 1 < W;
                         const float rcnt = (hy && hx) ? 0.25f : ((hy || hx) ? 0.5f : 1.f);
-                        const float* t1 = s_t1 + (i & 1) * T1F + (Yp - ((qs - R) >> 1)) * CB + (Xp - cxs);
+                        const float* t1 = s_t1 + (i % NST) * T1F + (Yp - ((qs - R) >> 1)) * CB + (Xp - cxs);
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             if (c >= nc) break;

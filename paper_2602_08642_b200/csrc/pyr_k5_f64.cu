@@ -1,0 +1,7 @@
+// Pyramid filter instantiations for k = 5, f64 logits (one TU per (k, logit
+// dtype) for build parallelism).
+#include "pyr_launch.cuh"
+
+namespace ssb {
+SSB_INSTANTIATE_PYR(5, double, double)
+}  // namespace ssb

@@ -1,0 +1,7 @@
+// Pyramid filter instantiations for k = 7, bf16 logits (one TU per (k, logit
+// dtype) for build parallelism).
+#include "pyr_launch.cuh"
+
+namespace ssb {
+SSB_INSTANTIATE_PYR(7, __nv_bfloat16, float)
+}  // namespace ssb

@@ -118,9 +118,9 @@ inline bool tma_disabled() {
     return e && e[0] == '1';
 }
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4>
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0>
 bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>;
     // needs the forward output (level 0) / Lhat^l for the softmax-backward inner product
     if ((L0 && !a0.demod) || !a0.outp || tma_disabled()) return false;
     const long long plane = (long long)a0.H * a0.W;
@@ -357,15 +357,12 @@ BwdLevel bwd_level(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io
 // final g_noisy / g_demod (no coarse->fine sweep kernel).  Returns 1 without
 // launching anything if level 0 is not TMA-addressable.
 // SSB_BWD_S8=1 (experiment): the level-0 kernel with 8-row steps, 512 threads
-inline bool bwd_s8() {
-    static const bool on = [] {
-        const char* e = getenv("SSB_BWD_S8");
-        return e && e[0] == '1';
-    }();
-    return on;
+inline bool bwd_s8() {  // read per call (tests switch it in-process, like SSB_NO_TMA)
+    const char* e = getenv("SSB_BWD_S8");
+    return e && e[0] == '1';
 }
 
-template <int K, typename TL, bool TIED, int SS>
+template <int K, typename TL, bool TIED, int SS, int NST = 2, int TXO = 0>
 int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
                           void* ws, cudaStream_t s) {
     const char* tp = (const char*)tape;
@@ -375,7 +372,7 @@ int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr
     BwdLevel a0 = bwd_level<float>(d, p, io, tp, wp, 0, want, accum);
     a0.t1 = wp + p.gl_off[1];
     TmaMaps mp0;
-    if (!prepare_bwd_tma<K, TL, true, true, TIED, true, SS>(a0, mp0)) return 1;
+    if (!prepare_bwd_tma<K, TL, true, true, TIED, true, SS, NST, TXO>(a0, mp0)) return 1;
     {
         UpTransposeArgs u{};
         u.H = p.H;
@@ -407,8 +404,8 @@ int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr
         dim3 grid((p.wl[1] + 127) / 128, (p.hl[1] + 7) / 8, p.B);
         SSB_LAUNCH(s, k_pool_chain<<<grid, dim3(32, 8), 0, s>>>(c));
     }
-    using SH = TmaShape<K, TL, true, true, TIED, true, SS>;
-    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true, SS>;
+    using SH = TmaShape<K, TL, true, true, TIED, true, SS, NST, TXO>;
+    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true, SS, NST, TXO>;
     static std::atomic<unsigned long long> attr_mask{0};
     smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     const int strips = (a0.W + SH::TXB - 1) / SH::TXB;
@@ -418,11 +415,41 @@ int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr
     return cuda_check("ssb_pyr_backward");
 }
 
+// SSB_BWD0=<stages>,<own columns> (experiment): level-0 kernel ring depth and
+// strip width among the instantiated variants (0 = the default)
+inline int bwd0_variant() {
+    const char* e = getenv("SSB_BWD0");
+    if (!e) return 0;
+    int nst = 0, txo = 0;
+    if (sscanf(e, "%d,%d", &nst, &txo) < 1) return 0;
+    return nst * 1000 + txo;
+}
+
 template <int K, typename TL, bool TIED>
 int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
                        void* ws, cudaStream_t s) {
-    if constexpr (K == 5 && std::is_same<TL, float>::value)
+    if constexpr (K == 5 && std::is_same<TL, float>::value) {
         if (bwd_s8()) return run_backward_chain_ss<K, TL, TIED, 8>(d, p, io, tape, ws, s);
+#ifdef SSB_BWD_VARIANTS
+        switch (bwd0_variant()) {
+            // measured (r02, c4a bwd_l0 8.37 ms at 2,60): 3,40 10.31 ms; 3,32
+            // / 2,32 / 4,32 ~10.4-13.4 ms -- narrower strips double the
+            // barriers per pixel and the kernel is issue-bound, not ring-depth
+            // bound (profiles/r02_variants.txt)
+            case 3040: return run_backward_chain_ss<K, TL, TIED, 4, 3, 40>(d, p, io, tape, ws, s);
+            default: break;
+        }
+#endif
+    }
+    if constexpr (K == 7 && std::is_same<TL, __nv_bfloat16>::value) {
+#ifdef SSB_BWD_VARIANTS
+        switch (bwd0_variant()) {
+            // measured (r02, c3 bwd_l0 0.880 ms at 2,32): 3,32 1.222 ms (1 CTA/SM), 3,24 1.475 ms
+            case 3000: return run_backward_chain_ss<K, TL, TIED, 4, 3, 0>(d, p, io, tape, ws, s);
+            default: break;
+        }
+#endif
+    }
     return run_backward_chain_ss<K, TL, TIED, 4>(d, p, io, tape, ws, s);
 }
 
@@ -515,6 +542,14 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
     }
     return cuda_check("ssb_pyr_backward");
 }
+
+// declarations for the TUs that only call them (pyr_api.cu): no implicit
+// instantiation there -- each (k, logit dtype) is compiled once, in its own TU
+#define SSB_EXTERN_PYR(K, TL, T)                                                           \
+    extern template int run_forward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,         \
+                                              const ssb_pyr_fwd_io*, void*, cudaStream_t); \
+    extern template int run_backward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,        \
+                                               const ssb_pyr_bwd_io*, const void*, void*, cudaStream_t);
 
 #define SSB_INSTANTIATE_PYR(K, TL, T)                                                       \
     template int run_forward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,                 \

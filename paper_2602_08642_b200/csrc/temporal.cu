@@ -202,7 +202,9 @@ __global__ void k_motion_absmax(long long n, const T* __restrict__ motion, unsig
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n;
          i += (long long)gridDim.x * blockDim.x) {
         const double v = fabs((double)motion[b * 2 * n + i]);
-        m = v > m ? v : m;  // NaN motion is ignored (the reference warps it to weight 0 taps)
+        // non-finite motion is ignored: the reference gives its taps weight 0
+        // (images.py:111-116: inf/NaN positions are never `inside`)
+        m = (v > m && v < (double)INFINITY) ? v : m;
     }
     for (int o = 16; o > 0; o >>= 1) {
         const double t = __shfl_xor_sync(0xffffffffu, m, o);
@@ -211,7 +213,7 @@ __global__ void k_motion_absmax(long long n, const T* __restrict__ motion, unsig
     if ((threadIdx.x & 31) == 0) atomicMax(amax + b, (unsigned long long)__double_as_longlong(m));
 }
 
-// float32: max over the bit patterns of |m| (NaN ignored), 16-B loads when
+// float32: max over the bit patterns of |m| (inf / NaN ignored), 16-B loads when
 // the frame stride allows; stored as the double bits k_motion_absmax writes
 __global__ void k_motion_absmax_f32(long long n2, const float* __restrict__ motion, unsigned long long* amax) {
     const int b = blockIdx.y;
@@ -219,7 +221,7 @@ __global__ void k_motion_absmax_f32(long long n2, const float* __restrict__ moti
     unsigned m = 0u;
     auto take = [&](float v) {
         const unsigned a = __float_as_uint(v) & 0x7fffffffu;
-        m = max(m, a > 0x7f800000u ? 0u : a);
+        m = max(m, a >= 0x7f800000u ? 0u : a);  // inf / NaN: weight-0 taps, ignored
     };
     const long long stride = (long long)gridDim.x * blockDim.x;
     if (((reinterpret_cast<size_t>(mb)) & 15) == 0) {

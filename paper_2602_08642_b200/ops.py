@@ -138,6 +138,10 @@ def pyramid_forward(noisy, logits, demod=None, prev=None, *, ksize=None, blend="
     buf = torch.empty(max(tb.value, 1), dtype=torch.uint8, device=dev)
     if out is None:
         out = torch.empty_like(noisy)
+    else:
+        _need(out, "out", dev, noisy.dtype)
+        if out.shape != noisy.shape:
+            raise ValueError("out must match noisy's shape")
     io = _lib.PyrFwdIO()
     io.noisy, io.demod, io.prev, io.out = (_ptr(noisy), _ptr(demod), _ptr(prev), _ptr(out))
     for l, z in enumerate(logits):
@@ -153,7 +157,9 @@ def pyramid_backward(tape: PyramidTape, upstream, want_param_grads: bool = True,
     """Exact gradients of sum(upstream * out) (ref `reconstruct_backward`).
 
     accumulate_into: optional list of per-level logit-gradient tensors that
-    receive ``+=`` (frame-summed parameter gradients without an extra pass)."""
+    receive ``+=`` instead of being overwritten (e.g. summing the two frames
+    of an optimisation window without an extra pass); each must have exactly
+    its level's logits shape (B, C_l, H_l, W_l) -- per-frame accumulators."""
     lib = _lib.load()
     dev = tape.noisy.device
     _need(upstream, "upstream", dev, tape.noisy.dtype)
@@ -173,8 +179,16 @@ def pyramid_backward(tape: PyramidTape, upstream, want_param_grads: bool = True,
     g_logits = None
     if want_param_grads:
         if accumulate_into is not None:
+            # one (B, C_l, H_l, W_l) tensor per level, the logits' own shape:
+            # the kernels index it per frame (no frame-summed accumulators)
+            if len(accumulate_into) != len(tape.logits):
+                raise ValueError(f"accumulate_into needs {len(tape.logits)} tensors, got {len(accumulate_into)}")
             g_logits = [_need(g, f"accumulate_into[{l}]", dev, z.dtype)
                         for l, (g, z) in enumerate(zip(accumulate_into, tape.logits))]
+            for l, (g, z) in enumerate(zip(g_logits, tape.logits)):
+                if g.shape != z.shape:
+                    raise ValueError(f"accumulate_into[{l}] must have the logits' shape {tuple(z.shape)}, "
+                                     f"got {tuple(g.shape)}")
             io.accumulate_logits = 1
         else:
             g_logits = [torch.empty_like(z) for z in tape.logits]

@@ -37,8 +37,44 @@ def device_glogits_to_ref(glogits, ref_logits, k, temporal):
 
 
 def assert_close(got, ref, rtol, name="", atol_frac=None):
-    """rtol with an atol floor of atol_frac * max|ref|."""
+    """Per-tensor comparator: elementwise rtol with an
+    atol floor of atol_frac * max|ref| taken over THIS tensor only, plus a
+    relative-L2 bound ||got - ref|| / ||ref|| <= rtol."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     atol = (rtol if atol_frac is None else atol_frac) * max(np.abs(ref).max(initial=0.0), 1e-300)
     np.testing.assert_allclose(got, ref, rtol=rtol, atol=atol, err_msg=name)
+    nref = float(np.sqrt(np.sum(ref * ref)))
+    if nref > 0.0:
+        rel = float(np.sqrt(np.sum((got - ref) ** 2))) / nref
+        assert rel <= rtol, f"{name}: relative L2 error {rel:.3e} > {rtol:g}"
+
+
+def assert_levels_close(got_levels, ref_levels, rtol, name="g_logits", scales=None):
+    """Per-level logit-gradient parity: every level is its own tensor, so the
+    atol floor is rtol * max|ref_l| of that level (coarse-level gradients are
+    orders of magnitude below level 0's and would be unchecked by a floor
+    taken over all levels), plus the per-level relative-L2 bound.
+
+    scales (oracle `Grads.operand_scale`): per level, the magnitude of the two
+    softmax-backward operands w*gw and w*sum(w gw) whose DIFFERENCE the logit
+    gradient is.  Any float implementation errs by ~eps times that, so the
+    floor is rtol * max(max|ref_l|, scale_l).  On ordinary levels scale_l is
+    1-3x max|ref_l| (the floor is unchanged to that factor); it only matters on
+    levels whose gradient cancels analytically -- a 1x1 coarse level, where
+    all k*k taps read the same clamped pixel and the reference's own values
+    are rounding noise ~1e-16 x scale_l.  The relative-L2 bound uses the same
+    floor as its absolute term."""
+    assert len(got_levels) == len(ref_levels)
+    for l, (g, r) in enumerate(zip(got_levels, ref_levels)):
+        g = np.asarray(g, dtype=np.float64)
+        r = np.asarray(r, dtype=np.float64)
+        m = float(np.abs(r).max(initial=0.0))
+        if scales is None or scales[l] <= m:
+            assert_close(g, r, rtol, f"{name}{l}")
+            continue
+        atol = rtol * scales[l]
+        np.testing.assert_allclose(g, r, rtol=rtol, atol=atol, err_msg=f"{name}{l}")
+        err = float(np.sqrt(np.sum((g - r) ** 2)))
+        assert err <= rtol * float(np.sqrt(np.sum(r * r))) + atol * np.sqrt(r.size), \
+            f"{name}{l}: L2 error {err:.3e} (operand scale {scales[l]:.3e})"

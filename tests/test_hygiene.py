@@ -28,3 +28,13 @@ def test_ops_refuse_cpu_tensors():
     x = torch.zeros(1, 3, 8, 8)
     with pytest.raises(ValueError):
         ops.pyramid_forward(x, [torch.zeros(1, 29, 8, 8)] * 1)
+
+
+def test_package_never_reads_staged_reference():
+    """baseline/_ref (the staged reference + its tests) is a test-only fixture:
+    the product package never names it (compat.install() patches whatever
+    `sparse_sampler` the caller has importable)."""
+    for path in glob.glob(os.path.join(ROOT, "paper_2602_08642_b200", "**", "*.py"), recursive=True):
+        src = open(path).read()
+        for needle in ("baseline/_ref", "ref_tests", "/root/reference"):
+            assert needle not in src, f"{path} names {needle}"

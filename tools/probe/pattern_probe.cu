@@ -35,7 +35,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 #ifndef NTHR
 #define NTHR 256
 #endif
-constexpr int NLOG = 29, S = PS, TXB = 60, RX = 68, RA = 4, SEG = 120, CB = 36, CT = S;
+#ifndef PTXB  // own columns per strip (multiple of 4)
+#define PTXB 60
+#endif
+#ifndef PSEG
+#define PSEG 120
+#endif
+constexpr int NLOG = 29, S = PS, TXB = PTXB, RX = TXB + 8, RA = 4, SEG = PSEG, CB = ((TXB / 2 + 4 + 3) / 4) * 4, CT = S;
+constexpr int NQ = TXB / 4;
 constexpr int al32(int n) { return (n + 31) & ~31; }  // TMA destinations 128-B aligned
 constexpr int LGF = al32(NLOG * S * RX), IMF = al32(3 * S * RX), T1F = al32(3 * CT * CB);
 constexpr int STAGE = LGF + 4 * IMF + T1F;  // floats per stage
@@ -89,8 +96,8 @@ __global__ void __launch_bounds__(NTHR, MINB) k_probe(const __grid_constant__ Ma
         const float* st = sm + (i % NST) * STAGE;
         const int qs = y0 + i * S;
         // writes: 29 + 6 planes x S rows x 60 own columns as float4 (15 quads per row)
-        for (int it = tid; it < (NLOG + 6) * S * 15; it += NTHR) {  // (S rows)
-            const int q = it % 15, r = (it / 15) % S, pl = it / (15 * S);
+        for (int it = tid; it < (NLOG + 6) * S * NQ; it += NTHR) {  // (S rows)
+            const int q = it % NQ, r = (it / NQ) % S, pl = it / (NQ * S);
             const int y = qs + r, x = x0 + 4 * q;
             if (y >= y1 || x >= W) continue;
             const float* src = pl < NLOG ? st + (pl * S + r) * RX + RA + 4 * q
@@ -134,7 +141,7 @@ int main(int argc, char** argv) {
     }
     const int smem = NST * STAGE * 4;
     cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    dim3 grid(W / TXB, (H + SEG - 1) / SEG, B);
+    dim3 grid((W + TXB - 1) / TXB, (H + SEG - 1) / SEG, B);
     for (int w = 0; w < 3; ++w) k_probe<<<grid, NTHR, smem>>>(mp, H, W, gl, gx);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -149,7 +156,9 @@ int main(int argc, char** argv) {
     ms /= reps;
     // algorithmic bytes of the real kernel's pattern (own pixels): reads 29 + 12 planes + T1/4, writes 29 + 6
     const double px = (double)B * hw, bytes = px * (4.0 * (NLOG + 12) + 3.0 + 4.0 * (NLOG + 6));
-    printf("pattern probe S=%d stages=%d minb=%d threads=%d: %d frames 1080p, smem %d B/CTA, %.3f ms, %.1f B/px -> %.1f GB/s (%s)\n",
-           PS, NST, MINB, NTHR, B, smem, ms, bytes / px, bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_probe, NTHR, smem);
+    printf("pattern probe TXB=%d SEG=%d S=%d stages=%d minb=%d threads=%d (resident %d/SM): %d frames 1080p, smem %d B/CTA, %.3f ms, %.1f B/px -> %.1f GB/s (%s)\n",
+           TXB, SEG, PS, NST, MINB, NTHR, nb, B, smem, ms, bytes / px, bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
