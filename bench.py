@@ -785,6 +785,22 @@ def small_configs(peak):
                  "step_frac_of_hbm": round(frames * (fwd_b + bwd_b) / (ms * 1e-3) / 1e9 / peak, 4),
                  "kernels_ms": {kk: (round(v, 4) if v else None) for kk, v in kern.items()}}
     del noisy, demod, logits, up, r
+    out.update(latency_configs(peak))
+    return out
+
+
+def latency_configs(peak):
+    """c1 / c0: per-frame latency of a CUDA-graph replay of the inference path
+    (fused placement + demod + L3 k5 forward), with the placement alone timed
+    the same way; plus the fused training placement (relaxed, with the
+    density gradient) at 8 x 1080p as a throughput line."""
+    import ctypes as C
+
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2602_08642_b200 import ops
+    out = {}
     for name, H, W in (("c1", 1080, 1920), ("c0", 256, 256)):
         L, k = 3, 5
         dev = torch.device("cuda")
@@ -820,13 +836,41 @@ def small_configs(peak):
             infer()
         reps = 200
         ms = _time_cuda(graph.replay, steps=reps, warmup=10)
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            ops.place_fused(scores, bank, 0.25, seed=3, noisy=noisy, workspace=ws)
+        ms_p = _time_cuda(g2.replay, steps=reps, warmup=10)
         fwd_b, _, _ = algorithmic_bytes(H, W, L, k, 4, 4)
         out[name] = {"workload": f"{name}: one {W}x{H} frame, fused placement (0.25 spp) + demod + "
                                  f"3-level 5x5 forward, fp32, CUDA-graph replay",
                      "us_per_frame": round(ms * 1e3, 2),
+                     "placement_us": round(ms_p * 1e3, 2),
                      "mpix_s": round(H * W / (ms * 1e-3) / 1e6, 1),
-                     "fwd_frac_of_hbm": round((fwd_b + 19 * H * W) / (ms * 1e-3) / 1e9 / peak, 4)}
-        del graph, scores, bank, demod, logits, noisy, outb
+                     "fwd_frac_of_hbm": round((fwd_b + 19 * H * W) / (ms * 1e-3) / 1e9 / peak, 4),
+                     "placement_frac_of_hbm": round(19 * H * W / (ms_p * 1e-3) / 1e9 / peak, 4)}
+        del graph, g2, scores, bank, demod, logits, noisy, outb
+    # fused training placement: relaxed estimator + density gradient, 8 x 1080p
+    B, H, W = 8, 1080, 1920
+    g = torch.Generator(device="cuda").manual_seed(5)
+    scores = torch.randn(B, H, W, generator=g, device="cuda") * 0.5
+    bank = torch.exp(-1.0 + 1.5 * torch.randn(B, 2, 3, H, W, generator=g, device="cuda"))
+    noisy = torch.empty(B, 3, H, W, device="cuda")
+    wsb = C.c_size_t()
+    ops._lib.load().ssb_density_workspace_bytes(B, H, W, C.byref(wsb))
+    ws = torch.empty(wsb.value, dtype=torch.uint8, device="cuda")
+    res = {}
+    res["r"] = ops.place(scores, bank, 0.25, "relaxed", noisy=noisy, want_grad=True, workspace=ws)
+    gbuf = res["r"]["grad"]
+
+    def train_place():
+        ops.place(scores, bank, 0.25, "relaxed", noisy=noisy, want_grad=True, workspace=ws)
+    ms = _time_cuda(train_place, steps=20, warmup=3)
+    # scores 4 + samples read 12 E[n] (3 at 0.25 spp) + noisy 12 + grad 12
+    out["place_train"] = {"workload": "8 x 1920x1080, fused placement, relaxed estimator + density gradient "
+                                      "(the training default), fp32 out, float64 decisions",
+                          "mpix_s": round(B * H * W / (ms * 1e-3) / 1e6, 1), "ms": round(ms, 4),
+                          "frac_of_hbm": round(31 * B * H * W / (ms * 1e-3) / 1e9 / peak, 4)}
+    del scores, bank, noisy, ws, gbuf, res
     torch.cuda.empty_cache()
     return out
 

@@ -193,7 +193,7 @@ int ssb_estimate(const ssb_estimate_desc* d, const double* spp, const int64_t* b
  * (floor, u < frac) are made in float64 from the float64 spp. */
 typedef struct ssb_place_desc {
     int32_t B, H, W, capacity;
-    int32_t variant; /* stochastic rule (SSB_VAR_STOCHASTIC) only on this path */
+    int32_t variant; /* SSB_VAR_* (ssb_place_fused: SSB_VAR_STOCHASTIC only) */
     int32_t reserved;
     uint64_t seed;
     int64_t frame0;
@@ -202,6 +202,34 @@ typedef struct ssb_place_desc {
 int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* bank,
                     float* noisy, float* spp_out, uint8_t* taken_out, void* workspace,
                     ssb_stream_t stream);
+
+/* The fused placement for every stochastic estimator variant (the training
+ * default is "relaxed", optimize.py:53): normalize_density -> allocate
+ * (take_rule(variant)) -> _stochastic_estimate over a materialised bank
+ * (density.py:55-65,209-233; estimators.py:90-149), two launches (per-block
+ * (max, sum) partials of the frame softmax; one pass that finishes the
+ * partials in every CTA in a fixed order and places the samples).  Decisions
+ * are exact: u = (h >> 11) 2^-53 is compared as the integer h >> 11 against
+ * frac 2^53 (stochastic) or (1 - frac) 2^53 (relaxed) in float64, the
+ * estimator values are float64 and stored float32.  Outputs (B,3,H,W) f32
+ * planar: noisy (>= 0, required), grad = d noisy / d density (optional);
+ * (B,H,W): spp f32, taken u8 (the allocation's holdout_taken for
+ * take_rule(variant)), drawn u8 (the estimator's drawn mask), all optional.
+ * workspace: ssb_density_workspace_bytes. */
+typedef struct ssb_place_cfg {
+    double lam, gumbel_temp, density_floor; /* EstimatorConfig (estimators.py:44-59) */
+} ssb_place_cfg;
+typedef struct ssb_place_io {
+    const float* scores; /* (B,H,W) */
+    const float* bank;   /* (B,S,3,H,W): sample j of channel c at [(b*S + j)*3 + c] */
+    float* noisy;
+    float* grad;
+    float* spp;
+    uint8_t* taken;
+    uint8_t* drawn;
+} ssb_place_io;
+int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place_io* io, void* workspace,
+              ssb_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Temporal path -- replaces images.py `warp_array`

@@ -26,7 +26,7 @@ EXPORTS = (
     "ssb_pyr_workspace_bytes", "ssb_pyr_forward", "ssb_pyr_backward",
     "ssb_softmax_channels", "ssb_gather", "ssb_upsample2", "ssb_avgpool2",
     "ssb_uniform_grid", "ssb_density_workspace_bytes", "ssb_normalize_density",
-    "ssb_allocate", "ssb_stochastic_core", "ssb_estimate", "ssb_place_fused",
+    "ssb_allocate", "ssb_stochastic_core", "ssb_estimate", "ssb_place_fused", "ssb_place",
     "ssb_warp", "ssb_warp_backward_workspace_bytes", "ssb_warp_backward",
     "ssb_score_grad_workspace_bytes", "ssb_score_grad",
     "ssb_tonemap", "ssb_tonemap_backward", "ssb_losses_workspace_bytes", "ssb_losses", "ssb_epilogue",
@@ -71,6 +71,15 @@ class PlaceDesc(C.Structure):
     _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("W", C.c_int32), ("capacity", C.c_int32),
                 ("variant", C.c_int32), ("reserved", C.c_int32), ("seed", C.c_uint64),
                 ("frame0", C.c_int64), ("budget", C.c_double)]
+
+
+class PlaceCfg(C.Structure):
+    _fields_ = [("lam", C.c_double), ("gumbel_temp", C.c_double), ("density_floor", C.c_double)]
+
+
+class PlaceIO(C.Structure):
+    _fields_ = [("scores", C.c_void_p), ("bank", C.c_void_p), ("noisy", C.c_void_p), ("grad", C.c_void_p),
+                ("spp", C.c_void_p), ("taken", C.c_void_p), ("drawn", C.c_void_p)]
 
 
 class SSBError(RuntimeError):
@@ -123,6 +132,7 @@ def load(build_if_missing: bool = False):
             "ssb_stochastic_core": (C.c_int, [P(EstimateDesc)] + [vp] * 10),
             "ssb_estimate": (C.c_int, [P(EstimateDesc)] + [vp] * 11),
             "ssb_place_fused": (C.c_int, [P(PlaceDesc)] + [vp] * 7),
+            "ssb_place": (C.c_int, [P(PlaceDesc), P(PlaceCfg), P(PlaceIO), vp, vp]),
             "ssb_warp": (C.c_int, [C.c_int] * 5 + [vp] * 5),
             "ssb_warp_backward_workspace_bytes": (C.c_int, [C.c_int, P(C.c_size_t)]),
             "ssb_warp_backward": (C.c_int, [C.c_int] * 5 + [vp] * 5),

@@ -6,6 +6,7 @@
 // is compiled with -fmad=false so that elementwise results (floor/frac, u,
 // u < frac, the estimator formulas) are bit-identical to numpy's.
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -273,36 +274,314 @@ __global__ void k_density_apply(long long n, const double* scores, const double*
     }
 }
 
-// fused inference placement: scores f32 -> spp -> counts/mask -> noisy f32
-__global__ void k_place_fused(ssb_place_desc d, const float* scores, const double* fstat, const float* bank,
-                              float* noisy, float* spp_out, uint8_t* taken_out) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    const int b = blockIdx.z;
-    if (x >= d.W || y >= d.H) return;
-    const double sm = fstat[2 * b], ss = fstat[2 * b + 1];
-    const long long hw = (long long)d.H * d.W, p = (long long)y * d.W + x;
-    const double adaptive = (1.0 - 0.125) * d.budget * (double)hw;
-    const double e = exp((double)scores[b * hw + p] - sm);
-    const double spp = 0.125 * d.budget + adaptive * (e / ss);
+// ---------------------------------------------------------------- fused placement
+// Two launches per call (SURVEY.md 8(a) a1-a6 on the inference/training path):
+//  k_place_partials: per block of the frame, the (max, sum exp(v - max)) pair
+//    of its scores -- each thread folds its elements (max pass, then sum pass
+//    over the same L1-resident values), pairs combine in a fixed shuffle /
+//    warp order (deterministic);
+//  k_place: every CTA first folds the frame's partial pairs in the same fixed
+//    order (identical (m, S) in every CTA, no finish launch), then places 4
+//    horizontally adjacent pixels per thread: spp, floor/frac, the counter hash
+//    (the per-frame prefix of key_hash hoisted), the exact integer decision,
+//    the bank read (S = 2 specialised) and the estimator.
+constexpr int kPlThreads = 256;
+constexpr int kPlParts = 512;  // max partial pairs per frame
+
+// exp(d) for d <= 0 in float64, ~3 ulp (the frame softmax's terms; not the
+// compat normalize_density, which keeps libdevice exp): d = (64 n + j) ln2/64
+// + r with |r| <= ln2/128 (Cody-Waite split, the high part with 20 trailing
+// zero bits so k * hi is exact), e^r by a degree-5 polynomial (truncation
+// r^6/720 < 3.5e-17), times 2^(j/64) from a 64-entry table (correctly rounded,
+// generated with mpmath) and 2^n on the exponent bits.  d < -700 -> 0: such
+// terms are < 1e-304 of the frame maximum's.
+__device__ const double kExp2Tab[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+
+__device__ __forceinline__ void load_exp_table(double* t2) {
+    if (threadIdx.x < 64) t2[threadIdx.x] = kExp2Tab[threadIdx.x];
+}
+
+__device__ __forceinline__ double exp_neg(double d, const double* t2) {
+    if (!(d >= -700.0)) return 0.0;
+    const double kf = rint(d * 0x1.71547652b82fep+6);  // round(d * 64 / ln2)
+    const int k = (int)kf;
+    const double r = fma(-kf, 0x1.473de6af278edp-40, fma(-kf, 0x1.62e42fef00000p-7, d));
+    double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const double v = t2[k & 63] * p;
+    return __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kPlThreads) k_place_partials(long long n, const float* __restrict__ scores,
+                                                              double* __restrict__ parts, int nparts) {
+    __shared__ double t2[64];
+    __shared__ double bm;
+    load_exp_table(t2);
+    const int b = blockIdx.y;
+    const float* p = scores + (long long)b * n;
+    const long long t0 = (long long)blockIdx.x * kPlThreads + threadIdx.x, step = (long long)nparts * kPlThreads;
+    // pass 1: the block's max (a float32 value), broadcast
+    float mf = -INFINITY;
+    if constexpr (VEC) {
+        const float4* p4 = reinterpret_cast<const float4*>(p);
+        for (long long g = t0; g < (n >> 2); g += step) {
+            const float4 v = __ldg(p4 + g);
+            mf = fmaxf(fmaxf(mf, fmaxf(v.x, v.y)), fmaxf(v.z, v.w));
+        }
+    } else {
+        for (long long i = t0; i < n; i += step) mf = fmaxf(mf, p[i]);
+    }
+    const double mb = block_reduce((double)mf, true);
+    if (threadIdx.x == 0) bm = mb;
+    __syncthreads();
+    const double m = bm;
+    // pass 2: sum of exp(v - max) over the same (L1-resident) values, four chains
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    if constexpr (VEC) {
+        const float4* p4 = reinterpret_cast<const float4*>(p);
+        for (long long g = t0; g < (n >> 2); g += step) {
+            const float4 v = __ldg(p4 + g);
+            s4[0] += exp_neg((double)v.x - m, t2);
+            s4[1] += exp_neg((double)v.y - m, t2);
+            s4[2] += exp_neg((double)v.z - m, t2);
+            s4[3] += exp_neg((double)v.w - m, t2);
+        }
+    } else {
+        for (long long i = t0; i < n; i += step) s4[0] += exp_neg((double)p[i] - m, t2);
+    }
+    const double sb = block_reduce((s4[0] + s4[1]) + (s4[2] + s4[3]), false);
+    if (threadIdx.x == 0) {
+        parts[2 * ((long long)b * kPlParts + blockIdx.x)] = m;
+        parts[2 * ((long long)b * kPlParts + blockIdx.x) + 1] = sb;
+    }
+}
+
+struct PlaceArgs {
+    int B, H, W, S, variant, nparts;
+    uint64_t seed;
+    int64_t frame0;
+    double budget, lam, temp, floor_;
+    const float* scores;
+    const float* bank;
+    const double* stat;
+    float *noisy, *grad, *spp;
+    uint8_t *taken, *drawn;
+};
+
+// one pixel: the allocation decision and the estimator outputs
+struct PlacePx {
+    float noisy[3], grad[3], spp;
+    uint8_t taken, drawn;
+};
+
+template <int VAR, bool S2>
+__device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double ssum, double uni, double adaptive,
+                                            uint64_t hf, int x, int y, float score, const float* bp, long long hw,
+                                            const double* t2) {
+    PlacePx o;
+    // key_hash with the (seed, frame) prefix hoisted: rng.py:43-48
+    uint64_t h = mix64(hf ^ ((uint64_t)x * kGold + kGold));
+    h = mix64(h ^ ((uint64_t)y * kGold + kGold));
+    h = mix64(h ^ kGold);  // stream STREAM_ALLOC = 0
+    const double k53 = (double)(h >> 11);  // u = k53 * 2^-53 exactly
+    const int S = S2 ? 2 : a.S;
+    if constexpr (VAR == SSB_VAR_STOCHASTIC) {
+        // float32 fast path with a rigorous bound on |spp32 - spp64|.  The
+        // exponent x = (score - max) log2 e is carried as x_hi + x_lo (TwoSum
+        // of the difference, split product with the float log2 e and its
+        // residual), e32 = ex2.approx(x_hi) (1 + ln2 x_lo): the relative error
+        // is the MUFU's (<= 2^-22) plus a few float32 roundings, < 5e-7, and
+        // the constants / product / sum add ~2e-7 spp: err = 1.5e-6 spp + 1e-7
+        // (3x margin).  Where the floor or the decision u < frac could come out
+        // differently within err (~3e-6 of the pixels), the float64 path below
+        // decides instead.  (This TU is built with -fmad=false: TwoSum exact.)
+        const float mf = (float)m;  // the max of float32 scores: exact
+        // TwoSum(score, -mf): dh + tl == score - mf exactly
+        const float dh = score - mf;
+        const float bb = dh - score, ab = dh - bb;
+        const float tl = (score - ab) + (-mf - bb);
+        constexpr float kL2eLo = 1.925963033500011e-08f;  // log2(e) - (float)log2(e)
+        const float xh = dh * kLog2e;
+        const float xl = fmaf(dh, kLog2e, -xh) + (tl * kLog2e + dh * kL2eLo);
+        const float e32 = ex2_ftz(xh) * fmaf(0.6931471805599453f, xl, 1.0f);
+        const float spp32 = fmaf((float)adaptive, e32, (float)uni);
+        const float fl32 = floorf(spp32), fr32 = spp32 - fl32;
+        const float err = fmaf(1.5e-6f, spp32, 1e-7f);
+        const float u32 = (float)(h >> 11) * 0x1.0p-53f;  // |u32 - u| <= 6e-8
+        if (fr32 > err && fr32 < 1.0f - err && fabsf(u32 - fr32) > err + 1e-7f && spp32 < 8388608.0f) {
+            const bool tk = u32 < fr32;
+            o.taken = o.drawn = tk;
+            o.spp = a.spp ? (float)(uni + adaptive * exp_neg((double)score - m, t2)) : spp32;  // (optional output)
+            const int idx = (int)(fl32 < (float)(S - 1) ? fl32 : (float)(S - 1));
+            const float sden = spp32 > (float)a.floor_ ? spp32 : (float)a.floor_;
+            const float rs = 1.0f / sden;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float acc = 0.0f;
+                if (S2) {
+                    if (idx == 1) acc = bp[(0 * 3 + c) * hw];
+                } else {
+                    for (int j = 0; j < idx; ++j) acc += bp[(j * 3 + c) * hw];
+                }
+                if (tk) acc += bp[(idx * 3 + c) * hw];
+                const float nv = acc * rs;
+                o.noisy[c] = nv > 0.0f ? nv : 0.0f;
+                o.grad[c] = -nv * rs;
+            }
+            return o;
+        }
+    }
+    const double e = exp_neg((double)score - m, t2);
+    // density.py:63-64, spp = uni + adaptive * (e / sum); `adaptive` arrives
+    // pre-divided by the sum (one rounding apart: like the libdevice exp,
+    // ~1 ulp from numpy's spp -- the decisions below are exact given spp)
+    const double spp = uni + adaptive * e;
+    (void)ssum;
     const double fl = floor(spp);
     const double fr = spp - fl;
-    const double uv = key_uniform(d.seed, (uint64_t)(d.frame0 + b), (uint64_t)x, (uint64_t)y, 0);
-    const bool taken = uv < fr;
-    const int S = d.capacity;
     const int idx = (int)(fl < (double)(S - 1) ? fl : (double)(S - 1));
-    const double sden = spp > 1e-8 ? spp : 1e-8;
-    const double rs = 1.0 / sden;  // one division; the float32 result rounds the same to ~1 ulp
-    const float* bp = bank + (long long)b * S * 3 * hw + p;
-    for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
-        for (int j = 0; j < idx; ++j) acc += (double)bp[(j * 3 + c) * hw];
-        if (taken) acc += (double)bp[(idx * 3 + c) * hw];
-        const double nv = acc * rs;
-        noisy[(b * 3 + c) * hw + p] = (float)(nv > 0.0 ? nv : 0.0);
+    o.spp = (float)spp;
+    if constexpr (VAR == SSB_VAR_STOCHASTIC) {
+        const bool tk = k53 < fr * 0x1.0p53;  // u < frac (density.py:199)
+        o.taken = o.drawn = tk;
+        // the estimator value only feeds float32 outputs: float32 from here
+        const float sden = (float)(spp > a.floor_ ? spp : a.floor_);
+        const float rs = 1.0f / sden;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float acc = 0.0f;
+            if (S2) {
+                if (idx == 1) acc = bp[(0 * 3 + c) * hw];
+            } else {
+                for (int j = 0; j < idx; ++j) acc += bp[(j * 3 + c) * hw];
+            }
+            if (tk) acc += bp[(idx * 3 + c) * hw];
+            const float nv = acc * rs;
+            o.noisy[c] = nv > 0.0f ? nv : 0.0f;
+            o.grad[c] = -nv * rs;
+        }
+    } else {
+        const double u = k53 * 0x1.0p-53;
+        double bs[3] = {0.0, 0.0, 0.0}, ho[3];
+        for (int j = 0; j < idx; ++j)
+            for (int c = 0; c < 3; ++c) bs[c] += (double)bp[(j * 3 + c) * hw];
+        for (int c = 0; c < 3; ++c) ho[c] = (double)bp[(idx * 3 + c) * hw];
+        const CoreOut co = core_pixel(VAR, spp, fr, u, bs, ho, a.lam, a.temp, a.floor_);
+        constexpr int rule = VAR == SSB_VAR_RELAXED ? SSB_RULE_RELAXED
+                                                    : (VAR == SSB_VAR_GUMBEL ? SSB_RULE_GUMBEL : SSB_RULE_STOCHASTIC);
+        o.taken = rule == SSB_RULE_GUMBEL ? co.drawn : take_rule(rule, u, fr, a.temp);
+        o.drawn = co.drawn;
+        for (int c = 0; c < 3; ++c) {
+            o.noisy[c] = (float)(co.noisy[c] > 0.0 ? co.noisy[c] : 0.0);
+            o.grad[c] = (float)co.grad[c];
+        }
     }
-    if (spp_out) spp_out[b * hw + p] = (float)spp;
-    if (taken_out) taken_out[b * hw + p] = taken;
+    return o;
+}
+
+// the frame's (max, sum) from its partial pairs, in a fixed order: the max
+// of the partial maxima, then every partial sum rescaled by exp(m_b - max)
+// and summed; stat[2b] = max, stat[2b+1] = sum.  (Measured: folding the pairs
+// in every CTA of k_place instead costs more than this launch.)
+__global__ void __launch_bounds__(kPlThreads) k_place_finish(const double* __restrict__ parts, int nparts,
+                                                            double* __restrict__ stat) {
+    __shared__ double t2[64];
+    __shared__ double bm;
+    load_exp_table(t2);
+    const int b = blockIdx.x;
+    const double* pb = parts + 2 * (long long)b * kPlParts;
+    double m = -INFINITY;
+    for (int k = threadIdx.x; k < nparts; k += kPlThreads) m = fmax(m, pb[2 * k]);
+    const double mm = block_reduce(m, true);
+    if (threadIdx.x == 0) bm = mm;
+    __syncthreads();
+    double s = 0.0;
+    for (int k = threadIdx.x; k < nparts; k += kPlThreads) s += pb[2 * k + 1] * exp_neg(pb[2 * k] - bm, t2);
+    const double ss = block_reduce(s, false);
+    if (threadIdx.x == 0) {
+        stat[2 * b] = bm;
+        stat[2 * b + 1] = ss;
+    }
+}
+
+template <int VAR, bool S2, bool VEC>
+__global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
+    __shared__ double t2[64];
+    load_exp_table(t2);
+    __syncthreads();
+    const int b = blockIdx.y;
+    const double m = a.stat[2 * b], ssum = a.stat[2 * b + 1];
+    const long long hw = (long long)a.H * a.W;
+    const double uni = 0.125 * a.budget, adaptive = (1.0 - 0.125) * a.budget * (double)hw / ssum;
+    const uint64_t hf = mix64(mix64(a.seed + kGold) ^ ((uint64_t)(a.frame0 + b) * kGold + kGold));
+    const int S = S2 ? 2 : a.S;
+    const float* bankb = a.bank + (long long)b * S * 3 * hw;
+    constexpr int NPX = VEC ? 4 : 1;
+    const long long p0 = ((long long)blockIdx.x * kPlThreads + threadIdx.x) * NPX;
+    if (p0 >= hw) return;
+    const int y = (int)(p0 / a.W), x0 = (int)(p0 - (long long)y * a.W);
+    float sc[NPX];
+    if constexpr (VEC) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a.scores + (long long)b * hw + p0));
+        sc[0] = v.x;
+        sc[1] = v.y;
+        sc[2] = v.z;
+        sc[3] = v.w;
+    } else {
+        sc[0] = a.scores[(long long)b * hw + p0];
+    }
+    PlacePx px[NPX];
+#pragma unroll
+    for (int j = 0; j < NPX; ++j) px[j] = place_px<VAR, S2>(a, m, ssum, uni, adaptive, hf, x0 + j, y, sc[j], bankb + p0 + j, hw, t2);
+    float* nz = a.noisy + (long long)b * 3 * hw + p0;
+    float* gr = a.grad ? a.grad + (long long)b * 3 * hw + p0 : nullptr;
+    if constexpr (VEC) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            __stcs(reinterpret_cast<float4*>(nz + c * hw),
+                   make_float4(px[0].noisy[c], px[1].noisy[c], px[2].noisy[c], px[3].noisy[c]));
+            if (gr)
+                __stcs(reinterpret_cast<float4*>(gr + c * hw),
+                       make_float4(px[0].grad[c], px[1].grad[c], px[2].grad[c], px[3].grad[c]));
+        }
+        if (a.spp)
+            __stcs(reinterpret_cast<float4*>(a.spp + (long long)b * hw + p0),
+                   make_float4(px[0].spp, px[1].spp, px[2].spp, px[3].spp));
+        if (a.taken)
+            *reinterpret_cast<uchar4*>(a.taken + (long long)b * hw + p0) =
+                make_uchar4(px[0].taken, px[1].taken, px[2].taken, px[3].taken);
+        if (a.drawn)
+            *reinterpret_cast<uchar4*>(a.drawn + (long long)b * hw + p0) =
+                make_uchar4(px[0].drawn, px[1].drawn, px[2].drawn, px[3].drawn);
+    } else {
+        for (int c = 0; c < 3; ++c) {
+            nz[c * hw] = px[0].noisy[c];
+            if (gr) gr[c * hw] = px[0].grad[c];
+        }
+        if (a.spp) a.spp[(long long)b * hw + p0] = px[0].spp;
+        if (a.taken) a.taken[(long long)b * hw + p0] = px[0].taken;
+        if (a.drawn) a.drawn[(long long)b * hw + p0] = px[0].drawn;
+    }
 }
 
 // partial maxima -> frame max -> partial sums of exp(s - max) -> frame sum
@@ -343,7 +622,8 @@ int ssb_density_workspace_bytes(int B, int H, int W, size_t* bytes) {
         set_error("ssb_density_workspace_bytes: bad arguments");
         return SSB_EINVAL;
     }
-    *bytes = ((size_t)2 * B * kRedBlocks + 2 * (size_t)B) * sizeof(double);
+    // (the fused placement uses 2 x kPlParts + 2 doubles per frame of it)
+    *bytes = ((size_t)2 * B * (kRedBlocks > kPlParts ? kRedBlocks : kPlParts) + 2 * (size_t)B) * sizeof(double);
     return SSB_OK;
 }
 
@@ -430,30 +710,92 @@ int ssb_estimate(const ssb_estimate_desc* d, const double* spp, const int64_t* b
     return cuda_check("ssb_estimate");
 }
 
-int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* bank, float* noisy,
-                    float* spp_out, uint8_t* taken_out, void* workspace, ssb_stream_t stream) {
-    if (!d || !scores || !bank || !noisy || !workspace || d->B < 1 || d->H < 1 || d->W < 1 ||
+int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place_io* io, void* workspace,
+              ssb_stream_t stream) {
+    if (!d || !io || !io->scores || !io->bank || !io->noisy || !workspace || d->B < 1 || d->H < 1 || d->W < 1 ||
         d->capacity < 1) {
-        set_error("ssb_place_fused: bad arguments");
+        set_error("ssb_place: bad arguments");
         return SSB_EINVAL;
     }
-    if (d->variant != SSB_VAR_STOCHASTIC) {
-        set_error("ssb_place_fused: only the stochastic variant is fused");
-        return SSB_EUNSUPPORTED;
+    if (d->variant < SSB_VAR_STOCHASTIC || d->variant > SSB_VAR_GUMBEL) {
+        set_error("ssb_place: not a stochastic variant");
+        return SSB_EINVAL;
+    }
+    if (d->variant != SSB_VAR_STOCHASTIC && !cfg) {
+        set_error("ssb_place: the estimator config is required for this variant");
+        return SSB_EINVAL;
     }
     if (!(d->budget > 0.0)) {
         set_error("budget must be positive");
         return SSB_EINVAL;
     }
     const long long n = (long long)d->H * d->W;
-    double* pmax = (double*)workspace;
-    double* psum = pmax + (size_t)d->B * kRedBlocks;
-    double* fstat = psum + (size_t)d->B * kRedBlocks;
+    if (n >= (1ll << 31)) {
+        set_error("ssb_place: H*W must be < 2^31");
+        return SSB_EUNSUPPORTED;
+    }
     cudaStream_t s = (cudaStream_t)stream;
-    launch_reductions<float>(d->B, n, scores, pmax, psum, fstat, s);
-    dim3 block(32, 8), grid((d->W + 31) / 32, (d->H + 7) / 8, d->B);
-    SSB_LAUNCH(s, k_place_fused<<<grid, block, 0, s>>>(*d, scores, fstat, bank, noisy, spp_out, taken_out));
-    return cuda_check("ssb_place_fused");
+    const bool vec = (d->W % 4) == 0;
+    // partial pairs: ~4 float4 groups (16 scores) per thread, at most kPlParts
+    // per frame (measured: 1 group per thread and 2048 pairs is no faster)
+    const long long units = vec ? n / 4 : n;
+    long long np = (units + kPlThreads * 4 - 1) / (kPlThreads * 4);
+    np = np < 1 ? 1 : (np > kPlParts ? kPlParts : np);
+    double* parts = (double*)workspace;  // B x kPlParts x 2 doubles + B x 2 (inside the density workspace)
+    dim3 pgrid((unsigned)np, d->B);
+    if (vec) SSB_LAUNCH(s, k_place_partials<true><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np));
+    else SSB_LAUNCH(s, k_place_partials<false><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np));
+    double* stat = parts + (size_t)2 * d->B * kPlParts;
+    SSB_LAUNCH(s, k_place_finish<<<d->B, kPlThreads, 0, s>>>(parts, (int)np, stat));
+
+    PlaceArgs a{};
+    a.B = d->B;
+    a.H = d->H;
+    a.W = d->W;
+    a.S = d->capacity;
+    a.variant = d->variant;
+    a.nparts = (int)np;
+    a.seed = d->seed;
+    a.frame0 = d->frame0;
+    a.budget = d->budget;
+    a.lam = cfg ? cfg->lam : 10.0;
+    a.temp = cfg ? cfg->gumbel_temp : 1.0;
+    a.floor_ = cfg ? cfg->density_floor : 1e-8;
+    a.scores = io->scores;
+    a.bank = io->bank;
+    a.stat = stat;
+    a.noisy = io->noisy;
+    a.grad = io->grad;
+    a.spp = io->spp;
+    a.taken = io->taken;
+    a.drawn = io->drawn;
+    const long long per = vec ? 4 * kPlThreads : kPlThreads;
+    dim3 grid((unsigned)((n + per - 1) / per), d->B);
+    const bool s2 = d->capacity == 2;
+    auto go = [&](auto var_t) {
+        constexpr int V = decltype(var_t)::value;
+        if (s2 && vec) SSB_LAUNCH(s, k_place<V, true, true><<<grid, kPlThreads, 0, s>>>(a));
+        else if (s2) SSB_LAUNCH(s, k_place<V, true, false><<<grid, kPlThreads, 0, s>>>(a));
+        else if (vec) SSB_LAUNCH(s, k_place<V, false, true><<<grid, kPlThreads, 0, s>>>(a));
+        else SSB_LAUNCH(s, k_place<V, false, false><<<grid, kPlThreads, 0, s>>>(a));
+    };
+    switch (d->variant) {
+        case SSB_VAR_STOCHASTIC: go(std::integral_constant<int, SSB_VAR_STOCHASTIC>{}); break;
+        case SSB_VAR_RELAXED: go(std::integral_constant<int, SSB_VAR_RELAXED>{}); break;
+        case SSB_VAR_STRAIGHT_THROUGH: go(std::integral_constant<int, SSB_VAR_STRAIGHT_THROUGH>{}); break;
+        default: go(std::integral_constant<int, SSB_VAR_GUMBEL>{}); break;
+    }
+    return cuda_check("ssb_place");
+}
+
+int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* bank, float* noisy,
+                    float* spp_out, uint8_t* taken_out, void* workspace, ssb_stream_t stream) {
+    if (d && d->variant != SSB_VAR_STOCHASTIC) {
+        set_error("ssb_place_fused: only the stochastic variant (use ssb_place for the others)");
+        return SSB_EUNSUPPORTED;
+    }
+    ssb_place_io io{scores, bank, noisy, nullptr, spp_out, taken_out, nullptr};
+    return ssb_place(d, nullptr, &io, workspace, stream);
 }
 
 }  // extern "C"

@@ -400,31 +400,60 @@ def estimate(variant, spp, base, frac, u, samples, lam=10.0, gumbel_temp=1.0,
     return noisy, grad, contrib, used, n32
 
 
-def place_fused(scores, bank, budget: float, seed: int = 0, frame0: int = 0, noisy=None,
-                want_spp=False, want_taken=False, workspace=None):
-    """Inference placement: scores (B,H,W) f32, bank (B,S,3,H,W) f32 ->
-    noisy (B,3,H,W) f32 (sample-count-weighted radiance at the allocated counts)."""
+def place(scores, bank, budget: float, variant: str = "stochastic", seed: int = 0, frame0: int = 0,
+          lam: float = 10.0, gumbel_temp: float = 1.0, density_floor: float = 1e-8, noisy=None,
+          want_grad=False, want_spp=False, want_taken=False, want_drawn=False, workspace=None):
+    """Fused placement for any stochastic estimator variant (ref
+    normalize_density -> allocate(rule=take_rule(variant)) -> estimate over a
+    SampleBank; density.py:55-65,209-233, estimators.py:90-149):
+    scores (B,H,W) f32, bank (B,S,3,H,W) f32 -> dict with noisy (B,3,H,W) f32
+    (>= 0) and, on request, grad (d noisy / d density, (B,3,H,W) f32), spp
+    (B,H,W) f32, taken / drawn (B,H,W) u8.  Counts and masks are exact (the
+    uniforms are compared as integers against frac * 2^53)."""
     lib = _lib.load()
     _need(scores, "scores", dtype=torch.float32)
     _need(bank, "bank", scores.device, torch.float32)
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"{variant!r} is not a stochastic variant")
+    if scores.dim() != 3:
+        raise ValueError("scores must be (B, H, W)")
     B, H, W = scores.shape
     S = bank.shape[1]
-    if tuple(bank.shape) != (B, S, 3, H, W):
+    if bank.dim() != 5 or tuple(bank.shape) != (B, S, 3, H, W):
         raise ValueError("bank must be (B, S, 3, H, W)")
+    dev = scores.device
     if noisy is None:
-        noisy = torch.empty((B, 3, H, W), dtype=torch.float32, device=scores.device)
-    spp = torch.empty((B, H, W), dtype=torch.float32, device=scores.device) if want_spp else None
-    taken = torch.empty((B, H, W), dtype=torch.uint8, device=scores.device) if want_taken else None
+        noisy = torch.empty((B, 3, H, W), dtype=torch.float32, device=dev)
+    else:
+        _need(noisy, "noisy", dev, torch.float32)
+        if tuple(noisy.shape) != (B, 3, H, W):
+            raise ValueError("noisy must be (B, 3, H, W)")
+    out = {"noisy": noisy}
+    out["grad"] = torch.empty((B, 3, H, W), dtype=torch.float32, device=dev) if want_grad else None
+    out["spp"] = torch.empty((B, H, W), dtype=torch.float32, device=dev) if want_spp else None
+    out["taken"] = torch.empty((B, H, W), dtype=torch.uint8, device=dev) if want_taken else None
+    out["drawn"] = torch.empty((B, H, W), dtype=torch.uint8, device=dev) if want_drawn else None
     if workspace is None:
         wb = C.c_size_t()
         check(lib.ssb_density_workspace_bytes(B, H, W, C.byref(wb)), "ssb_density_workspace_bytes")
-        workspace = torch.empty(wb.value, dtype=torch.uint8, device=scores.device)
-    d = _lib.PlaceDesc(B, H, W, S, 0, 0, seed & (2**64 - 1), frame0, float(budget))
-    with torch.cuda.device(scores.device):
-        check(lib.ssb_place_fused(C.byref(d), _ptr(scores), _ptr(bank), _ptr(noisy), _ptr(spp),
-                                  _ptr(taken), _ptr(workspace), _stream(scores.device)),
-              "ssb_place_fused")
-    return noisy, spp, taken
+        workspace = torch.empty(wb.value, dtype=torch.uint8, device=dev)
+    d = _lib.PlaceDesc(B, H, W, S, _lib.VARIANTS[variant], 0, seed & (2**64 - 1), frame0, float(budget))
+    cfg = _lib.PlaceCfg(float(lam), float(gumbel_temp), float(density_floor))
+    io = _lib.PlaceIO(scores.data_ptr(), bank.data_ptr(), noisy.data_ptr(),
+                      *[(out[k].data_ptr() if out[k] is not None else None)
+                        for k in ("grad", "spp", "taken", "drawn")])
+    with torch.cuda.device(dev):
+        check(lib.ssb_place(C.byref(d), C.byref(cfg), C.byref(io), _ptr(workspace), _stream(dev)), "ssb_place")
+    return out
+
+
+def place_fused(scores, bank, budget: float, seed: int = 0, frame0: int = 0, noisy=None,
+                want_spp=False, want_taken=False, workspace=None):
+    """Inference placement (stochastic rule): scores (B,H,W) f32, bank
+    (B,S,3,H,W) f32 -> (noisy (B,3,H,W) f32, spp or None, taken or None)."""
+    r = place(scores, bank, budget, "stochastic", seed=seed, frame0=frame0, noisy=noisy, want_spp=want_spp,
+              want_taken=want_taken, workspace=workspace)
+    return r["noisy"], r["spp"], r["taken"]
 
 
 # ---------------------------------------------------------------------------

@@ -155,3 +155,59 @@ def test_place_fused_matches_oracle_pipeline(ops):
         nr, _, _, _ = oe.estimate("stochastic", spp_r, base, frac, u, samples)
         np.testing.assert_allclose(noisy[b].permute(1, 2, 0).cpu().numpy(), nr, rtol=1e-6,
                                    atol=1e-7)
+
+
+def _oracle_place(scores_b, bank_b, budget, variant, frame, seed, lam, temp):
+    """The reference pipeline on one frame: normalize_density -> allocate with
+    take_rule(variant) -> estimate over the materialised bank."""
+    spp_r = od.normalize_density(scores_b.astype(np.float64), budget)
+    rule = {"relaxed": "relaxed", "gumbel": "gumbel"}.get(variant, "stochastic")
+    base, frac, u, tk = od.allocate(spp_r, frame=frame, seed=seed, rule=rule, gumbel_temp=temp)
+    samples = bank_b.transpose(2, 3, 0, 1).astype(np.float64)  # (H, W, S, 3)
+    nr, gr, _, used = oe.estimate(variant, spp_r, base, frac, u, samples, lam=lam, gumbel_temp=temp)
+    drawn = used - np.minimum(base, samples.shape[2] - 1)
+    return spp_r, tk, drawn.astype(bool), nr, gr
+
+
+@pytest.mark.parametrize("variant", ["stochastic", "relaxed", "straight-through", "gumbel"])
+@pytest.mark.parametrize("h,w,S,budget", [(96, 128, 2, 0.25), (45, 70, 2, 0.5), (64, 64, 4, 1.7),
+                                          (33, 37, 3, 0.9)])
+def test_place_all_variants_vs_oracle(ops, variant, h, w, S, budget):
+    """ssb_place for every stochastic variant (the fused training path):
+    taken (take_rule(variant)) and drawn bit-exact; noisy and the density
+    gradient within fp32 rounding of the float64 reference pipeline.  Covers
+    the float4 (W % 4 == 0) and scalar paths, S = 2 specialised and general S,
+    budgets with base counts >= 1 (1.7 spp)."""
+    rng = np.random.default_rng(h * w + S)
+    B, lam, temp = 2, 7.0, 0.8
+    scores = rng.normal(0, 1, (B, h, w)).astype(np.float32)
+    bank = rng.lognormal(-1.0, 1.5, (B, S, 3, h, w)).astype(np.float32)
+    r = ops.place(cu(scores), cu(bank), budget, variant, seed=11, frame0=5, lam=lam, gumbel_temp=temp,
+                  want_grad=True, want_spp=True, want_taken=True, want_drawn=True)
+    for b in range(B):
+        spp_r, tk, dr, nr, gr = _oracle_place(scores[b], bank[b], budget, variant, 5 + b, 11, lam, temp)
+        np.testing.assert_allclose(r["spp"][b].cpu().numpy(), spp_r.astype(np.float32), rtol=1e-6)
+        np.testing.assert_array_equal(r["taken"][b].cpu().numpy().astype(bool), tk)
+        np.testing.assert_array_equal(r["drawn"][b].cpu().numpy().astype(bool), dr)
+        np.testing.assert_allclose(r["noisy"][b].permute(1, 2, 0).cpu().numpy(), np.maximum(nr, 0.0),
+                                   rtol=2e-6, atol=1e-30)
+        np.testing.assert_allclose(r["grad"][b].permute(1, 2, 0).cpu().numpy(), gr, rtol=2e-6,
+                                   atol=2e-6 * np.abs(gr).max())
+
+
+def test_place_1080p_baseline_frame_counts_exact(ops):
+    """A full BASELINE-distribution 1080p frame (GRF density, 0.25 spp): every
+    pixel's holdout decision equals the reference allocation's."""
+    import scipy.ndimage as ndi
+    rng = np.random.default_rng(21)
+    h, w = 1080, 1920
+    z = ndi.gaussian_filter(rng.normal(size=(h, w)), 8, mode="wrap")
+    z = (z - z.mean()) / z.std()
+    scores = np.log(np.log1p(np.exp(z))).astype(np.float32)[None]
+    bank = rng.lognormal(-1.0, 1.5, (1, 2, 3, h, w)).astype(np.float32)
+    r = ops.place(cu(scores), cu(bank), 0.25, "stochastic", seed=1234, frame0=3, want_taken=True)
+    spp_r, tk, _, nr, _ = _oracle_place(scores[0], bank[0], 0.25, "stochastic", 3, 1234, 10.0, 1.0)
+    got = r["taken"][0].cpu().numpy().astype(bool)
+    assert got.mean() > 0.2
+    np.testing.assert_array_equal(got, tk)
+    np.testing.assert_allclose(r["noisy"][0].permute(1, 2, 0).cpu().numpy(), nr, rtol=2e-6, atol=1e-30)
