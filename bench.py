@@ -321,31 +321,31 @@ class Runner:
 
 
 class BandRunner:
-    """c4b at N > 1: this rank owns one row band of the frame; every step
-    exchanges the halo rows with its neighbours and runs the forward on the
-    extended crop (bands.forward_distributed)."""
+    """c4b at N > 1: this rank owns one row band of the frame (bands.py):
+    halo rows of each pooled level and one Lhat row per level move over peer
+    memory (CUDA IPC + P2P stores + generation flags; no NCCL on the data
+    path), every level runs the library's level kernel on the band's
+    row-extended buffers."""
 
     fwd_only = True
 
     def __init__(self, dist, rank, world, H, W, L, k, dev):
         import torch
 
-        from paper_2602_08642_b200 import _lib, bands
-        self.lib = _lib.load()
-        self.dist, self.rank, self.world, self.H, self.k = dist, rank, world, H, k
-        b = bands.plan(H, L, k, world)[rank]
+        from paper_2602_08642_b200 import bands
+        self.bands = bands
+        pl = bands.plan(H, L, k, world)
+        self.eng = bands.BandForward(pl, rank, H, W, L, k, bands.CudaCompute(k), device=dev)
         g = torch.Generator(device=dev).manual_seed(77 + rank)
-        own = [bands.level_rows(b.own, l, H) for l in range(L)]
-        shapes = level_shapes(H, W, L)
-        self.noisy = torch.rand(1, 3, own[0][1] - own[0][0], W, generator=g, device=dev)
-        self.demod = torch.rand(1, 3, own[0][1] - own[0][0], W, generator=g, device=dev) * 0.95 + 0.05
-        self.logits = [torch.randn(1, logit_channels(l, L, k), o[1] - o[0], shapes[l][1], generator=g,
-                                   device=dev) for l, o in enumerate(own)]
+        self.eng.noisy_own.copy_(torch.rand(self.eng.noisy_own.shape, generator=g, device=dev))
+        self.eng.demod_own.copy_(torch.rand(self.eng.demod_own.shape, generator=g, device=dev) * 0.95 + 0.05)
+        for z in self.eng.logits_own:
+            z.copy_(torch.randn(z.shape, generator=g, device=dev))
+        self.tr = bands.PeerTransport(dist, self.eng, dev)
+        self.tr.setup()
 
     def step(self, stream):
-        from paper_2602_08642_b200 import bands
-        bands.forward_distributed(self.dist, self.rank, self.world, self.H, self.noisy, self.logits,
-                                  self.demod, ksize=self.k)
+        self.eng.run(self.tr)
 
 
 def chain_order():

@@ -232,6 +232,46 @@ int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place
               ssb_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * Row bands: one 8K frame split into G row bands,
+ * one per GPU, exchanging only r rows of each pooled level and one Lhat row
+ * per level with the neighbours (paper_2602_08642_b200/bands.py).  The band
+ * runs the pyramid level by level on caller-laid-out, row-extended buffers:
+ *
+ * ssb_pyr_forward_level -- one level of reconstruct_core (pyramid.py:321-338)
+ * on planar buffers of the SAME geometry (B, C, H, W) for img / demod / out
+ * and (B, C_l, H, W) for the logits: out = gather_k(img', w[:k^2]) +
+ * upsample2(coarse, w[k^2:]) with w = softmax(logits) and img' = img /
+ * max(demod, 1e-3), out *= max(demod, 1e-3) when demod != NULL (level 0);
+ * coarse (B, C, Hc, Wc), parent(y) = min((y + i) / 2, Hc - 1), NULL at the
+ * coarsest level (has_coarse = 0).  The same fused kernels as ssb_pyr_forward:
+ * every output pixel is bit-identical to the full-frame call's. */
+typedef struct ssb_pyr_level_desc {
+    int32_t batch, channels, height, width, ksize;
+    int32_t image_dtype, logit_dtype, blend_mode;
+    int32_t has_coarse, coarse_height, coarse_width;
+    int32_t reserved;
+} ssb_pyr_level_desc;
+int ssb_pyr_forward_level(const ssb_pyr_level_desc* d, const void* img, const void* demod, const void* logits,
+                          const void* coarse, void* out, ssb_stream_t stream);
+/* count-correct 2x2 pooling (pyramid.py:140-149) on strided planar views
+ * (element strides per channel plane and per batch item), demodulating on
+ * load when demod != NULL (x0 = in / max(demod, 1e-3), same strides as in):
+ * the kernel of ssb_pyr_forward's pyramid build, so bands pool bit-identically */
+int ssb_pool2_strided(int dtype, int B, int C, int H, int W, const void* in, long long in_c, long long in_b,
+                      const void* demod, void* out, long long out_c, long long out_b, ssb_stream_t stream);
+/* halo transport over peer memory (NVLink P2P stores; the destination may be
+ * another GPU's buffer mapped into this process through CUDA IPC, peer access
+ * enabled with ssb_enable_peer): copy `planes` planes of `rows` x `row_elems`
+ * elements (esz bytes each; source / destination plane pitches in elements),
+ * then a system-scope release store of `value` into *flag.  ssb_flag_wait
+ * blocks `stream` (one spinning thread, acquire loads) until *flag >= value.
+ * Generation counters make the flags reusable without resets. */
+int ssb_halo_put(void* dst, long long dst_pitch, const void* src, long long src_pitch, int planes, int rows,
+                 int row_elems, int esz, int* flag, int value, ssb_stream_t stream);
+int ssb_flag_wait(const int* flag, int value, ssb_stream_t stream);
+int ssb_enable_peer(int device, int peer);
+
+/* ------------------------------------------------------------------------
  * Temporal path -- replaces images.py `warp_array`
  * (:88-119) and `warp_backward` (:122-147).  Planar: prev/out/grad (B,C,H,W),
  * motion (B,2,H,W) = (mx, my), validity (B,H,W) (may be NULL).  dtype

@@ -30,6 +30,7 @@ EXPORTS = (
     "ssb_warp", "ssb_warp_backward_workspace_bytes", "ssb_warp_backward",
     "ssb_score_grad_workspace_bytes", "ssb_score_grad",
     "ssb_tonemap", "ssb_tonemap_backward", "ssb_losses_workspace_bytes", "ssb_losses", "ssb_epilogue",
+    "ssb_pyr_forward_level", "ssb_pool2_strided", "ssb_halo_put", "ssb_flag_wait", "ssb_enable_peer",
 )
 
 vp = C.c_void_p
@@ -71,6 +72,13 @@ class PlaceDesc(C.Structure):
     _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("W", C.c_int32), ("capacity", C.c_int32),
                 ("variant", C.c_int32), ("reserved", C.c_int32), ("seed", C.c_uint64),
                 ("frame0", C.c_int64), ("budget", C.c_double)]
+
+
+class PyrLevelDesc(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("channels", C.c_int32), ("height", C.c_int32), ("width", C.c_int32),
+                ("ksize", C.c_int32), ("image_dtype", C.c_int32), ("logit_dtype", C.c_int32),
+                ("blend_mode", C.c_int32), ("has_coarse", C.c_int32), ("coarse_height", C.c_int32),
+                ("coarse_width", C.c_int32), ("reserved", C.c_int32)]
 
 
 class PlaceCfg(C.Structure):
@@ -133,6 +141,13 @@ def load(build_if_missing: bool = False):
             "ssb_estimate": (C.c_int, [P(EstimateDesc)] + [vp] * 11),
             "ssb_place_fused": (C.c_int, [P(PlaceDesc)] + [vp] * 7),
             "ssb_place": (C.c_int, [P(PlaceDesc), P(PlaceCfg), P(PlaceIO), vp, vp]),
+            "ssb_pyr_forward_level": (C.c_int, [P(PyrLevelDesc)] + [vp] * 6),
+            "ssb_pool2_strided": (C.c_int, [C.c_int] * 5 + [vp, C.c_longlong, C.c_longlong, vp, vp,
+                                                             C.c_longlong, C.c_longlong, vp]),
+            "ssb_halo_put": (C.c_int, [vp, C.c_longlong, vp, C.c_longlong, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, vp, C.c_int, vp]),
+            "ssb_flag_wait": (C.c_int, [vp, C.c_int, vp]),
+            "ssb_enable_peer": (C.c_int, [C.c_int, C.c_int]),
             "ssb_warp": (C.c_int, [C.c_int] * 5 + [vp] * 5),
             "ssb_warp_backward_workspace_bytes": (C.c_int, [C.c_int, P(C.c_size_t)]),
             "ssb_warp_backward": (C.c_int, [C.c_int] * 5 + [vp] * 5),

@@ -337,6 +337,70 @@ int ssb_pyr_forward(const ssb_pyr_desc* d, const ssb_pyr_fwd_io* io, void* tape,
     return by_types(d, c);
 }
 
+int ssb_pyr_forward_level(const ssb_pyr_level_desc* d, const void* img, const void* demod, const void* logits,
+                          const void* coarse, void* out, ssb_stream_t stream) {
+    if (!d || !img || !logits || !out || d->batch < 1 || d->channels < 1 || d->height < 1 || d->width < 1) {
+        set_error("ssb_pyr_forward_level: bad arguments");
+        return SSB_EINVAL;
+    }
+    if (d->has_coarse && (!coarse || d->coarse_height < 1 || d->coarse_width < 1)) {
+        set_error("ssb_pyr_forward_level: has_coarse needs the coarse level and its dims");
+        return SSB_EINVAL;
+    }
+    if (d->ksize != 3 && d->ksize != 5 && d->ksize != 7) {
+        set_error("unsupported ksize");
+        return SSB_EUNSUPPORTED;
+    }
+    const bool f64 = d->image_dtype == SSB_F64;
+    if (f64 != (d->logit_dtype == SSB_F64) || (d->image_dtype != SSB_F32 && !f64)) {
+        set_error("ssb_pyr_forward_level: images f32 with f32/bf16 logits, or f64 with f64");
+        return SSB_EUNSUPPORTED;
+    }
+    if ((long long)d->channels * d->height * d->width >= (1ll << 32)) {
+        set_error("ssb_pyr_forward_level: C*H*W must be < 2^32 per frame");
+        return SSB_EUNSUPPORTED;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const void* dm = d->has_coarse ? coarse : nullptr;
+    switch (d->ksize) {
+#define LEVEL_K(KV)                                                                                          \
+    case KV:                                                                                                 \
+        if (d->logit_dtype == SSB_F32) return run_forward_level<KV, float, float>(d, img, demod, logits, dm, out, s); \
+        if (d->logit_dtype == SSB_BF16)                                                                      \
+            return run_forward_level<KV, __nv_bfloat16, float>(d, img, demod, logits, dm, out, s);          \
+        return run_forward_level<KV, double, double>(d, img, demod, logits, dm, out, s);
+        LEVEL_K(3)
+        LEVEL_K(5)
+        LEVEL_K(7)
+#undef LEVEL_K
+    }
+    return SSB_EUNSUPPORTED;
+}
+
+int ssb_pool2_strided(int dtype, int B, int C, int H, int W, const void* in, long long in_c, long long in_b,
+                      const void* demod, void* out, long long out_c, long long out_b, ssb_stream_t stream) {
+    if (B < 1 || C < 1 || H < 1 || W < 1 || !in || !out || in_c < (long long)H * W || out_c < 1) {
+        set_error("ssb_pool2_strided: bad arguments");
+        return SSB_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int c0 = 0; c0 < C; c0 += kMaxCh) {
+        const int nc = C - c0 < kMaxCh ? C - c0 : kMaxCh;
+        if (dtype == SSB_F32)
+            launch_pool<float>(B, nc, H, W, (const float*)in + c0 * in_c, in_b, in_c,
+                               demod ? (const float*)demod + c0 * in_c : nullptr, (float*)out + c0 * out_c, out_b, out_c, s);
+        else if (dtype == SSB_F64)
+            launch_pool<double>(B, nc, H, W, (const double*)in + c0 * in_c, in_b, in_c,
+                                demod ? (const double*)demod + c0 * in_c : nullptr, (double*)out + c0 * out_c, out_b,
+                                out_c, s);
+        else {
+            set_error("ssb_pool2_strided: dtype must be f32 or f64");
+            return SSB_EUNSUPPORTED;
+        }
+    }
+    return cuda_check("ssb_pool2_strided");
+}
+
 int ssb_pyr_backward(const ssb_pyr_desc* d, const ssb_pyr_bwd_io* io, const void* tape,
                      void* workspace, ssb_stream_t stream) {
     PyrPlan p;

@@ -543,18 +543,61 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
     return cuda_check("ssb_pyr_backward");
 }
 
+// one level on caller-laid-out buffers (row bands): the same dispatch as
+// run_forward, per channel group
+template <int K, typename TL, typename T>
+int run_forward_level(const ssb_pyr_level_desc* d, const void* img, const void* demod, const void* logits,
+                      const void* coarse, void* out, cudaStream_t s) {
+    const bool tied = d->blend_mode == SSB_BLEND_TIED;
+    const bool up = d->has_coarse != 0;
+    const long long e_l = (long long)d->height * d->width;
+    const long long e_c = up ? (long long)d->coarse_height * d->coarse_width : 0;
+    const int nlog = K * K + (up ? (tied ? 1 : 4) : 0);
+    for (int c0 = 0; c0 < d->channels; c0 += kMaxCh) {
+        const int nc = d->channels - c0 < kMaxCh ? d->channels - c0 : kMaxCh;
+        FwdLevel a{};
+        a.nc = nc;
+        a.H = d->height;
+        a.W = d->width;
+        a.c0 = c0;
+        a.ctot = d->channels;
+        a.batch = d->batch;
+        a.nlog = nlog;
+        a.logits = logits;
+        a.lg_b = (long long)nlog * e_l;
+        a.in_b = (long long)d->channels * e_l;
+        a.in_c = e_l;
+        a.lin = (const T*)img + (long long)c0 * e_l;
+        a.demod = demod ? (const T*)demod + (long long)c0 * e_l : nullptr;
+        a.out = (T*)out + (long long)c0 * e_l;
+        if (up) {
+            a.Hc = d->coarse_height;
+            a.Wc = d->coarse_width;
+            a.lhat_c = (const T*)coarse + (long long)c0 * e_c;
+            a.c_b = (long long)d->channels * e_c;
+            a.c_c = e_c;
+        }
+        dispatch_fwd<K, TL, T>(a, d->batch, demod != nullptr, up, tied, false, s);
+    }
+    return cuda_check("ssb_pyr_forward_level");
+}
+
 // declarations for the TUs that only call them (pyr_api.cu): no implicit
 // instantiation there -- each (k, logit dtype) is compiled once, in its own TU
 #define SSB_EXTERN_PYR(K, TL, T)                                                           \
     extern template int run_forward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,         \
                                               const ssb_pyr_fwd_io*, void*, cudaStream_t); \
     extern template int run_backward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,        \
-                                               const ssb_pyr_bwd_io*, const void*, void*, cudaStream_t);
+                                               const ssb_pyr_bwd_io*, const void*, void*, cudaStream_t); \
+    extern template int run_forward_level<K, TL, T>(const ssb_pyr_level_desc*, const void*, const void*, \
+                                                    const void*, const void*, void*, cudaStream_t);
 
 #define SSB_INSTANTIATE_PYR(K, TL, T)                                                       \
     template int run_forward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,                 \
                                        const ssb_pyr_fwd_io*, void*, cudaStream_t);         \
     template int run_backward<K, TL, T>(const ssb_pyr_desc*, const PyrPlan&,                \
-                                        const ssb_pyr_bwd_io*, const void*, void*, cudaStream_t);
+                                        const ssb_pyr_bwd_io*, const void*, void*, cudaStream_t); \
+    template int run_forward_level<K, TL, T>(const ssb_pyr_level_desc*, const void*, const void*,  \
+                                             const void*, const void*, void*, cudaStream_t);
 
 }  // namespace ssb

@@ -288,6 +288,114 @@ def build_pyramid(img, levels):
 
 
 # ---------------------------------------------------------------------------
+# row bands (bands.py): one level on caller-laid-out buffers,
+# strided pooling, and the peer-memory halo transport
+
+
+def pyramid_forward_level(img, logits, *, ksize, demod=None, coarse=None, out=None, blend="native"):
+    """One level of the coarse-to-fine reconstruction (ref pyramid.py:321-338)
+    on row-extended band buffers: img / demod / out (B, C, H, W), logits
+    (B, C_l, H, W) with C_l = k*k (+4 or +1 with a coarse level), coarse
+    (B, C, Hc, Wc) whose row min((y + i) / 2, Hc - 1) is fine row y's parent.
+    Every output pixel equals the full-frame ssb_pyr_forward's bit for bit."""
+    lib = _lib.load()
+    _need(img, "img")
+    dev = img.device
+    B, Cc, H, W = img.shape
+    _need(logits, "logits", dev)
+    nl = ksize * ksize + ((4 if blend == "native" else 1) if coarse is not None else 0)
+    if tuple(logits.shape) != (B, nl, H, W):
+        raise ValueError(f"logits must be {(B, nl, H, W)}, got {tuple(logits.shape)}")
+    if demod is not None:
+        _need(demod, "demod", dev, img.dtype)
+        if demod.shape != img.shape:
+            raise ValueError("demod must match img")
+    hc = wc = 0
+    if coarse is not None:
+        _need(coarse, "coarse", dev, img.dtype)
+        if coarse.dim() != 4 or coarse.shape[:2] != img.shape[:2]:
+            raise ValueError("coarse must be (B, C, Hc, Wc)")
+        hc, wc = coarse.shape[2], coarse.shape[3]
+    if out is None:
+        out = torch.empty_like(img)
+    else:
+        _need(out, "out", dev, img.dtype)
+        if out.shape != img.shape:
+            raise ValueError("out must match img")
+    d = _lib.PyrLevelDesc(B, Cc, H, W, ksize, _DT[img.dtype], _DT[logits.dtype],
+                          _lib.SSB_BLEND_TIED if blend == "tied" else _lib.SSB_BLEND_NATIVE,
+                          int(coarse is not None), hc, wc, 0)
+    with torch.cuda.device(dev):
+        check(lib.ssb_pyr_forward_level(C.byref(d), _ptr(img), _ptr(demod), _ptr(logits), _ptr(coarse), _ptr(out),
+                                        _stream(dev)), "ssb_pyr_forward_level")
+    return out
+
+
+def pool2_into(src, out, demod=None):
+    """Count-correct 2x2 pooling of the (possibly row-offset) view `src`
+    (B, C, H, W) into the view `out` (B, C, ceil(H/2), ceil(W/2)),
+    demodulating on load when `demod` (same strides as src) is given: the
+    pyramid build's own kernel.  Views must keep unit column stride and row
+    stride W (row slices of contiguous planar buffers)."""
+    lib = _lib.load()
+    for name, t in (("src", src), ("out", out)) + ((("demod", demod),) if demod is not None else ()):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.stride(3) != 1 or t.stride(2) != t.shape[3]:
+            raise ValueError(f"{name} must be a row slice of a contiguous planar buffer")
+    B, Cc, H, W = src.shape
+    if tuple(out.shape) != (B, Cc, (H + 1) // 2, (W + 1) // 2):
+        raise ValueError("out must be (B, C, ceil(H/2), ceil(W/2))")
+    if demod is not None and (demod.shape != src.shape or demod.stride() != src.stride()):
+        raise ValueError("demod must match src (shape and strides)")
+    with torch.cuda.device(src.device):
+        check(lib.ssb_pool2_strided(_DT[src.dtype], B, Cc, H, W, _ptr(src), src.stride(1), src.stride(0),
+                                    _ptr(demod), _ptr(out), out.stride(1), out.stride(0), _stream(src.device)),
+              "ssb_pool2_strided")
+    return out
+
+
+def halo_put(dst, src, flag=None, value=0):
+    """Copy the row block `src` (B, C, rows, W view) into `dst` (same shape;
+    may live on a peer GPU mapped through CUDA IPC) with P2P stores, then
+    publish `value` into `flag` (int32 element, possibly on the peer) with a
+    system-scope release store; stream-ordered on src's device."""
+    lib = _lib.load()
+    if dst.shape != src.shape or dst.dtype != src.dtype:
+        raise ValueError("halo_put: dst and src must match")
+    B, Cc, rows, W = src.shape
+    for name, t in (("src", src), ("dst", dst)):
+        if t.stride(3) != 1 or t.stride(2) != W or t.stride(0) != Cc * t.stride(1):
+            raise ValueError(f"halo_put: {name} must be a row slice of a contiguous planar buffer")
+    with torch.cuda.device(src.device):
+        check(lib.ssb_halo_put(_ptr(dst), dst.stride(1), _ptr(src), src.stride(1), B * Cc, rows, W,
+                               src.element_size(), _ptr(flag), int(value), _stream(src.device)), "ssb_halo_put")
+
+
+def flag_release(flag, value, device=None):
+    """Stream-ordered (on `device`'s current stream) system-scope release
+    store of `value` into `flag` (an int32 element, possibly a peer GPU's
+    mapped through CUDA IPC)."""
+    lib = _lib.load()
+    p = _ptr(flag)
+    dev = device if device is not None else torch.cuda.current_device()
+    with torch.cuda.device(dev):
+        check(lib.ssb_halo_put(p, 0, p, 0, 1, 0, 1, 4, p, int(value), _stream(dev)), "ssb_halo_put")
+
+
+def flag_wait(flag, value, device=None):
+    """Block the current stream of `device` until flag >= value."""
+    lib = _lib.load()
+    dev = device or flag.device
+    with torch.cuda.device(dev):
+        check(lib.ssb_flag_wait(_ptr(flag), int(value), _stream(dev)), "ssb_flag_wait")
+
+
+def enable_peer(device: int, peer: int):
+    check(_lib.load().ssb_enable_peer(int(device), int(peer)), "ssb_enable_peer")
+
+
+# ---------------------------------------------------------------------------
 # placement (ref rng.py, density.py, estimators.py)
 
 
