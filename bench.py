@@ -494,6 +494,54 @@ def time_e2e(dev, frames, steps, k, H, W, L, ldt, chunk=4, pool_frames=16):
     return dt, in_bytes, out_bytes
 
 
+def time_e2e_compat(frames=2, H=1080, W=1920, L=3, k=5):
+    """The drop-in caller's cost: the reference's own call
+    shapes through compat (reconstruct_core + reconstruct_backward on HWC
+    float64 numpy arrays, the reference KernelField layout with the 25-logit
+    temporal group at level 0), float32 kernels; wall clock per frame,
+    including the host<->device transfers of every float64 input and result
+    and the device-side HWC <-> planar transposes."""
+    import time
+
+    import numpy as np
+    import torch
+
+    from paper_2602_08642_b200 import compat
+    rng = np.random.default_rng(5)
+    shapes = level_shapes(H, W, L)
+    chans = [k * k + 4 + k * k] + [k * k + 4] * (L - 2) + [k * k]
+
+    class KF:  # the reference KernelField's shape (pyramid.py:56-68)
+        def __init__(self, logits):
+            self.logits = logits
+    kf = KF([rng.normal(0, 1, (h, w, c)) for (h, w), c in zip(shapes, chans)])
+    noisy = rng.lognormal(-1.0, 1.5, (H, W, 3))
+    demod = rng.uniform(0.05, 1.0, (H, W, 3))
+    up = rng.normal(size=(H, W, 3))
+    prev = compat.precision()
+    compat.set_precision("f32")
+    try:
+        def frame():
+            out, tape = compat.pyramid.reconstruct_core(noisy, kf, None, demod)
+            g = compat.pyramid.reconstruct_backward(tape, up)
+            return out, g
+        frame()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(frames):
+            frame()
+        dt = (time.perf_counter() - t0) / frames
+    finally:
+        compat.set_precision(prev)
+    h2d = 8 * (3 * H * W * 3 + sum(h * w * c for (h, w), c in zip(shapes, chans)))
+    d2h = 8 * (3 * H * W * 3 + sum(h * w * c for (h, w), c in zip(shapes, chans)))
+    return {"value": round(H * W / dt / 1e6, 3), "unit": "Mpix/s", "ms_per_frame": round(dt * 1e3, 2),
+            "h2d_bytes_per_frame": h2d, "d2h_bytes_per_frame": d2h,
+            "path": "compat.reconstruct_core + reconstruct_backward (the reference's call shapes: HWC float64 "
+                    "numpy in and out, level-0 logits with the temporal group), float32 kernels, one 1080p "
+                    "L3 k5 frame per call, wall clock"}
+
+
 def pcie_gbs(dev, nbytes=1 << 30):
     """Pinned host <-> device copy bandwidth of this box: one 1 GiB copy each
     way, then both at once on two streams (aggregate), after a warm-up -- the
@@ -696,6 +744,8 @@ def main():
                       "frac_of_pcie_ceiling": round(B * H * W / dt / 1e6 / ceil, 4)}
     else:
         res["e2e"] = None
+    if rank == 0 and world == 1 and not args.no_e2e and args.workload == "c4a":
+        res["e2e_compat"] = time_e2e_compat()
 
     if rank == 0 and world == 1 and not args.no_cpu:
         r = run_cpu(1, 1, args.workload)  # (one warm-up step: worker imports out of the timing)

@@ -51,17 +51,20 @@ def device() -> torch.device:
 
 
 def to_planar(a, dt=None) -> torch.Tensor:
-    """(H, W, C) array -> (1, C, H, W) device tensor."""
+    """(H, W, C) array -> (1, C, H, W) device tensor.  The caller's array is
+    copied to the device as it lies (one contiguous H2D copy) and transposed /
+    cast there -- no host-side transpose of the reference's HWC float64."""
     a = np.asarray(a, dtype=np.float64)
     if a.ndim == 2:
         a = a[:, :, None]
-    t = torch.from_numpy(np.ascontiguousarray(a.transpose(2, 0, 1))[None])
-    return t.to(device=device(), dtype=dt or dtype()).contiguous()
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(device=device(), non_blocking=False)
+    return t.permute(2, 0, 1).to(dtype=dt or dtype()).contiguous()[None]
 
 
 def to_hwc(t: torch.Tensor) -> np.ndarray:
-    """(1, C, H, W) device tensor -> (H, W, C) float64 array."""
-    return t[0].permute(1, 2, 0).to(torch.float64).cpu().numpy()
+    """(1, C, H, W) device tensor -> (H, W, C) float64 array (transposed and
+    widened on the device, one contiguous D2H copy)."""
+    return t[0].permute(1, 2, 0).to(torch.float64).contiguous().cpu().numpy()
 
 
 def to_dev(a, dt=torch.float64) -> torch.Tensor:

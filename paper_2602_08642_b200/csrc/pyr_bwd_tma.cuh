@@ -464,7 +464,8 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         else win[k >> 1][c].x += v;
     };
 
-    for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1) {
+    int su_i = 0;  // upstream-ring slot of step i (i mod NBU), kept incrementally
+    for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1, su_i = (su_i + 1 == NBU) ? 0 : su_i + 1) {
         const int qs = qstart + i * S;
         float* lgb = SEP ? s_lg : s_lg + (i % NST) * LGF;  // exponentials of this step
         SSB_RT(const long long rt_t0 = clock64();)
@@ -718,6 +719,27 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             }
             // block of S window rows starting at compile-time kb: reduce-scatter
             // across the B2SPL lanes of the column, each lane writes S/B2SPL rows
+            // window row J (compile-time) = image row qs - R + J: its image-ring
+            // block / row and upstream-ring block / row are compile-time offsets
+            // from this step's slots (no per-row division / modulo)
+            auto lin_base_j = [&](auto j_t) -> const float* {
+                constexpr int J = decltype(j_t)::value;
+                constexpr int REL = J - 2 * R + NPRO * S;
+                static_assert(REL >= 0, "window row above the image ring");
+                int slt = sl_i + (REL / S - NPRO);
+                slt += slt < 0 ? NBL : 0;
+                slt -= slt >= NBL ? NBL : 0;
+                return s_lin + slt * BLKF + (REL % S) * RX + ri2;
+            };
+            auto up_base_j = [&](auto j_t) -> const float* {
+                constexpr int J = decltype(j_t)::value;
+                constexpr int RELU = J - R + S;
+                static_assert(RELU >= 0, "window row above the upstream ring");
+                int slt = su_i + (RELU / S - 1);
+                slt += slt < 0 ? NBU : 0;
+                slt -= slt >= NBU ? NBU : 0;
+                return s_up + slt * UPF + (RELU % S) * RX + ri2;
+            };
             auto flush_block = [&](auto kb_t) {
                 constexpr int KB = decltype(kb_t)::value;
                 constexpr int PB = KB / 2;  // first pair (KB even)
@@ -768,6 +790,19 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                     }
                 }
                 if (!act2) return;
+                // the block's 4 window rows KB .. KB+3: ring pointers (compile-time
+                // offsets), selected per written row below
+                const float* lb4[4] = {lin_base_j(std::integral_constant<int, KB>{}),
+                                       lin_base_j(std::integral_constant<int, KB + 1>{}),
+                                       lin_base_j(std::integral_constant<int, KB + 2>{}),
+                                       lin_base_j(std::integral_constant<int, KB + 3>{})};
+                const float* ub4[4] = {up_base_j(std::integral_constant<int, KB>{}),
+                                       up_base_j(std::integral_constant<int, KB + 1>{}),
+                                       up_base_j(std::integral_constant<int, KB + 2>{}),
+                                       up_base_j(std::integral_constant<int, KB + 3>{})};
+                auto sel4 = [](const float* const* a, int k) {
+                    return k == 0 ? a[0] : (k == 1 ? a[1] : (k == 2 ? a[2] : a[3]));
+                };
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     if (r >= nrow) break;
@@ -779,13 +814,17 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         // T1(parent) / (children of the parent), joins the
                         // level-0 input gradient; g_d masked by d > floor
                         // (pyramid.py:415-421, 436-447)
-                        const float* xr = lin_row_step(qs, P, 0) + ri2;
-                        const float* dr = lin_row_step(qs, P, 1) + ri2;
-                        const float* uor = ring_row(s_up, P) + ri2;  // u * out
+                        // (B2SPL = 4: one row per lane -- the generic row lookup is
+                        // cheaper than selecting among the block's four)
+                        const int kk = krow - KB + r;  // 0..3
+                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2;
+                        const float* dr = xr + DEMOFF;
+                        const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2;  // u * out
                         const int Yp = P >> 1, Xp = gx2 >> 1;
                         const bool hy = 2 * Yp + 1 < H, hx = 2 * Xp + 1 < W;
                         const float rcnt = (hy && hx) ? 0.25f : ((hy || hx) ? 0.5f : 1.f);
-                        const float* t1 = s_t1 + (i % NST) * T1F + (Yp - ((qs - R) >> 1)) * CB + (Xp - cxs);
+                        // T1 row of parent Yp: window row J -> (J + (R & 1)) >> 1
+                        const float* t1 = s_t1 + (i % NST) * T1F + ((KB + kk + (R & 1)) >> 1) * CB + (Xp - cxs);
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             if (c >= nc) break;
@@ -797,9 +836,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                             if (gdo) __stcs(gdo + o, d > (float)kDemodFloor ? (uor[c * PL] - v * xr[c * PL]) * rd : 0.f);
                         }
                     } else if constexpr (L0) {
-                        const float* xr = lin_row_step(qs, P, 0) + ri2;
-                        const float* dr = lin_row_step(qs, P, 1) + ri2;
-                        const float* uor = ring_row(s_up, P) + ri2;  // u * out
+                        const int kk = krow - KB + r;
+                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2;
+                        const float* dr = xr + DEMOFF;
+                        const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2;  // u * out
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             if (c >= nc) break;
