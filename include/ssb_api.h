@@ -276,11 +276,13 @@ int ssb_enable_peer(int device, int peer);
  * (:88-119) and `warp_backward` (:122-147).  Planar: prev/out/grad (B,C,H,W),
  * motion (B,2,H,W) = (mx, my), validity (B,H,W) (may be NULL).  dtype
  * SSB_F32 | SSB_F64.  The transpose is a deterministic gather in the
- * reference's summation order (float64: bit-exact); workspace: B x 8 bytes.
+ * reference's summation order (float64: bit-exact) for any motion: frames with
+ * max |motion| + 1 > 16 take an O(HW) segment-candidate path instead of the
+ * per-pixel scan; workspace: ssb_warp_backward_workspace_bytes(B, H, W).
  * ---------------------------------------------------------------------- */
 int ssb_warp(int dtype, int B, int C, int H, int W, const void* prev, const void* motion,
              void* out, void* validity, ssb_stream_t stream);
-int ssb_warp_backward_workspace_bytes(int B, size_t* bytes);
+int ssb_warp_backward_workspace_bytes(int B, int H, int W, size_t* bytes);
 int ssb_warp_backward(int dtype, int B, int C, int H, int W, const void* grad_out,
                       const void* motion, void* grad_prev, void* workspace, ssb_stream_t stream);
 

@@ -151,7 +151,7 @@ def load(build_if_missing: bool = False):
             "ssb_flag_wait": (C.c_int, [vp, C.c_int, vp]),
             "ssb_enable_peer": (C.c_int, [C.c_int, C.c_int]),
             "ssb_warp": (C.c_int, [C.c_int] * 5 + [vp] * 5),
-            "ssb_warp_backward_workspace_bytes": (C.c_int, [C.c_int, P(C.c_size_t)]),
+            "ssb_warp_backward_workspace_bytes": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_size_t)]),
             "ssb_warp_backward": (C.c_int, [C.c_int] * 5 + [vp] * 5),
             "ssb_score_grad_workspace_bytes": (C.c_int, [C.c_int] * 3 + [P(C.c_size_t)]),
             "ssb_score_grad": (C.c_int, [C.c_int] * 6 + [vp, vp, vp, C.c_double, C.c_double,

@@ -12,6 +12,7 @@
 // run-to-run identical.  Compiled with -fmad=false (products and sums rounded
 // like numpy; the float32 kernels use explicit FMAs where they want them).
 #include <math.h>
+#include <climits>
 #include <string>
 
 #include "common.cuh"
@@ -248,6 +249,7 @@ __global__ void k_motion_absmax_f32(long long n2, const float* __restrict__ moti
 // sources from shared memory, one pass per tap, sources in raster order --
 // the np.add.at order (bit-exact).
 constexpr int WT_X = 32, WT_Y = 8, WMAX = 6;
+constexpr int SCAN_MR = 16;  // per-pixel source scans up to this radius; beyond: k_warp_backward_seg
 constexpr int WM_MR = 4;  // float32 frames with MR <= WM_MR: k_warp_backward_mask
 constexpr int WWX = WT_X + 2 * WMAX, WWY = WT_Y + 2 * WMAX;
 
@@ -530,8 +532,9 @@ __global__ void __launch_bounds__(256) k_warp_backward_mask(int C, int H, int W,
         warp_bwd_mask_body<1>(sm, C, H, W, b, tx0, ty0, gout, motion, gprev);
     } else if (mm <= 3.0) {
         warp_bwd_mask_body<2>(sm, C, H, W, b, tx0, ty0, gout, motion, gprev);
-    } else {  // large (or non-finite) motion: general scan
-        const int MR = (int)fmin(ceil(mm) + 1.0, (double)(H > W ? H : W));
+    } else {  // larger motion: general scan up to SCAN_MR (beyond: k_warp_backward_seg)
+        const int MR = (int)ceil(mm) + 1;
+        if (MR > SCAN_MR) return;
         for (int h = 0; h < WM_Y / 8; ++h) {
             const int x = tx0 + (threadIdx.x & 31), y = ty0 + (threadIdx.x >> 5) + 8 * h;
             if (x < W && y < H) warp_backward_scan<float>(C, H, W, b, x, y, MR, gout, motion, gprev);
@@ -572,7 +575,8 @@ __device__ void warp_backward_scan(int C, int H, int W, int b, int x, int y, int
     }
 }
 
-// float64 frames whose max |motion| exceeds WMAX - 1
+// float64 frames whose max |motion| exceeds WMAX - 1 (up to SCAN_MR: beyond,
+// k_warp_backward_seg)
 template <typename T>
 __global__ void k_warp_backward(int C, int H, int W, const T* __restrict__ gout,
                                 const T* __restrict__ motion, const unsigned long long* __restrict__ amax,
@@ -584,8 +588,135 @@ __global__ void k_warp_backward(int C, int H, int W, const T* __restrict__ gout,
     const double mm = __longlong_as_double((long long)amax[b]);
     if ((int)ceil(mm) + 1 <= WMAX) return;  // handled by the tiled kernel
     // sources farther than ceil(max|m|) + 1 cannot land on this pixel
-    const int MR = (int)fmin(ceil(mm) + 1.0, (double)(H > W ? H : W));
+    const int MR = (int)ceil(mm) + 1;
+    if (MR > SCAN_MR) return;  // large motion: k_warp_backward_seg
     warp_backward_scan<T>(C, H, W, b, x, y, MR, gout, motion, gprev);
+}
+
+// Large motion (max |motion| + 1 > SCAN_MR), any dtype: O(HW) candidates
+// instead of a (2 MR + 1)^2 scan per pixel (one outlier vector no longer turns
+// every pixel's scan frame-wide).  Sources are taken in segments of SEG
+// pixels of one row; k_warp_seg_bbox records the bounding box of each
+// segment's in-frame, non-zero-weight landing cells; every 32 x 8 target tile
+// then walks the segments in raster order (chunks of 256 tested at once and
+// compacted in order), stages each intersecting segment's landings for tap k
+// in shared memory and adds the matching ones -- tap-major, sources in raster
+// order: the np.add.at order of images.py:140-146 (float64 bit-exact).
+constexpr int SEG = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_warp_seg_bbox(int H, int W, const T* __restrict__ motion,
+                                                       const unsigned long long* __restrict__ amax,
+                                                       int4* __restrict__ bbox, int nseg) {
+    const int b = blockIdx.y;
+    const double mm = __longlong_as_double((long long)amax[b]);
+    if ((int)ceil(mm) + 1 <= SCAN_MR) return;
+    const int wid = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (wid >= H * nseg) return;  // warp-uniform
+    const int y = wid / nseg, sx = (wid - y * nseg) * SEG + lane;
+    int x0 = INT_MAX, x1 = INT_MIN, y0 = INT_MAX, y1 = INT_MIN;
+    if (sx < W) {
+        const long long hw = (long long)H * W, q = (long long)y * W + sx;
+        const T mx = motion[(b * 2 + 0) * hw + q], my = motion[(b * 2 + 1) * hw + q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            T w;
+            int ix, iy;
+            warp_tap(k, sx, y, W, H, mx, my, w, ix, iy);
+            if (w != (T)0) {
+                x0 = min(x0, ix);
+                x1 = max(x1, ix);
+                y0 = min(y0, iy);
+                y1 = max(y1, iy);
+            }
+        }
+    }
+    x0 = __reduce_min_sync(0xffffffffu, x0);
+    x1 = __reduce_max_sync(0xffffffffu, x1);
+    y0 = __reduce_min_sync(0xffffffffu, y0);
+    y1 = __reduce_max_sync(0xffffffffu, y1);
+    if (lane == 0) bbox[(long long)b * H * nseg + wid] = make_int4(x0, x1, y0, y1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_warp_backward_seg(int C, int H, int W, const T* __restrict__ gout,
+                                                           const T* __restrict__ motion,
+                                                           const int4* __restrict__ bbox, int nseg,
+                                                           const unsigned long long* __restrict__ amax,
+                                                           T* __restrict__ gprev) {
+    const int b = blockIdx.z;
+    const double mm = __longlong_as_double((long long)amax[b]);
+    if ((int)ceil(mm) + 1 <= SCAN_MR) return;  // block-uniform
+    constexpr int CG = 4;
+    __shared__ int s_cand[256];
+    __shared__ int s_wc[8];
+    __shared__ int s_ix[SEG], s_iy[SEG];
+    __shared__ T s_w[SEG];
+    __shared__ T s_gv[CG][SEG];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tx0 = blockIdx.x * 32, ty0 = blockIdx.y * 8;
+    const int x = tx0 + lane, y = ty0 + warp;
+    const long long hw = (long long)H * W;
+    const long long total = (long long)H * nseg;
+    const int4* bb = bbox + (long long)b * total;
+    for (int c0 = 0; c0 < C; c0 += CG) {
+        const int nc = min(CG, C - c0);
+        T acc[CG];
+#pragma unroll
+        for (int c = 0; c < CG; ++c) acc[c] = (T)0;
+        for (int k = 0; k < 4; ++k) {
+            for (long long s0 = 0; s0 < total; s0 += 256) {
+                // segments of this chunk whose landing box meets the tile, in order
+                bool hit = false;
+                if (s0 + tid < total) {
+                    const int4 r = bb[s0 + tid];
+                    hit = r.x <= tx0 + 31 && r.y >= tx0 && r.z <= ty0 + 7 && r.w >= ty0;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (lane == 0) s_wc[warp] = __popc(m);
+                __syncthreads();
+                int off = 0, n = 0;
+#pragma unroll
+                for (int w2 = 0; w2 < 8; ++w2) {
+                    off += w2 < warp ? s_wc[w2] : 0;
+                    n += s_wc[w2];
+                }
+                if (hit) s_cand[off + __popc(m & ((1u << lane) - 1u))] = (int)(s0 + tid);
+                __syncthreads();
+                for (int j = 0; j < n; ++j) {
+                    const int seg = s_cand[j];
+                    const int sy = seg / nseg, sx = (seg - sy * nseg) * SEG + tid;
+                    if (tid < SEG) {
+                        T w = (T)0;
+                        int ix = -1, iy = -1;
+                        if (sx < W) {
+                            const long long q = (long long)sy * W + sx;
+                            warp_tap(k, sx, sy, W, H, motion[(b * 2 + 0) * hw + q], motion[(b * 2 + 1) * hw + q], w,
+                                     ix, iy);
+                            if (w != (T)0)
+                                for (int c = 0; c < nc; ++c) s_gv[c][tid] = gout[((long long)b * C + c0 + c) * hw + q];
+                        }
+                        s_w[tid] = w;
+                        s_ix[tid] = ix;
+                        s_iy[tid] = iy;
+                    }
+                    __syncthreads();
+                    if (x < W && y < H) {
+                        for (int jj = 0; jj < SEG; ++jj) {
+                            if (s_w[jj] != (T)0 && s_ix[jj] == x && s_iy[jj] == y) {
+#pragma unroll
+                                for (int c = 0; c < CG; ++c)
+                                    if (c < nc) acc[c] = acc[c] + s_w[jj] * s_gv[c][jj];
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+        if (x < W && y < H)
+            for (int c = 0; c < nc; ++c) gprev[((long long)b * C + c0 + c) * hw + (long long)y * W + x] = acc[c];
+    }
 }
 
 }  // namespace ssb
@@ -624,12 +755,15 @@ int ssb_warp(int dtype, int B, int C, int H, int W, const void* prev, const void
     return cuda_check("ssb_warp");
 }
 
-int ssb_warp_backward_workspace_bytes(int B, size_t* bytes) {
-    if (B <= 0 || !bytes) {
+int ssb_warp_backward_workspace_bytes(int B, int H, int W, size_t* bytes) {
+    if (B <= 0 || H <= 0 || W <= 0 || !bytes) {
         set_error("ssb_warp_backward_workspace_bytes: invalid arguments");
         return SSB_EINVAL;
     }
-    *bytes = (size_t)B * sizeof(unsigned long long);
+    // per frame: max |motion| (8 B), then the segment landing boxes (16 B
+    // each) of the large-motion path
+    const size_t nseg = (size_t)(W + SEG - 1) / SEG;
+    *bytes = (((size_t)B * sizeof(unsigned long long) + 15) & ~(size_t)15) + (size_t)B * H * nseg * sizeof(int4);
     return 0;
 }
 
@@ -669,6 +803,22 @@ int ssb_warp_backward(int dtype, int B, int C, int H, int W, const void* grad_ou
         smem_attr_once(attr_mask, (const void*)k_warp_backward_mask, (int)sizeof(MaskSmem));
         SSB_LAUNCH(s, k_warp_backward_mask<<<mgrid, 256, sizeof(MaskSmem), s>>>(C, H, W, (const float*)grad_out,
                                                                  (const float*)motion, amax, (float*)grad_prev));
+    }
+    // large motion (frames with max |motion| + 1 > SCAN_MR; the kernels exit
+    // at once for the others)
+    const int nseg = (W + SEG - 1) / SEG;
+    int4* bbox = (int4*)((char*)workspace + (((size_t)B * sizeof(unsigned long long) + 15) & ~(size_t)15));
+    dim3 bgrid((unsigned)(((long long)H * nseg + 7) / 8), B);
+    if (dtype == SSB_F64) {
+        SSB_LAUNCH(s, k_warp_seg_bbox<double><<<bgrid, 256, 0, s>>>(H, W, (const double*)motion, amax, bbox, nseg));
+        SSB_LAUNCH(s, k_warp_backward_seg<double><<<grid, 256, 0, s>>>(C, H, W, (const double*)grad_out,
+                                                                     (const double*)motion, bbox, nseg, amax,
+                                                                     (double*)grad_prev));
+    } else {
+        SSB_LAUNCH(s, k_warp_seg_bbox<float><<<bgrid, 256, 0, s>>>(H, W, (const float*)motion, amax, bbox, nseg));
+        SSB_LAUNCH(s, k_warp_backward_seg<float><<<grid, 256, 0, s>>>(C, H, W, (const float*)grad_out,
+                                                                    (const float*)motion, bbox, nseg, amax,
+                                                                    (float*)grad_prev));
     }
     return cuda_check("ssb_warp_backward");
 }

@@ -606,7 +606,7 @@ def warp_backward(grad_out, motion):
         raise ValueError("warp: image and motion dimensions must match")
     B, Cc, H, W = grad_out.shape
     wb = C.c_size_t()
-    check(lib.ssb_warp_backward_workspace_bytes(B, C.byref(wb)), "ssb_warp_backward_workspace_bytes")
+    check(lib.ssb_warp_backward_workspace_bytes(B, H, W, C.byref(wb)), "ssb_warp_backward_workspace_bytes")
     ws = torch.empty(wb.value, dtype=torch.uint8, device=grad_out.device)
     gp = torch.empty_like(grad_out)
     with torch.cuda.device(grad_out.device):

@@ -188,3 +188,37 @@ def test_score_grad_sums_to_zero(ops):
     g = ops.score_grad(sc, gi, gd, 0.25, 1.5)
     tot = g.abs().sum(dim=(1, 2))
     assert torch.all(g.sum(dim=(1, 2)).abs() <= 1e-9 * tot)
+
+
+@pytest.mark.parametrize("case", ["outlier", "pan", "nonfinite", "chaos"])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_warp_backward_large_motion(ops, case, precision):
+    """max |motion| + 1 > 16 takes the O(HW) segment-candidate path (ADVICE
+    r01: one 64-px vector, or an inf, used to turn every pixel's source scan
+    frame-wide): float64 bit-exact to the reference's np.add.at order, float32
+    within 1e-5; infinite motion lands nowhere, as in the reference."""
+    rng = np.random.default_rng(len(case))
+    h, w = 70, 150
+    m = rng.uniform(-2, 2, (h, w, 2))
+    if case == "outlier":
+        m[33, 71] = (64.3, -20.7)
+        m[5, 140] = (-139.5, 60.25)
+    elif case == "pan":
+        m += np.array([37.25, -19.5])
+    elif case == "nonfinite":
+        m[10, 10] = (np.inf, 0.5)  # (NaN motion makes the reference itself raise: not an input)
+        m[40, 100] = (3.0, -np.inf)
+        m[1, 2] = (25.0, 3.0)
+    else:
+        m = rng.uniform(-80, 80, (h, w, 2))
+    g = rng.normal(size=(h, w, 3))
+    if precision == "f32":
+        m = m.astype(np.float32).astype(np.float64)
+        g = g.astype(np.float32).astype(np.float64)
+    ref = ot.warp_backward(g, m)
+    dt = torch.float64 if precision == "f64" else torch.float32
+    gp = hwc(ops.warp_backward(planar(g, dt), planar(m, dt)))
+    if precision == "f64":
+        np.testing.assert_array_equal(gp, ref)
+    else:
+        np.testing.assert_allclose(gp, ref, rtol=1e-5, atol=1e-5 * np.abs(ref).max())
