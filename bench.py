@@ -811,7 +811,51 @@ def also_measurements():
     del noisy, demod, logits, up, r
     torch.cuda.empty_cache()
     out.update(small_configs(peak))
+    out.update(call_shapes(peak))
     out.update(next_rows(peak))
+    return out
+
+
+def call_shapes(peak, frames=4, H=1080, W=1920, L=3, k=5):
+    """The reference's other call shapes of the filter, fwd+bwd
+    at 4 x 1080p L3 k5 fp32: frame 1 of optimize.evaluate_step (the 25-tap
+    temporal group over the warped history, optimize.py:209), reconstruct_core's
+    default demod=None, and C = 12 batched draws (optimize.py:433-437).  Bytes
+    per 8(d) with the history terms (prev read in fwd, prev + g_prev in bwd,
+    k*k more level-0 logits)."""
+    import torch
+
+    from paper_2602_08642_b200 import ops
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(11)
+    shapes = level_shapes(H, W, L)
+    out = {}
+    for name, C, hist, dem in (("history", 3, True, True), ("no_demod", 3, False, False), ("draws_c12", 12, False, True)):
+        noisy = torch.rand(frames, C, H, W, generator=g, device=dev)
+        demod = (torch.rand(frames, C, H, W, generator=g, device=dev) * 0.95 + 0.05) if dem else None
+        prev = torch.rand(frames, C, H, W, generator=g, device=dev) if hist else None
+        logits = [torch.randn(frames, ops.logit_channels(l, L, k, has_prev=hist and l == 0), h, w, generator=g,
+                              device=dev) for l, (h, w) in enumerate(shapes)]
+        up = torch.randn(frames, C, H, W, generator=g, device=dev)
+
+        def step():
+            o, t = ops.pyramid_forward(noisy, logits, demod, prev, ksize=k)
+            ops.pyramid_backward(t, up)
+        ms = _time_cuda(step, steps=10, warmup=3)
+        img = 4 * C
+        lg = sum(a * b * ops.logit_channels(l, L, k, has_prev=hist and l == 0) for l, (a, b) in enumerate(shapes))
+        n0 = H * W
+        fwd = n0 * img * ((3 if dem else 2) + (1 if hist else 0)) + lg * 4
+        bwd = n0 * img * ((6 if dem else 4) + (2 if hist else 0)) + lg * 8
+        out[f"shape_{name}"] = {
+            "workload": f"{frames} x 1920x1080 L3 k5 fp32 fwd+bwd, " + {
+                "history": "with the temporal group over a warped history (evaluate_step frame 1)",
+                "no_demod": "demod=None (reconstruct_core's default)",
+                "draws_c12": "C = 12 (4 batched draws sharing the kernels)"}[name],
+            "mpix_s": round(frames * n0 / (ms * 1e-3) / 1e6, 1), "ms_per_step": round(ms, 4),
+            "frac_of_hbm": round(frames * (fwd + bwd) / (ms * 1e-3) / 1e9 / peak, 4)}
+        del noisy, demod, prev, logits, up
+        torch.cuda.empty_cache()
     return out
 
 

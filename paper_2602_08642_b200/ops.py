@@ -14,6 +14,7 @@ stream.  There is no eager/PyTorch fallback for any op in this module.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -104,6 +105,7 @@ class PyramidTape:
     demod: torch.Tensor | None
     prev: torch.Tensor | None
     out: torch.Tensor
+    demod_given: bool = True  # False: demod is the identity stand-in below
 
     @property
     def levels(self) -> int:
@@ -116,6 +118,24 @@ class PyramidGrads:
     demod: torch.Tensor | None
     input: torch.Tensor
     prev: torch.Tensor | None
+
+
+_IDENTITY_DEMOD: dict = {}
+
+
+def _identity_demod(noisy):
+    """demod=None (reconstruct_core's default) on the float32 3-channel path
+    runs the fused demodulating level kernels (TMA pipeline, level-0-last
+    backward) with an all-ones demod: max(1, 1e-3) = 1 and rcp(1) = 1 exactly,
+    so outputs and input gradients are those of the undemodulated filter; the
+    ones are allocated once per shape and device (SSB_NO_IDENTITY_DEMOD=1 keeps
+    the generic no-demod kernels)."""
+    key = (noisy.device, tuple(noisy.shape))
+    t = _IDENTITY_DEMOD.get(key)
+    if t is None:
+        t = torch.ones(noisy.shape, dtype=torch.float32, device=noisy.device)
+        _IDENTITY_DEMOD[key] = t
+    return t
 
 
 def pyramid_forward(noisy, logits, demod=None, prev=None, *, ksize=None, blend="native",
@@ -132,6 +152,10 @@ def pyramid_forward(noisy, logits, demod=None, prev=None, *, ksize=None, blend="
             _need(t, name, dev, noisy.dtype)
             if t.shape != noisy.shape:
                 raise ValueError(f"{name} must match noisy's shape")
+    demod_given = demod is not None
+    if (demod is None and prev is None and noisy.dtype == torch.float32 and noisy.shape[1] == 3
+            and len(logits) >= 2 and os.environ.get("SSB_NO_IDENTITY_DEMOD") != "1"):
+        demod = _identity_demod(noisy)
     d = _desc(noisy, logits, demod, prev, ksize, blend)
     tb = C.c_size_t()
     check(lib.ssb_pyr_tape_bytes(C.byref(d), C.byref(tb)), "ssb_pyr_tape_bytes")
@@ -149,7 +173,7 @@ def pyramid_forward(noisy, logits, demod=None, prev=None, *, ksize=None, blend="
     with torch.cuda.device(dev):
         check(lib.ssb_pyr_forward(C.byref(d), C.byref(io), _ptr(buf), _stream(dev)),
               "ssb_pyr_forward")
-    return out, PyramidTape(d, buf, noisy, logits, demod, prev, out)
+    return out, PyramidTape(d, buf, noisy, logits, demod, prev, out, demod_given)
 
 
 def pyramid_backward(tape: PyramidTape, upstream, want_param_grads: bool = True,
@@ -170,7 +194,8 @@ def pyramid_backward(tape: PyramidTape, upstream, want_param_grads: bool = True,
     check(lib.ssb_pyr_workspace_bytes(C.byref(d), C.byref(wb)), "ssb_pyr_workspace_bytes")
     ws = torch.empty(max(wb.value, 1), dtype=torch.uint8, device=dev)
     g_noisy = torch.empty_like(tape.noisy)
-    g_demod = torch.empty_like(tape.noisy) if (want_param_grads and tape.demod is not None) else None
+    g_demod = (torch.empty_like(tape.noisy)
+               if (want_param_grads and tape.demod is not None and tape.demod_given) else None)
     g_prev = torch.empty_like(tape.noisy) if tape.prev is not None else None
     io = _lib.PyrBwdIO()
     io.noisy, io.demod, io.prev = _ptr(tape.noisy), _ptr(tape.demod), _ptr(tape.prev)

@@ -424,3 +424,34 @@ def test_s8_level0_backward_matches_s4(ops, monkeypatch, H, W):
     monkeypatch.delenv("SSB_BWD_S8")
     for a_, b_ in [(g8.input, g4.input), (g8.demod, g4.demod)] + list(zip(g8.logits, g4.logits)):
         assert (a_ - b_).abs().max().item() <= 1e-5 * b_.abs().max().item()
+
+
+@pytest.mark.parametrize("h,w,L,k,ldt", [(96, 128, 3, 5, torch.float32), (72, 128, 4, 7, torch.bfloat16),
+                                         (45, 70, 3, 5, torch.float32)])
+def test_no_demod_identity_path(ops, monkeypatch, h, w, L, k, ldt):
+    """demod=None (reconstruct_core's default) runs the fused demodulating
+    kernels with an identity demod: against the oracle without demod, and
+    against the generic no-demod kernels (SSB_NO_IDENTITY_DEMOD=1)."""
+    rng = np.random.default_rng(h + w)
+    logits32 = op.random_logits(h, w, L, k, rng, temporal=False)
+    lg = [hwc_to_planar(z, torch.float32).to(ldt) for z in logits32]
+    logits = [planar_to_hwc(z) for z in lg]  # the device values (bf16-rounded)
+    noisy = rng.lognormal(-1.0, 1.5, (h, w, 3)).astype(np.float32).astype(np.float64)
+    up = rng.normal(size=(h, w, 3)).astype(np.float32).astype(np.float64)
+    out_r, tape = op.forward(noisy, logits, None, None, k=k)
+    g_r = op.backward(tape, up)
+    rtol = 1e-5 if ldt == torch.float32 else 2e-2
+    res = []
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("SSB_NO_IDENTITY_DEMOD", "1")
+        out, t = ops.pyramid_forward(hwc_to_planar(noisy, torch.float32), lg, None, ksize=k)
+        g = ops.pyramid_backward(t, hwc_to_planar(up, torch.float32))
+        monkeypatch.delenv("SSB_NO_IDENTITY_DEMOD", raising=False)
+        assert g.demod is None
+        assert_close(planar_to_hwc(out), out_r, rtol, "out")
+        assert_close(planar_to_hwc(g.input), g_r.input, rtol, "g_input")
+        assert_levels_close([planar_to_hwc(z) for z in g.logits], g_r.logits, rtol, scales=g_r.operand_scale)
+        res.append((out, g))
+    (o1, g1), (o2, g2) = res
+    assert (o1 - o2).abs().max().item() <= 2e-5 * o2.abs().max().item()
