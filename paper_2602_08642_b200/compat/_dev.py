@@ -63,8 +63,13 @@ def to_planar(a, dt=None) -> torch.Tensor:
 
 def to_hwc(t: torch.Tensor) -> np.ndarray:
     """(1, C, H, W) device tensor -> (H, W, C) float64 array (transposed and
-    widened on the device, one contiguous D2H copy)."""
-    return t[0].permute(1, 2, 0).to(torch.float64).contiguous().cpu().numpy()
+    widened on the device, one contiguous D2H copy into page-locked memory
+    from torch's caching host allocator: fresh pageable arrays cost a page
+    fault per 4 KB on first touch -- measured 2.3 GB/s against ~25 GB/s)."""
+    d = t[0].permute(1, 2, 0).to(torch.float64).contiguous()
+    h = torch.empty(d.shape, dtype=torch.float64, pin_memory=True)
+    h.copy_(d)
+    return h.numpy()
 
 
 def to_dev(a, dt=torch.float64) -> torch.Tensor:

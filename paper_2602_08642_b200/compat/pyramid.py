@@ -159,7 +159,10 @@ def reconstruct_core(noisy: np.ndarray, kf, prev_warped: np.ndarray | None = Non
         if l == 0:
             if z.shape[-1] < need:
                 raise ValueError("level-0 logits lack the temporal group")
-            z = z[:, :, :need]
+            # the unread temporal group is dropped on the device: the caller's
+            # contiguous array crosses PCIe as it lies (no host-side copy)
+            dev_logits.append(_dev.to_planar(z)[:, :need].contiguous())
+            continue
         elif z.shape[-1] != need:
             raise ValueError(f"level {l} logits must carry {need} channels")
         dev_logits.append(_dev.to_planar(z))
@@ -192,12 +195,13 @@ def reconstruct_backward(tape: ReconTape, upstream: np.ndarray,
     if want_param_grads:
         glogits = []
         for l, gz in enumerate(g.logits):
-            a = _dev.to_hwc(gz)
-            if a.shape[-1] != tape.ref_channels[l]:
-                full = np.zeros(a.shape[:2] + (tape.ref_channels[l],))
-                full[:, :, :a.shape[-1]] = a
-                a = full
-            glogits.append(a)
+            if gz.shape[1] != tape.ref_channels[l]:
+                # the reference layout's (zero) temporal gradients, padded on the device
+                full = torch.zeros((1, tape.ref_channels[l]) + tuple(gz.shape[2:]), dtype=gz.dtype,
+                                   device=gz.device)
+                full[:, :gz.shape[1]] = gz
+                gz = full
+            glogits.append(_dev.to_hwc(gz))
     gdemod = _dev.to_hwc(g.demod) if g.demod is not None else None
     gprev = _dev.to_hwc(g.prev) if g.prev is not None else None
     return _types.make("PyramidGrads", logits=glogits, demod=gdemod, input=_dev.to_hwc(g.input),
