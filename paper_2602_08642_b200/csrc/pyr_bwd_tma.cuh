@@ -76,7 +76,12 @@ struct TmaShape {
     static constexpr int NI = L0 ? 2 : 1;              // image planes per block (x0 [, demod])
     // B1: S * NQUAD pixel quads on warps 0-3; tap rows split in B1SPL warp-uniform parts
     static constexpr int NB1 = S * NQUAD;
-    static constexpr int B1SPL = NB1 <= HN / 4 ? 4 : (NB1 <= HN / 2 ? 2 : 1);
+    // quads of a row occupy QS = 8 or 16 consecutive lanes (one idle slot at
+    // 15 quads): a 16-B shared access's 8-lane phase never straddles two rows,
+    // whose 272-B pitch would put two lanes of the phase on the same banks
+    static constexpr int QS = NQUAD <= 8 ? 8 : 16;
+    static constexpr int NB1S = S * QS;
+    static constexpr int B1SPL = NB1S <= HN / 4 ? 4 : (NB1S <= HN / 2 ? 2 : 1);
     static constexpr int B1ITEMS = HN / B1SPL;
     static constexpr int DYS = (K + B1SPL - 1) / B1SPL;  // tap rows per part
     // B2: TXB columns x B2SPL tap-column groups on warps 4-7 (adjacent lanes)
@@ -126,7 +131,7 @@ struct TmaShape {
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
     static constexpr int MINB = (SS == 4 && 2 * (SMEM + 1024) <= 233472) ? 2 : 1;
-    static_assert(NB1 <= B1ITEMS, "B1 pixel pairs exceed warps 0-3");
+    static_assert(NB1S <= B1ITEMS && NQUAD <= QS, "B1 pixel quads exceed warps 0-3");
     // the upsample-tap gradients follow the last part's tap rows (t = NT)
     static_assert(!UP || (B1SPL - 1) * DYS < K, "last B1 part must own the last tap row");
     static_assert(TXB * B2SPL <= HN && 3 * TXC <= HN && TXB % 4 == 0, "B2/B3 items exceed their warps");
@@ -440,7 +445,8 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     int cnext = qstart >> 1;
     const int part = B1SPL == 1 ? 0 : (tid % HN) / SH::B1ITEMS;
     const int item = (tid % HN) - part * SH::B1ITEMS;
-    const int s = item / NQUAD, xi = 4 * (item - s * NQUAD), ri = xi + RA;
+    const int s = item / SH::QS, xi = 4 * (item % SH::QS), ri = xi + RA;
+    const bool act_b1 = item < SH::NB1S && (item % SH::QS) < NQUAD;
     // B2 role (warps 4-7)
     const int b2 = tid % HN;
     const int col = b2 / B2SPL, part2 = b2 - col * B2SPL;
@@ -477,7 +483,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             const int qy = qs + s, gx = x0 + xi;
             // W is a multiple of 4 on this path: the quad (gx .. gx + 3) is in
             // the image and 16-B aligned in every gradient plane
-            if (want && item < SH::NB1 && qy >= y0 && qy < y1 && gx < W) {
+            if (want && act_b1 && qy >= y0 && qy < y1 && gx < W) {
                 float g[4][3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 }
                 const float4 inn4 = *reinterpret_cast<const float4*>(s_inn + s * RX + ri);
                 const float inn[4] = {inn4.x, inn4.y, inn4.z, inn4.w};
-                const float* ep = lgb + s * RXE + ri - ESH;
+                const float* ep = static_cast<const float*>(__builtin_assume_aligned(lgb + s * RXE + ri - ESH, 16));
                 auto body = [&](auto acc_t) {
                     constexpr bool ACC = decltype(acc_t)::value;
                     constexpr int OFF = 4 - R;  // window value m = x(ri - 4 + m); pixel p, tap d -> m = p + d + OFF
@@ -497,7 +503,8 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                     TL* gp = (TL*)a.glogits + (long long)b * a.lg_b + ((unsigned)qy * (unsigned)W + (unsigned)gx) +
                              (size_t)t_first * hw32;
                     auto tap_row = [&](int dy) {
-                        const float* xr = lin_row_step(qs, qy + dy, 0) + ri - 4;
+                        const float* xr =
+                            static_cast<const float*>(__builtin_assume_aligned(lin_row_step(qs, qy + dy, 0) + ri - 4, 16));
                         // accumulators start at -inner': g_logit_t = e_t * (gw_t - inner')
                         float gw[4][K];
 #pragma unroll
@@ -746,6 +753,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 float2 keep[3];             // rows of this lane (pair or one component)
                 int krow;                   // first window row this lane writes
                 int nrow;                   // rows this lane writes (1 or 2 or 4)
+                int rstep = 1;              // window-row stride between them
                 float vout[4][3];
                 if constexpr (B2SPL == 1) {
 #pragma unroll
@@ -754,6 +762,26 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         for (int c = 0; c < 3; ++c) vout[r][c] = wget(KB + r, c);
                     krow = KB;
                     nrow = 4;
+                } else if constexpr (B2SPL == 2) {
+                    // the two lanes of a column split the block's rows even / odd
+                    // (rows 0, 2 | 1, 3): the rows a lane pair then reads in the
+                    // ring are 1 row (272 B = 16 banks) apart, not 2 (same banks)
+                    const bool odd = (part2 & 1) != 0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float2 lo = PB < NPW ? win[PB][c] : make_float2(0.f, 0.f);
+                        const float2 hi = PB + 1 < NPW ? win[PB + 1][c] : make_float2(0.f, 0.f);
+                        const float2 send = odd ? make_float2(lo.x, hi.x) : make_float2(lo.y, hi.y);
+                        float2 recv;
+                        recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+                        recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+                        keep[c] = fadd2(odd ? make_float2(lo.y, hi.y) : make_float2(lo.x, hi.x), recv);
+                        vout[0][c] = keep[c].x;
+                        vout[1][c] = keep[c].y;
+                    }
+                    krow = KB + (odd ? 1 : 0);
+                    nrow = 2;
+                    rstep = 2;
                 } else {
                     // round 1: halves (pairs PB, PB+1) between lanes part ^ (B2SPL/2)
                     const int hm = B2SPL / 2;
@@ -768,15 +796,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         recv.y = __shfl_xor_sync(0xffffffffu, send.y, hm);
                         keep[c] = fadd2(upper ? hi : lo, recv);
                     }
-                    if constexpr (B2SPL == 2) {
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            vout[0][c] = keep[c].x;
-                            vout[1][c] = keep[c].y;
-                        }
-                        krow = KB + (upper ? 2 : 0);
-                        nrow = 2;
-                    } else {
+                    {
                         // round 2: components between lanes part ^ 1
                         const bool odd = (part2 & 1) != 0;
 #pragma unroll
@@ -806,7 +826,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     if (r >= nrow) break;
-                    const int P = qs - R + krow + r;
+                    const int P = qs - R + krow + r * rstep;
                     if (P < y0 || P >= y1 || P > H - 1) continue;
                     const unsigned off = (unsigned)P * (unsigned)W + (unsigned)gx2;
                     if constexpr (L0 && CH) {
@@ -816,7 +836,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         // (pyramid.py:415-421, 436-447)
                         // (B2SPL = 4: one row per lane -- the generic row lookup is
                         // cheaper than selecting among the block's four)
-                        const int kk = krow - KB + r;  // 0..3
+                        const int kk = krow - KB + r * rstep;  // 0..3
                         const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2;
                         const float* dr = xr + DEMOFF;
                         const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2;  // u * out
@@ -836,7 +856,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                             if (gdo) __stcs(gdo + o, d > (float)kDemodFloor ? (uor[c * PL] - v * xr[c * PL]) * rd : 0.f);
                         }
                     } else if constexpr (L0) {
-                        const int kk = krow - KB + r;
+                        const int kk = krow - KB + r * rstep;
                         const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2;
                         const float* dr = xr + DEMOFF;
                         const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2;  // u * out
