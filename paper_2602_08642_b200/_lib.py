@@ -25,7 +25,7 @@ EXPORTS = (
     "ssb_pyr_logit_channels", "ssb_pyr_level_dims", "ssb_pyr_tape_bytes",
     "ssb_pyr_workspace_bytes", "ssb_pyr_forward", "ssb_pyr_backward",
     "ssb_softmax_channels", "ssb_gather", "ssb_upsample2", "ssb_avgpool2",
-    "ssb_uniform_grid", "ssb_density_workspace_bytes", "ssb_normalize_density",
+    "ssb_uniform_grid", "ssb_uniform_at", "ssb_density_workspace_bytes", "ssb_normalize_density",
     "ssb_allocate", "ssb_stochastic_core", "ssb_estimate", "ssb_place_fused", "ssb_place",
     "ssb_warp", "ssb_warp_backward_workspace_bytes", "ssb_warp_backward",
     "ssb_score_grad_workspace_bytes", "ssb_score_grad",
@@ -135,6 +135,7 @@ def load(build_if_missing: bool = False):
             "ssb_avgpool2": (C.c_int, [C.c_int] * 5 + [vp, vp, vp]),
             "ssb_uniform_grid": (C.c_int, [C.c_uint64, C.c_int64, vp, C.c_int, C.c_int, C.c_int,
                                            C.c_uint64, vp, vp]),
+            "ssb_uniform_at": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, vp, vp]),
             "ssb_density_workspace_bytes": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_size_t)]),
             "ssb_normalize_density": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.c_double, vp,
                                                 vp, vp]),

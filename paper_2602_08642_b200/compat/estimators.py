@@ -78,7 +78,11 @@ def estimate_gumbel(density, alloc, bank, cfg=None):
 
 
 def estimate(variant: str, density, alloc, bank, cfg, ref=None):
-    """ref :188-196"""
+    """ref :188-196.  The deterministic-rounding estimator (a prior-work
+    baseline outside the hot path, estimators.py:171-185) is NOT run on the
+    GPU: installed into the reference it is forwarded to the reference's own
+    CPU function (documented behaviour); standalone it
+    raises NotImplementedError."""
     if variant == "deterministic":
         if ref is None:
             raise ValueError("deterministic estimator needs a reference image")

@@ -38,6 +38,6 @@ def uniform_grid_batch(seed: int, frames, width: int, height: int, stream: int) 
 
 
 def pixel_uniform(key: PixelRngKey) -> float:
-    g = ops.uniform_grid(int(key.seed), key.y + 1, key.x + 1, frame0=int(key.frame),
-                         stream_id=int(key.stream), device=_dev.device())
-    return float(g[0, key.y, key.x].item())
+    """One variate (ref rng.py:51-54): a single-thread launch, not a grid."""
+    return float(ops.uniform_at(int(key.seed), int(key.frame), int(key.x), int(key.y), int(key.stream),
+                                device=_dev.device()).item())

@@ -50,6 +50,11 @@ __global__ void k_uniform_grid(uint64_t seed, int64_t frame0, const int64_t* fra
     u[((long long)b * H + y) * W + x] = key_uniform(seed, f, (uint64_t)x, (uint64_t)y, stream);
 }
 
+// one variate (rng.pixel_uniform): a single thread, no grid
+__global__ void k_uniform_at(uint64_t seed, int64_t frame, int64_t x, int64_t y, uint64_t stream, double* u) {
+    *u = key_uniform(seed, (uint64_t)frame, (uint64_t)x, (uint64_t)y, stream);
+}
+
 // ---------------------------------------------------------------- estimator math
 constexpr double kGateFloor = 1e-4;
 constexpr double kLogitClamp = 1e-6;
@@ -615,6 +620,16 @@ int ssb_uniform_grid(uint64_t seed, int64_t frame0, const int64_t* frames, int B
     dim3 block(32, 8), grid((W + 31) / 32, (H + 7) / 8, B);
     SSB_LAUNCH((cudaStream_t)stream, k_uniform_grid<<<grid, block, 0, (cudaStream_t)stream>>>(seed, frame0, frames, H, W, stream_id, u));
     return cuda_check("ssb_uniform_grid");
+}
+
+int ssb_uniform_at(uint64_t seed, int64_t frame, int64_t x, int64_t y, uint64_t stream_id, double* u,
+                   ssb_stream_t stream) {
+    if (!u || x < 0 || y < 0) {
+        set_error("ssb_uniform_at: null output or negative coordinate");
+        return SSB_EINVAL;
+    }
+    SSB_LAUNCH((cudaStream_t)stream, k_uniform_at<<<1, 1, 0, (cudaStream_t)stream>>>(seed, frame, x, y, stream_id, u));
+    return cuda_check("ssb_uniform_at");
 }
 
 int ssb_density_workspace_bytes(int B, int H, int W, size_t* bytes) {

@@ -440,6 +440,18 @@ def uniform_grid(seed: int, height: int, width: int, frame0: int = 0, batch: int
     return u
 
 
+def uniform_at(seed: int, frame: int, x: int, y: int, stream_id: int = 0, device="cuda"):
+    """One variate u(seed, frame, x, y, stream) (ref rng.pixel_uniform): a
+    one-element float64 device tensor."""
+    lib = _lib.load()
+    dev = torch.device(device)
+    u = torch.empty((1,), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib.ssb_uniform_at(seed & (2**64 - 1), int(frame), int(x), int(y), stream_id & (2**64 - 1), _ptr(u),
+                                 _stream(dev)), "ssb_uniform_at")
+    return u
+
+
 def normalize_density(scores, budget: float):
     lib = _lib.load()
     _need(scores, "scores", dtype=torch.float64)
