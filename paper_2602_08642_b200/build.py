@@ -21,7 +21,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIBDIR = os.path.join(PKG, "lib")
+# (SSB_BUILD_DIR: experiment builds elsewhere, e.g. for same-box A/B via SSB_LIB_PATH)
+LIBDIR = os.environ.get("SSB_BUILD_DIR") or os.path.join(PKG, "lib")
 OBJDIR = os.path.join(LIBDIR, "obj")
 LIB = os.path.join(LIBDIR, "libssb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -37,10 +37,10 @@ namespace ssb {
 
 struct TmaMaps {
     CUtensorMap lg;   // logits (W, H, NLOG, B), box (RX, S, NLOG)
-    CUtensorMap lin;  // noisy (level 0) or L^l, box (RX, S, 3)
-    CUtensorMap dem;  // demod (level 0), box (RX, S, 3)
-    CUtensorMap up;   // upstream (level 0) or ghat^l, box (RX, S, 3)
-    CUtensorMap out;  // forward output (level 0) or Lhat^l, box (RX, S, 3)
+    CUtensorMap lin;  // noisy (level 0) or L^l, box (RXI, S, 3)
+    CUtensorMap dem;  // demod (level 0), box (RXI, S, 3)
+    CUtensorMap up;   // upstream (level 0) or ghat^l, box (RXI, S, 3)
+    CUtensorMap out;  // forward output (level 0) or Lhat^l, box (RXI, S, 3)
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
     CUtensorMap t1;   // CH (level 0 last): T1 = level-1 input gradient incl. the pool chain, box (CB, CT, 3)
 };
@@ -68,6 +68,10 @@ struct TmaShape {
     static constexpr int TXW = ((64 - 2 * R) / RA) * RA;
     static constexpr int TXB = TXO ? TXO : (K >= 7 ? 32 : TXW), RX = TXB + 2 * RA, RW = TXB + 2 * R;
     static constexpr int TXC = TXB / 2, NQUAD = TXB / 4;
+    // fp32 image boxes need only 16 B = 4 columns of alignment halo: image
+    // rows are RXI = TXB + 8 wide from global x0 - 4, so image column =
+    // logit column - DI (bf16: DI = 4, fp32: 0)
+    static constexpr int RAI = 4, DI = RA - RAI, RXI = TXB + 2 * RAI;
     static constexpr int NPRO = (2 * R + S - 1) / S;  // image-ring blocks above step 0
     static constexpr int NBL = NPRO + NST;             // image-ring blocks (incl. prefetch)
     // upstream ring (level 0: the flush needs u * out, R rows behind); other
@@ -86,6 +90,19 @@ struct TmaShape {
     static constexpr int DYS = (K + B1SPL - 1) / B1SPL;  // tap rows per part
     // B2: TXB columns x B2SPL tap-column groups on warps 4-7 (adjacent lanes)
     static constexpr int B2SPL = TXB * 4 <= HN ? 4 : (TXB * 2 <= HN ? 2 : 1);
+    // B2W: each tap-column group (part) on its own warp(s) -- 32 consecutive
+    // columns per warp, so the parts' shared loads (exponentials of different
+    // tap planes) cannot collide on banks -- and the parts' window partials
+    // summed through shared memory at the flush (each part owns rows r with
+    // r % B2SPL == part) instead of lane shuffles
+#ifndef SSB_B2W
+#define SSB_B2W 1
+#endif
+    // (measured, same-box A/B: k7 bf16 level 0 -13%, k5 level 1 -4%; k5 level
+    // 0, whose two parts split the 5 tap columns 3:2, +3..7% -- kept on shuffles)
+    static constexpr bool B2W = SSB_B2W && SS == 4 && (B2SPL == 4 || (B2SPL == 2 && !L0));
+    static constexpr int WPP = B2W ? 4 / B2SPL : 1;  // warps per part (the 4 B2 warps)
+    static constexpr int B2C = 32 * WPP;              // column slots per part
     static constexpr int AW = S + 2 * R, NPW = (AW + 1) / 2;  // output-row window (float2 pairs)
     // coarse box: 16-B aligned start (x0/2 rounded down to 4), TXC + 1 + 3 cols
     static constexpr int CR = 4, CB = ((TXB / 2 + 4 + 3) / 4) * 4, CROWS = S / 2 + 1;
@@ -97,13 +114,19 @@ struct TmaShape {
     static constexpr int ESH = SEP ? RA - 4 : 0;
     static constexpr int RXE = SEP ? ((TXB + R + 4 + 3) / 4) * 4 : RX;
     static constexpr int EPL = S * RXE;                // floats per exponential plane
+    static_assert(ESH == DI && RXE == RXI, "exponential and image columns coincide");
+    // phase A: pixel (row s, region column rw) on thread s * PV + rw -- PV =
+    // the image / exponential row pitch when S of them fit the CTA, so every
+    // warp's shared accesses are one contiguous run (no bank conflicts where
+    // a warp straddles two rows); else dense (PV = RW)
+    static constexpr int PV = S * RXI <= NTH ? RXI : RW;
     static constexpr int LGF = al32(NLOG * EPL);       // floats per exponentials buffer
     // logits staging (storage type): fp32 = the two exponential buffers
     // themselves (in place); bf16 = staging box(es) + one fp32 buffer
     static constexpr int LGS1 = SEP ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
-    static constexpr int DEMOFF = al32(3 * S * RX);    // demod plane offset inside a ring block
+    static constexpr int DEMOFF = al32(3 * S * RXI);   // demod plane offset inside a ring block
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
-    static constexpr int UPF = al32(3 * S * RX);       // floats per upstream / output block
+    static constexpr int UPF = al32(3 * S * RXI);      // floats per upstream / output block
     static constexpr int LHF = UP ? al32(3 * CROWS * CB) : 0;
     // coarse rows of the flushed fine rows (bottom step: the AW window rows from
     // qs - R; qs is even, so the first coarse row is aligned when R is even)
@@ -121,13 +144,14 @@ struct TmaShape {
     static constexpr int LGS = EARLY ? NST * LGS1 : LGS1;  // staging floats (all boxes)
     static constexpr int LGBUF = SEP ? LGF + LGS : NST * LGF;
     // transaction bytes (exact box sizes, not the padded buffer sizes)
-    static constexpr uint32_t TX_IMG = 3 * S * RX * 4;
+    static constexpr uint32_t TX_IMG = 3 * S * RXI * 4;
     static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
                                         (CH ? 3 * CT * CB * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr int NBU = L0 ? NBU0 : (EARLY ? 2 : 1);
+    static constexpr int REDF = B2W ? al32(4 * (B2SPL - 1) * 3 * B2C) : 0;  // B2W partial rows
     static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F +
-                                     3 * S * RX + S * RX + (B3ON ? CR * 3 * TXC : 0);
+                                     3 * S * RXI + S * RXI + (B3ON ? CR * 3 * TXC : 0) + REDF;
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
     static constexpr int MINB = (SS == 4 && 2 * (SMEM + 1024) <= 233472) ? 2 : 1;
@@ -135,7 +159,7 @@ struct TmaShape {
     // the upsample-tap gradients follow the last part's tap rows (t = NT)
     static_assert(!UP || (B1SPL - 1) * DYS < K, "last B1 part must own the last tap row");
     static_assert(TXB * B2SPL <= HN && 3 * TXC <= HN && TXB % 4 == 0, "B2/B3 items exceed their warps");
-    static_assert(S * RW <= NTH && RW <= 64, "phase A items exceed the CTA");
+    static_assert(S * PV <= NTH && RW <= 64, "phase A items exceed the CTA");
     static_assert((S == 4 || S == 8) && (32 % B2SPL) == 0 && NST >= 2 && NST <= 4 && TXB % RA == 0, "step geometry");
     static_assert(!(UP && !CH) || S == 4, "the B3 coarse-row ring (CR = 4) assumes 4-row steps");
     static_assert(SMEM + 1024 <= 233472 / MINB, "CTAs per SM");
@@ -232,32 +256,35 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     constexpr bool B3ON = SH::B3ON;
     constexpr int CT = SH::CT, T1F = SH::T1F;
     constexpr bool SEP = SH::SEP;
-    constexpr int R = SH::R, NT = SH::NT, NLOG = SH::NLOG, S = SH::S, RX = SH::RX;
+    constexpr int R = SH::R, NT = SH::NT, NLOG = SH::NLOG, S = SH::S, RX = SH::RX, RXI = SH::RXI, DI = SH::DI;
     constexpr int RA = SH::RA, RW = SH::RW, NQUAD = SH::NQUAD;
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
     constexpr int NI = SH::NI, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
     constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF;
     constexpr int EPL = SH::EPL, RXE = SH::RXE, ESH = SH::ESH, LGS1 = SH::LGS1;
     constexpr int B1SPL = SH::B1SPL, B2SPL = SH::B2SPL, AW = SH::AW, NPW = SH::NPW;
-    constexpr int PL = S * RX;  // floats per image plane in a block
+    constexpr int PL = S * RXI;  // floats per image plane in a block
+    constexpr int PLG = S * RX;  // logits per plane in the staging box
     constexpr int RUP = (R + 1) & ~1;
 
     extern __shared__ __align__(128) unsigned char smem_tma[];
     float* s_lg = reinterpret_cast<float*>(smem_tma);  // [NST][NLOG][S][RX] | [NLOG][S][RX] + staging
-    float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RX]
-    float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RX]  (level 0: u * out after A)
-    float* s_ob = s_up + NBU * UPF;                    // [NOB][3][S][RX]  forward output / Lhat^l
+    float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RXI]
+    float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RXI] (level 0: u * out after A)
+    float* s_ob = s_up + NBU * UPF;                    // [NOB][3][S][RXI] forward output / Lhat^l
     float* s_lhc = s_ob + SH::NOB * UPF;               // [NST][3][CROWS][CB]
     float* s_t1 = s_lhc + NST * SH::LHF;               // [NST][3][CT][CB]   (CH)
-    float* s_g = s_t1 + NST * T1F;                     // [3][S][RX]  G = gout / sum
-    float* s_inn = s_g + 3 * PL;                       // [S][RX]     inner' = sum_c gin_c out_c / sum
+    float* s_g = s_t1 + NST * T1F;                     // [3][S][RXI] G = gout / sum
+    float* s_inn = s_g + 3 * PL;                       // [S][RXI]    inner' = sum_c gin_c out_c / sum
     float* s_cac = s_inn + PL;                         // [CR][3][TXC] coarse ghat accumulators
+    float* s_red = s_cac + (B3ON ? CR * 3 * TXC : 0);  // [4 (B2SPL-1)][3][B2C] B2W partial rows
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
 
     const int tid = threadIdx.x;
     const int b = blockIdx.z;
     const int nc = a.nc, H = a.H, W = a.W, c0 = a.c0;
-    const int x0 = blockIdx.x * TXB, xs0 = x0 - RA;   // xs0: global x of smem column 0
+    const int x0 = blockIdx.x * TXB, xs0 = x0 - RA;   // xs0: global x of logit column 0
+    const int xsi0 = xs0 + DI;                         // global x of image column 0
     const int cxs = (x0 >> 1) & ~3;                   // coarse box start (16-B aligned)
     const int y0 = blockIdx.y * a.seg_h, y1 = min(y0 + a.seg_h, H);
     const int qstart = max(y0 - RUP, 0);
@@ -272,17 +299,17 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         int slt = sl_i - NPRO + rel / S;
         slt += slt < 0 ? NBL : 0;
         slt -= slt >= NBL ? NBL : 0;
-        return s_lin + slt * BLKF + which * DEMOFF + (rel % S) * RX;
+        return s_lin + slt * BLKF + which * DEMOFF + (rel % S) * RXI;
     };
     auto ring_block = [&](float* base, int j) { return base + ((j + 64 * NBU) % NBU) * UPF; };
     // image-ring row r (absolute) -> pointer to plane `which` (0: x0/L, 1: demod), channel 0
     auto lin_row = [&](int r, int which) {
         const int rel = r - qstart - R + NPRO * S;
-        return lin_block(rel / S - NPRO) + which * DEMOFF + (rel % S) * RX;
+        return lin_block(rel / S - NPRO) + which * DEMOFF + (rel % S) * RXI;
     };
     auto ring_row = [&](float* base, int r) {  // q row r -> upstream ring, channel 0
         const int rel = r - qstart + S;
-        return ring_block(base, rel / S - 1) + (rel % S) * RX;
+        return ring_block(base, rel / S - 1) + (rel % S) * RXI;
     };
 
     // ---- TMA issue (thread 0)
@@ -292,10 +319,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         const int qs = qstart + j * S;
         mbar_expect_tx(bar, SH::TX_STEP);
         tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? js * LGS1 : 0) : s_lg + js * LGF, &mp.lg, xs0, qs, 0, b, bar);
-        tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
-        if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
-        tma_load_4d(ring_block(s_up, j), &mp.up, xs0, qs, c0, b, bar);
-        tma_load_4d(s_ob + (SH::EARLY ? js * UPF : 0), &mp.out, xs0, qs, c0, b, bar);
+        tma_load_4d(lin_block(j), &mp.lin, xsi0, qs + R, c0, b, bar);
+        if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xsi0, qs + R, c0, b, bar);
+        tma_load_4d(ring_block(s_up, j), &mp.up, xsi0, qs, c0, b, bar);
+        tma_load_4d(s_ob + (SH::EARLY ? js * UPF : 0), &mp.out, xsi0, qs, c0, b, bar);
         if constexpr (UP) tma_load_4d(s_lhc + js * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
         if constexpr (CH) tma_load_4d(s_t1 + js * T1F, &mp.t1, cxs, (qs - R) >> 1, c0, b, bar);
     };
@@ -303,11 +330,11 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
 
     // ---- clamp-to-edge patch of image-ring rows [r0, r1) (after conversion);
     // called by all threads with uniform arguments
-    const bool col_border = xs0 < 0 || xs0 + RX > W;
+    const bool col_border = xsi0 < 0 || xsi0 + RXI > W;
     auto patch_rows = [&](int r0, int r1) {
         if (col_border) {
-            // only the columns outside the image: [0, lo) and [hi, RX)
-            const int lo = max(0, -xs0), hi = min(RX, W - xs0), nb = lo + (RX - hi);
+            // only the columns outside the image: [0, lo) and [hi, RXI)
+            const int lo = max(0, -xsi0), hi = min(RXI, W - xsi0), nb = lo + (RXI - hi);
             for (int i = tid; i < (r1 - r0) * NI * 3 * nb; i += NTH) {
                 const int k = i % nb, rest = i / nb;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
@@ -318,8 +345,8 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             cta_sync<NTH>();
         }
         if (r0 < 0 || r1 > H) {
-            for (int i = tid; i < (r1 - r0) * NI * 3 * RX; i += NTH) {
-                const int ri = i % RX, rest = i / RX;
+            for (int i = tid; i < (r1 - r0) * NI * 3 * RXI; i += NTH) {
+                const int ri = i % RXI, rest = i / RXI;
                 const int pc = rest % (NI * 3), r = r0 + rest / (NI * 3);
                 const int src = clampi(r, 0, H - 1);
                 if (src != r) lin_row(r, pc / 3)[(pc % 3) * PL + ri] = lin_row(src, pc / 3)[(pc % 3) * PL + ri];
@@ -328,13 +355,14 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         }
     };
     // x0 = noisy / max(d, floor) in place (level 0), for ring rows of block j
+    // (ri: image column)
     auto convert_block = [&](int j, int s, int ri) {
         if constexpr (L0) {
             float* blk = lin_block(j);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float d = blk[DEMOFF + c * PL + s * RX + ri];
-                blk[c * PL + s * RX + ri] *= rcp_fast(fmaxf(d, (float)kDemodFloor));
+                const float d = blk[DEMOFF + c * PL + s * RXI + ri];
+                blk[c * PL + s * RXI + ri] *= rcp_fast(fmaxf(d, (float)kDemodFloor));
             }
         }
     };
@@ -350,23 +378,24 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     if (tid == 0) {
         mbar_expect_tx(&bars[PBAR], SH::TX_PRO);
         for (int j = -NPRO; j < 0; ++j) {
-            tma_load_4d(lin_block(j), &mp.lin, xs0, qstart + R + j * S, c0, b, &bars[PBAR]);
-            if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qstart + R + j * S, c0, b, &bars[PBAR]);
+            tma_load_4d(lin_block(j), &mp.lin, xsi0, qstart + R + j * S, c0, b, &bars[PBAR]);
+            if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xsi0, qstart + R + j * S, c0, b, &bars[PBAR]);
         }
         // the first steps: NST - 1 ahead when issuing early, else one
         for (int j = 0; j < (SH::EARLY ? NST - 1 : 1) && j < nsteps; ++j) issue_step(j);
     }
     mbar_wait(&bars[PBAR], 0);
-    for (int i = tid; i < NPRO * S * RX; i += NTH) {
-        const int jj = i / (S * RX), rem = i % (S * RX);
-        convert_block(jj - NPRO, rem / RX, rem % RX);
+    for (int i = tid; i < NPRO * S * RXI; i += NTH) {
+        const int jj = i / (S * RXI), rem = i % (S * RXI);
+        convert_block(jj - NPRO, rem / RXI, rem % RXI);
     }
     __syncthreads();
     patch_rows(qstart + R - NPRO * S, qstart + R);
 
-    const int s_a = tid / RW, rw_a = tid - s_a * RW;  // phase A: S rows x RW columns, dense
-    const int ri_a = RA - R + rw_a;                     // smem column of this thread's region pixel
-    const bool act_a = tid < S * RW;
+    const int s_a = tid / SH::PV, rw_a = tid - s_a * SH::PV;  // phase A: S rows x RW columns (pitch PV)
+    const int ri_a = RA - R + rw_a;                             // logit column of this thread's region pixel
+    const int ii_a = ri_a - DI;                                 // its image / exponential column
+    const bool act_a = s_a < S && rw_a < RW;
 
     SSB_RT(long long rt_tw = 0; unsigned long long rt_acc[4] = {0, 0, 0, 0};)
     // ------------------------------------------------ A: softmax, G, inner'
@@ -386,7 +415,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         if (act_a) {
             float e[NLOG];
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PL + s_a * RX + ri_a]);
+            for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PLG + s_a * RX + ri_a]);
             const float m = max4(e);
             const float2 mk2 = bcast2(-m * kLog2e);
             float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 chains
@@ -405,14 +434,14 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];
             }
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) lgb[t * EPL + s_a * RXE + ri_a - ESH] = e[t];
+            for (int t = 0; t < NLOG; ++t) lgb[t * EPL + s_a * RXE + ii_a] = e[t];
             const float inv = rcp_fast(sum);
-            convert_block(i, s_a, ri_a);  // (block i = slot sl_i)
-            float* ub = ring_block(s_up, i) + s_a * RX + ri_a;
-            const float* ob = s_ob + (SH::EARLY ? (i % NST) * UPF : 0) + s_a * RX + ri_a;
+            convert_block(i, s_a, ii_a);  // (block i = slot sl_i)
+            float* ub = ring_block(s_up, i) + s_a * RXI + ii_a;
+            const float* ob = s_ob + (SH::EARLY ? (i % NST) * UPF : 0) + s_a * RXI + ii_a;
             float dq[3] = {1.f, 1.f, 1.f};
             if constexpr (L0) {
-                const float* dr = lin_row_step(qs, qs + s_a, 1) + ri_a;
+                const float* dr = lin_row_step(qs, qs + s_a, 1) + ii_a;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dq[c] = fmaxf(dr[c * PL], (float)kDemodFloor);
             }
@@ -421,10 +450,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             for (int c = 0; c < 3; ++c) {
                 const float u = ub[c * PL], uo = u * ob[c * PL];
                 inner += uo;
-                s_g[c * PL + s_a * RX + ri_a] = u * dq[c] * inv;
+                s_g[c * PL + s_a * RXI + ii_a] = u * dq[c] * inv;
                 if constexpr (L0) ub[c * PL] = uo;  // the flush's demod gradient needs u * out
             }
-            s_inn[s_a * RX + ri_a] = inner * inv;
+            s_inn[s_a * RXI + ii_a] = inner * inv;
         }
         cta_sync<NTH>();
         if constexpr (!SH::EARLY) {
@@ -449,7 +478,8 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     const bool act_b1 = item < SH::NB1S && (item % SH::QS) < NQUAD;
     // B2 role (warps 4-7)
     const int b2 = tid % HN;
-    const int col = b2 / B2SPL, part2 = b2 - col * B2SPL;
+    const int col = SH::B2W ? ((b2 >> 5) % SH::WPP) * 32 + (b2 & 31) : b2 / B2SPL;
+    const int part2 = SH::B2W ? (b2 >> 5) / SH::WPP : b2 - col * B2SPL;
     const int gx2 = x0 + col, ri2 = col + RA;
     const bool act2 = tid >= HN && col < TXB && gx2 < W;
     // the lanes of a column split the tap columns dx (window rows stay compile-time)
@@ -487,13 +517,13 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 float g[4][3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const float4 gg = *reinterpret_cast<const float4*>(s_g + c * PL + s * RX + ri);
+                    const float4 gg = *reinterpret_cast<const float4*>(s_g + c * PL + s * RXI + ri - DI);
                     g[0][c] = gg.x;
                     g[1][c] = gg.y;
                     g[2][c] = gg.z;
                     g[3][c] = gg.w;
                 }
-                const float4 inn4 = *reinterpret_cast<const float4*>(s_inn + s * RX + ri);
+                const float4 inn4 = *reinterpret_cast<const float4*>(s_inn + s * RXI + ri - DI);
                 const float inn[4] = {inn4.x, inn4.y, inn4.z, inn4.w};
                 const float* ep = static_cast<const float*>(__builtin_assume_aligned(lgb + s * RXE + ri - ESH, 16));
                 auto body = [&](auto acc_t) {
@@ -504,7 +534,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                              (size_t)t_first * hw32;
                     auto tap_row = [&](int dy) {
                         const float* xr =
-                            static_cast<const float*>(__builtin_assume_aligned(lin_row_step(qs, qy + dy, 0) + ri - 4, 16));
+                            static_cast<const float*>(__builtin_assume_aligned(lin_row_step(qs, qy + dy, 0) + ri - DI - 4, 16));
                         // accumulators start at -inner': g_logit_t = e_t * (gw_t - inner')
                         float gw[4][K];
 #pragma unroll
@@ -516,7 +546,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                             float2 vv[6];
 #pragma unroll
                             for (int k2 = 0; k2 < 3; ++k2) {
-                                const float4 t4 = *reinterpret_cast<const float4*>(xr + c * PL + 4 * k2);
+                                const float4 t4 = lds128(xr + c * PL + 4 * k2);
                                 vv[2 * k2] = make_float2(t4.x, t4.y);
                                 vv[2 * k2 + 1] = make_float2(t4.z, t4.w);
                             }
@@ -625,7 +655,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         const int cyb = qs >> 1;  // qs is even
 #pragma unroll
                         for (int ss = 0; ss < S; ++ss) {
-                            const float* gr = s_g + c * PL + ss * RX + rj;
+                            const float* gr = s_g + c * PL + ss * RXI + rj - DI;
                             const float gm = gr[-1], g0 = gr[0], gq = gr[1];
 #pragma unroll
                             for (int ii = 0; ii < 2; ++ii) {
@@ -662,7 +692,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 for (int ss = 0; ss < S; ++ss) {
                     float g[3], w[K];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) g[c] = s_g[c * PL + ss * RX + rj];
+                    for (int c = 0; c < 3; ++c) g[c] = s_g[c * PL + ss * RXI + rj - DI];
 #pragma unroll
                     for (int d = 0; d < K; ++d) w[d] = lgb[(d * K + dx + R) * EPL + ss * RXE + rj - ESH];
 #pragma unroll
@@ -736,7 +766,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 int slt = sl_i + (REL / S - NPRO);
                 slt += slt < 0 ? NBL : 0;
                 slt -= slt >= NBL ? NBL : 0;
-                return s_lin + slt * BLKF + (REL % S) * RX + ri2;
+                return s_lin + slt * BLKF + (REL % S) * RXI + ri2 - DI;
             };
             auto up_base_j = [&](auto j_t) -> const float* {
                 constexpr int J = decltype(j_t)::value;
@@ -745,7 +775,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 int slt = su_i + (RELU / S - 1);
                 slt += slt < 0 ? NBU : 0;
                 slt -= slt >= NBU ? NBU : 0;
-                return s_up + slt * UPF + (RELU % S) * RX + ri2;
+                return s_up + slt * UPF + (RELU % S) * RXI + ri2 - DI;
             };
             auto flush_block = [&](auto kb_t) {
                 constexpr int KB = decltype(kb_t)::value;
@@ -755,7 +785,40 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 int nrow;                   // rows this lane writes (1 or 2 or 4)
                 int rstep = 1;              // window-row stride between them
                 float vout[4][3];
-                if constexpr (B2SPL == 1) {
+                if constexpr (SH::B2W) {
+                    // partials of the rows other parts own -> shared memory; the
+                    // owner (r % B2SPL == part) adds them to its own
+                    if constexpr (KB > 0) asm volatile("bar.sync 1, %0;" ::"n"(HN) : "memory");  // (bottom blocks)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int own = r % B2SPL;
+                        if (own != part2) {
+                            const int sl = r * (B2SPL - 1) + (part2 < own ? part2 : part2 - 1);
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) s_red[(sl * 3 + c) * SH::B2C + col] = wget(KB + r, c);
+                        }
+                    }
+                    asm volatile("bar.sync 1, %0;" ::"n"(HN) : "memory");
+                    constexpr int NOWN = 4 / B2SPL;
+#pragma unroll
+                    for (int m = 0; m < NOWN; ++m) {
+                        const int r = part2 + B2SPL * m;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            // own partial of row r (compile-time window rows, selected)
+                            float v;
+                            if constexpr (B2SPL == 2) v = part2 ? wget(KB + 1 + 2 * m, c) : wget(KB + 2 * m, c);
+                            else v = part2 == 0 ? wget(KB, c) : (part2 == 1 ? wget(KB + 1, c) : (part2 == 2 ? wget(KB + 2, c) : wget(KB + 3, c)));
+#pragma unroll
+                            for (int w = 0; w < B2SPL; ++w)
+                                if (w != part2) v += s_red[((r * (B2SPL - 1) + (w < part2 ? w : w - 1)) * 3 + c) * SH::B2C + col];
+                            vout[m][c] = v;
+                        }
+                    }
+                    krow = KB + part2;
+                    nrow = NOWN;
+                    rstep = B2SPL;
+                } else if constexpr (B2SPL == 1) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -837,9 +900,9 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         // (B2SPL = 4: one row per lane -- the generic row lookup is
                         // cheaper than selecting among the block's four)
                         const int kk = krow - KB + r * rstep;  // 0..3
-                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2;
+                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2 - DI;
                         const float* dr = xr + DEMOFF;
-                        const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2;  // u * out
+                        const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2 - DI;  // u * out
                         const int Yp = P >> 1, Xp = gx2 >> 1;
                         const bool hy = 2 * Yp + 1 < H, hx = 2 * Xp + 1 < W;
                         const float rcnt = (hy && hx) ? 0.25f : ((hy || hx) ? 0.5f : 1.f);
@@ -857,9 +920,9 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                         }
                     } else if constexpr (L0) {
                         const int kk = krow - KB + r * rstep;
-                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2;
+                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2 - DI;
                         const float* dr = xr + DEMOFF;
-                        const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2;  // u * out
+                        const float* uor = B2SPL <= 2 ? sel4(ub4, kk) : ring_row(s_up, P) + ri2 - DI;  // u * out
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             if (c >= nc) break;

@@ -131,15 +131,15 @@ bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
     bool ok = make_tma_map_4d(&mp.lg, a0.logits, tma_dtype<TL>(), sizeof(TL), a0.W, a0.H, a0.nlog,
                               a0.batch, SH::RX, SH::S, SH::NLOG) &&
               make_tma_map_4d(&mp.lin, base(a0.lin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
-                              SH::RX, SH::S, 3) &&
+                              SH::RXI, SH::S, 3) &&
               make_tma_map_4d(&mp.up, base(a0.gin, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
-                              SH::RX, SH::S, 3);
+                              SH::RXI, SH::S, 3);
     if (ok)
         ok = make_tma_map_4d(&mp.out, base(a0.outp, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
-                             SH::RX, SH::S, 3);
+                             SH::RXI, SH::S, 3);
     if (ok && L0)
         ok = make_tma_map_4d(&mp.dem, base(a0.demod, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
-                             SH::RX, SH::S, 3);
+                             SH::RXI, SH::S, 3);
     if (ok && UP)
         ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
