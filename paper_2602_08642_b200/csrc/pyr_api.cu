@@ -167,10 +167,14 @@ int make_plan(const ssb_pyr_desc* d, PyrPlan* p) {
         p->gl_off[l] = w;
         w += bytes;
     }
-    p->lse_off = 0;
-    if (p->esz == 4) {  // float32: level-0 log-sum-exp for the level-0-last backward
-        p->lse_off = t;
-        t += align256((size_t)p->B * p->H * p->W * sizeof(float));
+    // float32: per-level base-2 log-sum-exp of the softmax (the TMA backward
+    // kernels evaluate their weights from it; k_up_transpose reads level 0)
+    for (int l = 0; l < p->L; ++l) {
+        p->lse_off[l] = 0;
+        if (p->esz == 4 && (l == 0 || p->K >= 7)) {
+            p->lse_off[l] = t;
+            t += align256((size_t)p->B * p->hl[l] * p->wl[l] * sizeof(float));
+        }
     }
     // kernels address channels of one frame with 32-bit offsets
     if ((unsigned long long)p->nlog[0] * (unsigned long long)p->H * (unsigned long long)p->W >=

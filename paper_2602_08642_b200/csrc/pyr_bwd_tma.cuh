@@ -43,6 +43,7 @@ struct TmaMaps {
     CUtensorMap out;  // forward output (level 0) or Lhat^l, box (RXI, S, 3)
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
     CUtensorMap t1;   // CH (level 0 last): T1 = level-1 input gradient incl. the pool chain, box (CB, CT, 3)
+    CUtensorMap lse;  // the forward's base-2 log-sum-exp, box (RXI, S, 1)
 };
 
 // CH: level 0 runs after the coarser levels (pyr_chain.cuh): no upsample
@@ -60,7 +61,6 @@ struct TmaShape {
     // with RA = 16 B of logits (4 fp32 / 8 bf16), rows are RX = TXB + 2 RA
     // wide, TXB a multiple of RA.  k = 7 uses narrower strips (shared memory).
     static constexpr int LGE = (int)sizeof(TL);  // logit element size
-    static constexpr bool SEP = LGE != 4;        // bf16: staging box + separate fp32 exponentials
     // SS = rows per step: 4 (256 threads, 2 CTAs per SM) or 8 (512 threads, one
     // CTA per SM: twice the TMA box rows per request)
     static constexpr int RA = 16 / LGE, S = SS;
@@ -108,22 +108,32 @@ struct TmaShape {
     static constexpr int CR = 4, CB = ((TXB / 2 + 4 + 3) / 4) * 4, CROWS = S / 2 + 1;
     // every TMA destination starts 128-B aligned (sizes rounded up to 32 floats)
     static constexpr int al32(int n) { return (n + 31) & ~31; }
-    // exponentials: fp32 logits = in place in the staging box (pitch RX);
-    // bf16 = a separate fp32 buffer with a tighter pitch RXE over the columns
-    // phase A fills, shifted by ESH (keeps 16-B alignment of pixel quads)
-    static constexpr int ESH = SEP ? RA - 4 : 0;
-    static constexpr int RXE = SEP ? ((TXB + R + 4 + 3) / 4) * 4 : RX;
-    static constexpr int EPL = S * RXE;                // floats per exponential plane
-    static_assert(ESH == DI && RXE == RXI, "exponential and image columns coincide");
     // phase A: pixel (row s, region column rw) on thread s * PV + rw -- PV =
-    // the image / exponential row pitch when S of them fit the CTA, so every
+    // the image row pitch when S of them fit the CTA, so every
     // warp's shared accesses are one contiguous run (no bank conflicts where
     // a warp straddles two rows); else dense (PV = RW)
     static constexpr int PV = S * RXI <= NTH ? RXI : RW;
+    // LSW (k = 7): the weights are evaluated where they are used, as
+    // w_t = 2^(z_t log2 e - lse) from the logits (one TMA box per ring stage,
+    // storage type, pitch RX) and the forward's base-2 log-sum-exp (one more
+    // plane per step) -- phase A is G / inner only, no exponentials buffer.
+    // k <= 5 keeps the softmax pass: phase A runs on all 8 warps there and
+    // its in-place exponentials are read once by B1 and once by B2.
+    // (Measured, same-box A/B: k7 bf16 level 0 -9%; k5 fp32 level 0 +19%.)
+    static constexpr bool LSW = K >= 7;
+    static constexpr bool SEP = !LSW && LGE != 4;  // bf16 softmax pass: separate fp32 exponentials
+    // exponentials (softmax pass): fp32 logits = in place in the staging box
+    // (pitch RX); bf16 = a separate fp32 buffer with a tighter pitch RXE over
+    // the columns phase A fills, shifted by ESH (keeps 16-B alignment of quads)
+    static constexpr int ESH = SEP ? RA - 4 : 0;
+    static constexpr int RXE = SEP ? ((TXB + R + 4 + 3) / 4) * 4 : RX;
+    static constexpr int EPL = S * RXE;                // floats per exponential plane
+    static_assert(LSW || (ESH == DI && RXE == RXI), "exponential and image columns coincide");
     static constexpr int LGF = al32(NLOG * EPL);       // floats per exponentials buffer
-    // logits staging (storage type): fp32 = the two exponential buffers
-    // themselves (in place); bf16 = staging box(es) + one fp32 buffer
-    static constexpr int LGS1 = SEP ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
+    // logits staging box in the storage type: LSW and bf16 (fp32 softmax pass:
+    // the exponential buffers themselves, in place)
+    static constexpr int LGS1 = (LSW || SEP) ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
+    static constexpr int LSF = LSW ? al32(S * RXI) : 0;  // log-sum-exp block (LSW)
     static constexpr int DEMOFF = al32(3 * S * RXI);   // demod plane offset inside a ring block
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
     static constexpr int UPF = al32(3 * S * RXI);      // floats per upstream / output block
@@ -136,21 +146,20 @@ struct TmaShape {
     // EARLY: the next step's TMA is issued at the top of the step (right after
     // the previous step's end barrier) instead of after phase A -- every
     // buffer it overwrites belongs to step i-1; needs a second output block,
-    // and for fp32 logits only (bf16 would need a second staging box)
-    // (bf16 at NST = 2: measured no gain at k = 7 with the second staging box
-    // -- issued after phase A instead; NST >= 3 always issues early)
-    static constexpr bool EARLY = !SEP || NST > 2;
+    // and a second staging box for bf16 logits with the softmax pass
+    // (measured no gain at k = 7 before LSW -- issued after phase A there)
+    static constexpr bool EARLY = LSW || !SEP || NST > 2;
     static constexpr int NOB = EARLY ? NST : 1;
     static constexpr int LGS = EARLY ? NST * LGS1 : LGS1;  // staging floats (all boxes)
-    static constexpr int LGBUF = SEP ? LGF + LGS : NST * LGF;
+    static constexpr int LGBUF = LSW ? LGS : (SEP ? LGF + LGS : NST * LGF);
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RXI * 4;
     static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
-                                        (CH ? 3 * CT * CB * 4 : 0);
+                                        (CH ? 3 * CT * CB * 4 : 0) + (LSW ? S * RXI * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr int NBU = L0 ? NBU0 : (EARLY ? 2 : 1);
     static constexpr int REDF = B2W ? al32(4 * (B2SPL - 1) * 3 * B2C) : 0;  // B2W partial rows
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F +
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F + NST * LSF +
                                      3 * S * RXI + S * RXI + (B3ON ? CR * 3 * TXC : 0) + REDF;
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
@@ -255,27 +264,30 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     constexpr int NTH = SH::NTH, HN = SH::HN;
     constexpr bool B3ON = SH::B3ON;
     constexpr int CT = SH::CT, T1F = SH::T1F;
-    constexpr bool SEP = SH::SEP;
     constexpr int R = SH::R, NT = SH::NT, NLOG = SH::NLOG, S = SH::S, RX = SH::RX, RXI = SH::RXI, DI = SH::DI;
     constexpr int RA = SH::RA, RW = SH::RW, NQUAD = SH::NQUAD;
     constexpr int TXB = SH::TXB, TXC = SH::TXC, NPRO = SH::NPRO, NBL = SH::NBL, NBU = SH::NBU;
     constexpr int NI = SH::NI, CR = SH::CR, CB = SH::CB, CROWS = SH::CROWS;
-    constexpr int LGF = SH::LGF, BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF;
-    constexpr int EPL = SH::EPL, RXE = SH::RXE, ESH = SH::ESH, LGS1 = SH::LGS1;
+    constexpr int BLKF = SH::BLKF, UPF = SH::UPF, DEMOFF = SH::DEMOFF, LGS1 = SH::LGS1, LSF = SH::LSF;
+    constexpr bool LSW = SH::LSW, SEP = SH::SEP;
+    constexpr int LGF = SH::LGF, EPL = SH::EPL, RXE = SH::RXE, ESH = SH::ESH;
     constexpr int B1SPL = SH::B1SPL, B2SPL = SH::B2SPL, AW = SH::AW, NPW = SH::NPW;
     constexpr int PL = S * RXI;  // floats per image plane in a block
     constexpr int PLG = S * RX;  // logits per plane in the staging box
     constexpr int RUP = (R + 1) & ~1;
 
     extern __shared__ __align__(128) unsigned char smem_tma[];
-    float* s_lg = reinterpret_cast<float*>(smem_tma);  // [NST][NLOG][S][RX] | [NLOG][S][RX] + staging
+    // LSW: [NST] logits boxes [NLOG][S][RX] (storage type); softmax pass:
+    // [NST][NLOG][S][RX] in place (fp32) | [NLOG][S][RXE] + staging box(es)
+    float* s_lg = reinterpret_cast<float*>(smem_tma);
     float* s_lin = s_lg + SH::LGBUF;                   // [NBL][NI][3][S][RXI]
     float* s_up = s_lin + NBL * BLKF;                  // [NBU][3][S][RXI] (level 0: u * out after A)
     float* s_ob = s_up + NBU * UPF;                    // [NOB][3][S][RXI] forward output / Lhat^l
     float* s_lhc = s_ob + SH::NOB * UPF;               // [NST][3][CROWS][CB]
     float* s_t1 = s_lhc + NST * SH::LHF;               // [NST][3][CT][CB]   (CH)
-    float* s_g = s_t1 + NST * T1F;                     // [3][S][RXI] G = gout / sum
-    float* s_inn = s_g + 3 * PL;                       // [S][RXI]    inner' = sum_c gin_c out_c / sum
+    float* s_lse = s_t1 + NST * T1F;                   // [NST][S][RXI] log-sum-exp (LSW)
+    float* s_g = s_lse + NST * LSF;                    // [3][S][RXI] G = gout (softmax pass: / sum)
+    float* s_inn = s_g + 3 * PL;                       // [S][RXI]    inner = sum_c gin_c out_c (/ sum)
     float* s_cac = s_inn + PL;                         // [CR][3][TXC] coarse ghat accumulators
     float* s_red = s_cac + (B3ON ? CR * 3 * TXC : 0);  // [4 (B2SPL-1)][3][B2C] B2W partial rows
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
@@ -318,7 +330,12 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         uint64_t* bar = &bars[js];
         const int qs = qstart + j * S;
         mbar_expect_tx(bar, SH::TX_STEP);
-        tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? js * LGS1 : 0) : s_lg + js * LGF, &mp.lg, xs0, qs, 0, b, bar);
+        if constexpr (LSW) {
+            tma_load_4d(s_lg + js * LGS1, &mp.lg, xs0, qs, 0, b, bar);
+            tma_load_4d(s_lse + js * LSF, &mp.lse, xsi0, qs, 0, b, bar);
+        } else {
+            tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? js * LGS1 : 0) : s_lg + js * LGF, &mp.lg, xs0, qs, 0, b, bar);
+        }
         tma_load_4d(lin_block(j), &mp.lin, xsi0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xsi0, qs + R, c0, b, bar);
         tma_load_4d(ring_block(s_up, j), &mp.up, xsi0, qs, c0, b, bar);
@@ -398,9 +415,11 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     const bool act_a = s_a < S && rw_a < RW;
 
     SSB_RT(long long rt_tw = 0; unsigned long long rt_acc[4] = {0, 0, 0, 0};)
-    // ------------------------------------------------ A: softmax, G, inner'
+    // ------------------------------------------------ A: [softmax,] G, inner
     // (every thread; ends with the CTA barrier, the next prefetch and the
-    // clamp patch of the image rows that arrived with this step)
+    // clamp patch of the image rows that arrived with this step).  LSW: no
+    // softmax -- B1 / B2 / B3 evaluate the normalised weights where they use
+    // them; else the exponentials e land in lgb and G, inner carry 1 / sum.
     auto phase_a = [&](int i, int qs, float* lgb, const TL* lgs) {
         if constexpr (SH::EARLY) {
             // every thread passed step i-1's end barrier: the buffers of step
@@ -413,29 +432,32 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         mbar_wait(&bars[i % NST], (i / NST) & 1);
         SSB_RT(rt_tw = clock64();)
         if (act_a) {
-            float e[NLOG];
+            float inv = 1.f;
+            if constexpr (!LSW) {
+                float e[NLOG];
 #pragma unroll
-            for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PLG + s_a * RX + ri_a]);
-            const float m = max4(e);
-            const float2 mk2 = bcast2(-m * kLog2e);
-            float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 chains
+                for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PLG + s_a * RX + ri_a]);
+                const float m = max4(e);
+                const float2 mk2 = bcast2(-m * kLog2e);
+                float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 chains
 #pragma unroll
-            for (int t = 0; t + 1 < NLOG; t += 2) {
-                const float2 z2 = ffma2(make_float2(e[t], e[t + 1]), bcast2(kLog2e), mk2);
-                e[t] = ex2_ftz(z2.x);
-                e[t + 1] = ex2_ftz(z2.y);
-                sum2[(t >> 1) & 1] = fadd2(sum2[(t >> 1) & 1],
-                                           make_float2((TIED && t == NT) ? 4.f * e[t] : e[t],
-                                                       (TIED && t + 1 == NT) ? 4.f * e[t + 1] : e[t + 1]));
+                for (int t = 0; t + 1 < NLOG; t += 2) {
+                    const float2 z2 = ffma2(make_float2(e[t], e[t + 1]), bcast2(kLog2e), mk2);
+                    e[t] = ex2_ftz(z2.x);
+                    e[t + 1] = ex2_ftz(z2.y);
+                    sum2[(t >> 1) & 1] = fadd2(sum2[(t >> 1) & 1],
+                                               make_float2((TIED && t == NT) ? 4.f * e[t] : e[t],
+                                                           (TIED && t + 1 == NT) ? 4.f * e[t + 1] : e[t + 1]));
+                }
+                float sum = (sum2[0].x + sum2[1].x) + (sum2[0].y + sum2[1].y);
+                if constexpr (NLOG & 1) {
+                    e[NLOG - 1] = ex2_ftz(fmaf(e[NLOG - 1], kLog2e, mk2.x));
+                    sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];
+                }
+#pragma unroll
+                for (int t = 0; t < NLOG; ++t) lgb[t * EPL + s_a * RXE + ii_a] = e[t];
+                inv = rcp_fast(sum);
             }
-            float sum = (sum2[0].x + sum2[1].x) + (sum2[0].y + sum2[1].y);
-            if constexpr (NLOG & 1) {
-                e[NLOG - 1] = ex2_ftz(fmaf(e[NLOG - 1], kLog2e, mk2.x));
-                sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];
-            }
-#pragma unroll
-            for (int t = 0; t < NLOG; ++t) lgb[t * EPL + s_a * RXE + ii_a] = e[t];
-            const float inv = rcp_fast(sum);
             convert_block(i, s_a, ii_a);  // (block i = slot sl_i)
             float* ub = ring_block(s_up, i) + s_a * RXI + ii_a;
             const float* ob = s_ob + (SH::EARLY ? (i % NST) * UPF : 0) + s_a * RXI + ii_a;
@@ -450,10 +472,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             for (int c = 0; c < 3; ++c) {
                 const float u = ub[c * PL], uo = u * ob[c * PL];
                 inner += uo;
-                s_g[c * PL + s_a * RXI + ii_a] = u * dq[c] * inv;
+                s_g[c * PL + s_a * RXI + ii_a] = LSW ? u * dq[c] : u * dq[c] * inv;
                 if constexpr (L0) ub[c * PL] = uo;  // the flush's demod gradient needs u * out
             }
-            s_inn[s_a * RXI + ii_a] = inner * inv;
+            s_inn[s_a * RXI + ii_a] = LSW ? inner : inner * inv;
         }
         cta_sync<NTH>();
         if constexpr (!SH::EARLY) {
@@ -503,10 +525,14 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     int su_i = 0;  // upstream-ring slot of step i (i mod NBU), kept incrementally
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1, su_i = (su_i + 1 == NBU) ? 0 : su_i + 1) {
         const int qs = qstart + i * S;
-        float* lgb = SEP ? s_lg : s_lg + (i % NST) * LGF;  // exponentials of this step
+        // LSW: the logits of this step and their log-sum-exp; softmax pass: the
+        // exponentials of this step (lgb) and the logits' staging box
+        float* lgb = LSW ? nullptr : (SEP ? s_lg : s_lg + (i % NST) * LGF);
+        const TL* lgs = reinterpret_cast<const TL*>(
+            LSW ? s_lg + (i % NST) * LGS1 : (SEP ? s_lg + LGF + (SH::EARLY ? (i % NST) * LGS1 : 0) : lgb));
+        const float* lsb = s_lse + (i % NST) * LSF;
         SSB_RT(const long long rt_t0 = clock64();)
-        phase_a(i, qs, lgb,
-                reinterpret_cast<const TL*>(SEP ? s_lg + LGF + (SH::EARLY ? (i % NST) * LGS1 : 0) : lgb));
+        phase_a(i, qs, lgb, lgs);
         SSB_RT(const long long rt_t1 = clock64(); rt_acc[0] += rt_tw - rt_t0; rt_acc[1] += rt_t1 - rt_tw;)
         if (tid < HN) {
             // -------------------------------------------- B1: logit gradients
@@ -525,7 +551,27 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 }
                 const float4 inn4 = *reinterpret_cast<const float4*>(s_inn + s * RXI + ri - DI);
                 const float inn[4] = {inn4.x, inn4.y, inn4.z, inn4.w};
-                const float* ep = static_cast<const float*>(__builtin_assume_aligned(lgb + s * RXE + ri - ESH, 16));
+                // weights of the quad's taps: LSW w_t = 2^(z_t log2 e - lse); else
+                // the exponentials of phase A (G, inner carry the 1 / sum)
+                const TL* lq = lgs + s * RX + ri;
+                float2 nl01 = make_float2(0.f, 0.f), nl23 = nl01;
+                if constexpr (LSW) {
+                    const float4 ls4 = lds128(lsb + s * RXI + ri - DI);
+                    nl01 = make_float2(-ls4.x, -ls4.y);
+                    nl23 = make_float2(-ls4.z, -ls4.w);
+                }
+                const float* ep = LSW ? nullptr : lgb + s * RXE + ri - ESH;
+                auto wquad = [&](int t) {
+                    if constexpr (LSW) {
+                        const float4 z = ld_quad(lq + t * PLG);
+                        const float2 p01 = ffma2(make_float2(z.x, z.y), bcast2(kLog2e), nl01);
+                        const float2 p23 = ffma2(make_float2(z.z, z.w), bcast2(kLog2e), nl23);
+                        return make_float4(ex2_ftz(p01.x), ex2_ftz(p01.y), ex2_ftz(p23.x), ex2_ftz(p23.y));
+                    } else {
+                        return *reinterpret_cast<const float4*>(
+                            static_cast<const float*>(__builtin_assume_aligned(ep, 16)) + t * EPL);
+                    }
+                };
                 auto body = [&](auto acc_t) {
                     constexpr bool ACC = decltype(acc_t)::value;
                     constexpr int OFF = 4 - R;  // window value m = x(ri - 4 + m); pixel p, tap d -> m = p + d + OFF
@@ -569,7 +615,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
 #pragma unroll
                         for (int d = 0; d < K; ++d) {
                             const int t = (dy + R) * K + d;
-                            const float4 e4 = *reinterpret_cast<const float4*>(ep + t * EPL);
+                            const float4 e4 = wquad(t);
                             st_gz4<ACC>(gp, e4.x * gw[0][d], e4.y * gw[1][d], e4.z * gw[2][d], e4.w * gw[3][d]);
                             gp += hw32;
                         }
@@ -617,7 +663,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                                     for (int jj = 0; jj < 2; ++jj) gu[p][2 * ii + jj] = dotc[p][(p + jj) >> 1];
                             }
                             if constexpr (TIED) {
-                                const float4 e4 = *reinterpret_cast<const float4*>(ep + NT * EPL);
+                                const float4 e4 = wquad(NT);
                                 float z[4];
 #pragma unroll
                                 for (int p = 0; p < 4; ++p) z[p] = (gu[p][0] + gu[p][1]) + (gu[p][2] + gu[p][3]);
@@ -625,7 +671,7 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                             } else {
 #pragma unroll
                                 for (int t4 = 0; t4 < 4; ++t4) {
-                                    const float4 e4 = *reinterpret_cast<const float4*>(ep + (NT + t4) * EPL);
+                                    const float4 e4 = wquad(NT + t4);
                                     st_gz4<ACC>(gp, e4.x * gu[0][t4], e4.y * gu[1][t4], e4.z * gu[2][t4], e4.w * gu[3][t4]);
                                     gp += hw32;
                                 }
@@ -659,10 +705,25 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                             const float gm = gr[-1], g0 = gr[0], gq = gr[1];
 #pragma unroll
                             for (int ii = 0; ii < 2; ++ii) {
-                                const float* w0 = lgb + (TIED ? NT : NT + 2 * ii) * EPL + ss * RXE + rj - ESH;
-                                const float* w1 = lgb + (TIED ? NT : NT + 2 * ii + 1) * EPL + ss * RXE + rj - ESH;
-                                const float am = w1[-1], a0 = w0[0] + w1[0];
-                                const float aq = lastX ? w0[1] + w1[1] : w0[1];
+                                float am, a0, aq;
+                                if constexpr (LSW) {
+                                    // log-sum-exp of fine columns 2X-1, 2X, 2X+1
+                                    const float* lr = lsb + ss * RXI + rj - DI;
+                                    const float nlm = -lr[-1], nl0 = -lr[0], nlq = -lr[1];
+                                    const TL* z0 = lgs + (TIED ? NT : NT + 2 * ii) * PLG + ss * RX + rj;
+                                    const TL* z1 = lgs + (TIED ? NT : NT + 2 * ii + 1) * PLG + ss * RX + rj;
+                                    auto wt = [](TL z, float nl) { return ex2_ftz(fmaf(to_f32(z), kLog2e, nl)); };
+                                    const float w0q = wt(z0[1], nlq);
+                                    am = wt(z1[-1], nlm);
+                                    a0 = wt(z0[0], nl0) + wt(z1[0], nl0);
+                                    aq = lastX ? w0q + wt(z1[1], nlq) : w0q;
+                                } else {
+                                    const float* w0 = lgb + (TIED ? NT : NT + 2 * ii) * EPL + ss * RXE + rj - ESH;
+                                    const float* w1 = lgb + (TIED ? NT : NT + 2 * ii + 1) * EPL + ss * RXE + rj - ESH;
+                                    am = w1[-1];
+                                    a0 = w0[0] + w1[0];
+                                    aq = lastX ? w0[1] + w1[1] : w0[1];
+                                }
                                 const int yl = (ss + ii) >> 1;  // compile-time after unrolling
                                 cv[yl] = fmaf(am, gm, fmaf(a0, g0, fmaf(aq, gq, cv[yl])));
                             }
@@ -693,8 +754,15 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                     float g[3], w[K];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) g[c] = s_g[c * PL + ss * RXI + rj - DI];
+                    if constexpr (LSW) {
+                        const float nl = -lsb[ss * RXI + rj - DI];
 #pragma unroll
-                    for (int d = 0; d < K; ++d) w[d] = lgb[(d * K + dx + R) * EPL + ss * RXE + rj - ESH];
+                        for (int d = 0; d < K; ++d)
+                            w[d] = ex2_ftz(fmaf(to_f32(lgs[(d * K + dx + R) * PLG + ss * RX + rj]), kLog2e, nl));
+                    } else {
+#pragma unroll
+                        for (int d = 0; d < K; ++d) w[d] = lgb[(d * K + dx + R) * EPL + ss * RXE + rj - ESH];
+                    }
 #pragma unroll
                     for (int d = 0; d < K; ++d) {
                         const int k = ss + d;

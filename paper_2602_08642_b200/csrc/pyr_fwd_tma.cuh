@@ -210,12 +210,10 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
                 const float2 sum2 = fadd2(sa[0], sa[1]);
                 const float inv0 = frcp(sum2.x), inv1 = frcp(sum2.y);
                 const bool two = gx + 1 < W;
-                if constexpr (L0) {  // base-2 log-sum-exp for the backward's upsample-transpose pre-pass
-                    if (a.lse) {
-                        float* lp = (float*)a.lse + (size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx;
-                        lp[0] = mk2.x + __log2f(sum2.x);
-                        if (two) lp[1] = mk2.y + __log2f(sum2.y);
-                    }
+                if (a.lse) {  // base-2 log-sum-exp: the backward's weights 2^(z log2 e - lse)
+                    float* lp = (float*)a.lse + (size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx;
+                    lp[0] = mk2.x + __log2f(sum2.x);
+                    if (two) lp[1] = mk2.y + __log2f(sum2.y);
                 }
                 float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                 // window of the pair: smem columns xi + RA - R .. xi + RA + R + 1,
@@ -317,9 +315,8 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
         if (qy < y1 && gx < W) {
             const float sum = sum4(e);
             const float inv = frcp(sum);
-            if constexpr (L0) {  // base-2 log-sum-exp for the backward's upsample-transpose pre-pass
-                if (a.lse) ((float*)a.lse)[(size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx] = mk + __log2f(sum);
-            }
+            // base-2 log-sum-exp: the backward's weights 2^(z log2 e - lse)
+            if (a.lse) ((float*)a.lse)[(size_t)b * hw32 + (unsigned)qy * (unsigned)W + (unsigned)gx] = mk + __log2f(sum);
             float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
             for (int dy = -R; dy <= R; ++dy) {

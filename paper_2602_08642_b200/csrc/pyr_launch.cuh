@@ -25,7 +25,8 @@ struct PyrPlan {
     size_t pool_off[SSB_MAX_LEVELS], lhat_off[SSB_MAX_LEVELS], tape_bytes;
     // workspace: ghat^l and gL_l for l >= 1
     size_t ghat_off[SSB_MAX_LEVELS], gl_off[SSB_MAX_LEVELS], ws_bytes;
-    size_t lse_off;  // tape (float32 plans): level-0 base-2 log-sum-exp, B x H x W floats
+    // tape (float32 plans): per-level base-2 log-sum-exp of the softmax, B x h_l x w_l floats
+    size_t lse_off[SSB_MAX_LEVELS];
 };
 
 int make_plan(const ssb_pyr_desc* d, PyrPlan* p);
@@ -122,7 +123,7 @@ template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int 
 bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
     using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>;
     // needs the forward output (level 0) / Lhat^l for the softmax-backward inner product
-    if ((L0 && !a0.demod) || !a0.outp || tma_disabled()) return false;
+    if ((L0 && !a0.demod) || !a0.outp || (SH::LSW && !a0.lse) || tma_disabled()) return false;
     const long long plane = (long long)a0.H * a0.W;
     auto base = [&](const void* p, long long pl) {
         return p ? (const void*)((const float*)p - (long long)a0.c0 * pl) : nullptr;
@@ -143,6 +144,8 @@ bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
     if (ok && UP)
         ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
+    if (ok && SH::LSW)  // the forward's log-sum-exp, (W, H, 1, B)
+        ok = make_tma_map_4d(&mp.lse, a0.lse, f32, 4, a0.W, a0.H, 1, a0.batch, SH::RXI, SH::S, 1);
     if (ok && CH)
         ok = a0.t1 && make_tma_map_4d(&mp.t1, base(a0.t1, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc, a0.Hc,
                                       a0.ctot, a0.batch, SH::CB, SH::CT, 3);
@@ -287,11 +290,13 @@ int run_forward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_fwd_io* i
                 a.demod = dem;
                 a.prev = io->prev ? (const T*)io->prev + coff0 : nullptr;
                 a.out = (T*)io->out + coff0;
-                a.lse = chain_path(d, p, io->demod) ? (void*)(tp + p.lse_off) : nullptr;
             } else {
                 a.lin = (const T*)(tp + p.pool_off[l]) + (long long)c0 * e_l;
                 a.out = (T*)(tp + p.lhat_off[l]) + (long long)c0 * e_l;
             }
+            // the log-sum-exp is channel independent: written once (group 0);
+            // read by k_up_transpose (level 0) and the k = 7 backward (LSW)
+            a.lse = (p.esz == 4 && c0 == 0 && (l == 0 || K >= 7)) ? (void*)(tp + p.lse_off[l]) : nullptr;
             const bool up = l < p.L - 1;
             if (up) {
                 const long long e_c = lvl_elems(p, l + 1);
@@ -327,6 +332,7 @@ BwdLevel bwd_level(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io
     a.glogits = want ? io->g_logits[l] : nullptr;
     a.in_b = (long long)p.C * e_l;
     a.in_c = e_l;
+    a.lse = p.esz == 4 ? (const float*)(tp + p.lse_off[l]) : nullptr;
     if (l == 0) {
         a.lin = io->noisy;
         a.demod = io->demod;
@@ -382,7 +388,7 @@ int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr
         u.nlog = p.nlog[0];
         u.logits = io->logits[0];
         u.lg_b = (long long)p.nlog[0] * lvl_elems(p, 0);
-        u.lse = (const float*)(tp + p.lse_off);
+        u.lse = (const float*)(tp + p.lse_off[0]);
         u.up = (const float*)io->upstream;
         u.demod = (const float*)io->demod;
         u.ghat = (float*)(wp + p.ghat_off[1]);
@@ -488,6 +494,7 @@ int run_backward(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* 
             a.glogits = want ? io->g_logits[l] : nullptr;
             a.in_b = (long long)p.C * e_l;
             a.in_c = e_l;
+            a.lse = p.esz == 4 ? (const float*)(tp + p.lse_off[l]) : nullptr;
             if (l == 0) {
                 a.lin = (const T*)io->noisy + coff0;
                 a.demod = io->demod ? (const T*)io->demod + coff0 : nullptr;

@@ -4,6 +4,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace ssb {
@@ -22,6 +23,15 @@ __device__ __forceinline__ float4 lds128(const float* p) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "r"(smem_u32(p)));
     return v;
+}
+
+// four consecutive logits (a pixel quad) from shared memory as floats
+__device__ __forceinline__ float4 ld_quad(const float* p) { return lds128(p); }
+__device__ __forceinline__ float4 ld_quad(const __nv_bfloat16* p) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+    return make_float4(a.x, a.y, b.x, b.y);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

@@ -9,5 +9,5 @@ cap() {  # tag skip args...
   ncu -i gpurun_out/$tag.ncu-rep --page raw --csv > gpurun_out/${tag}_raw.csv 2>&1
   rm -f gpurun_out/$tag.ncu-rep
 }
-cap b2w_c3 7 --frames 1 --h 2160 --w 3840 --levels 4 --k 7 --ldt bf16 --iters 2
-cap b2w_c4a 5 --frames 4 --iters 2
+cap ${TAG:-b2w}_c3 7 --frames 1 --h 2160 --w 3840 --levels 4 --k 7 --ldt bf16 --iters 2
+cap ${TAG:-b2w}_c4a 5 --frames 4 --iters 2

@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     a = ap.parse_args()
     lib = _lib.load()
-    fns = [getattr(lib, f"ssb_debug_role_cycles{t}") for t in (0, 3, 5, 7)]
+    fns = [getattr(lib, f"ssb_debug_role_cycles{t}") for t in ("0", "3", "5", "7", "5b", "7b")]
     buf = (C.c_ulonglong * 8)()
 
     def read():
