@@ -159,8 +159,18 @@ struct TmaShape {
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr int NBU = L0 ? NBU0 : (EARLY ? 2 : 1);
     static constexpr int REDF = B2W ? al32(4 * (B2SPL - 1) * 3 * B2C) : 0;  // B2W partial rows
+    // AHEAD: phase A of step i+1 runs at the end of step i (each warp after its
+    // B work, before the end-of-step barrier, which then also publishes
+    // G / inner of step i+1): one CTA barrier per step instead of two, and
+    // phase A overlaps the B work of slower warps.  G / inner double-buffered;
+    // needs the early-issued ring (every buffer phase A of step i+1 writes is
+    // one step i does not read).  (Measured, same-box A/B: level 0 k5 -1.4%,
+    // k7 -4.6%; k7 level 1 -6%; k5 levels >= 1, whose B1 warps also carry the
+    // upsample transpose, +4.5% -- kept in order there.)
+    static constexpr bool AHEAD = EARLY && (L0 || LSW);
+    static constexpr int NGB = AHEAD ? 2 : 1;
     static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F + NST * LSF +
-                                     3 * S * RXI + S * RXI + (B3ON ? CR * 3 * TXC : 0) + REDF;
+                                     NGB * 4 * S * RXI + (B3ON ? CR * 3 * TXC : 0) + REDF;
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
     static constexpr int MINB = (SS == 4 && 2 * (SMEM + 1024) <= 233472) ? 2 : 1;
@@ -286,9 +296,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     float* s_lhc = s_ob + SH::NOB * UPF;               // [NST][3][CROWS][CB]
     float* s_t1 = s_lhc + NST * SH::LHF;               // [NST][3][CT][CB]   (CH)
     float* s_lse = s_t1 + NST * T1F;                   // [NST][S][RXI] log-sum-exp (LSW)
-    float* s_g = s_lse + NST * LSF;                    // [3][S][RXI] G = gout (softmax pass: / sum)
-    float* s_inn = s_g + 3 * PL;                       // [S][RXI]    inner = sum_c gin_c out_c (/ sum)
-    float* s_cac = s_inn + PL;                         // [CR][3][TXC] coarse ghat accumulators
+    // [NGB][4][S][RXI] per step: G = gout (softmax pass: / sum), then
+    // inner = sum_c gin_c out_c (/ sum)
+    float* s_gi = s_lse + NST * LSF;
+    float* s_cac = s_gi + SH::NGB * 4 * PL;            // [CR][3][TXC] coarse ghat accumulators
     float* s_red = s_cac + (B3ON ? CR * 3 * TXC : 0);  // [4 (B2SPL-1)][3][B2C] B2W partial rows
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
 
@@ -416,27 +427,22 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
 
     SSB_RT(long long rt_tw = 0; unsigned long long rt_acc[4] = {0, 0, 0, 0};)
     // ------------------------------------------------ A: [softmax,] G, inner
-    // (every thread; ends with the CTA barrier, the next prefetch and the
-    // clamp patch of the image rows that arrived with this step).  LSW: no
-    // softmax -- B1 / B2 / B3 evaluate the normalised weights where they use
-    // them; else the exponentials e land in lgb and G, inner carry 1 / sum.
-    auto phase_a = [&](int i, int qs, float* lgb, const TL* lgs) {
-        if constexpr (SH::EARLY) {
-            // every thread passed step i-1's end barrier: the buffers of step
-            // i+NST-1 (those of step i-1) are free -- prefetch NST-1 steps ahead
-            if (tid == 0 && i + NST - 1 < nsteps) {
-                fence_proxy_async();
-                issue_step(i + NST - 1);
-            }
-        }
-        mbar_wait(&bars[i % NST], (i / NST) & 1);
-        SSB_RT(rt_tw = clock64();)
+    // of step j (rows qs_j ..) into G / inner buffer gb.  LSW: no softmax --
+    // B1 / B2 / B3 evaluate the normalised weights where they use them; else
+    // the exponentials e land in lgb_j and G, inner carry 1 / sum.
+    auto lgb_of = [&](int j) -> float* { return LSW ? nullptr : (SEP ? s_lg : s_lg + (j % NST) * LGF); };
+    auto lgs_of = [&](int j) -> const TL* {
+        return reinterpret_cast<const TL*>(
+            LSW ? s_lg + (j % NST) * LGS1 : (SEP ? s_lg + LGF + (SH::EARLY ? (j % NST) * LGS1 : 0) : lgb_of(j)));
+    };
+    auto gbuf = [&](int j) { return s_gi + (SH::AHEAD ? (j & 1) * 4 * PL : 0); };
+    auto phase_a_body = [&](int j, int qs_j, float* lgb_j, const TL* lgs_j, float* gb) {
         if (act_a) {
             float inv = 1.f;
             if constexpr (!LSW) {
                 float e[NLOG];
 #pragma unroll
-                for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs[t * PLG + s_a * RX + ri_a]);
+                for (int t = 0; t < NLOG; ++t) e[t] = to_f32(lgs_j[t * PLG + s_a * RX + ri_a]);
                 const float m = max4(e);
                 const float2 mk2 = bcast2(-m * kLog2e);
                 float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // 4 chains
@@ -455,15 +461,15 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                     sum += (TIED && NLOG - 1 == NT) ? 4.f * e[NLOG - 1] : e[NLOG - 1];
                 }
 #pragma unroll
-                for (int t = 0; t < NLOG; ++t) lgb[t * EPL + s_a * RXE + ii_a] = e[t];
+                for (int t = 0; t < NLOG; ++t) lgb_j[t * EPL + s_a * RXE + ii_a] = e[t];
                 inv = rcp_fast(sum);
             }
-            convert_block(i, s_a, ii_a);  // (block i = slot sl_i)
-            float* ub = ring_block(s_up, i) + s_a * RXI + ii_a;
-            const float* ob = s_ob + (SH::EARLY ? (i % NST) * UPF : 0) + s_a * RXI + ii_a;
+            convert_block(j, s_a, ii_a);
+            float* ub = ring_block(s_up, j) + s_a * RXI + ii_a;
+            const float* ob = s_ob + (SH::EARLY ? (j % NST) * UPF : 0) + s_a * RXI + ii_a;
             float dq[3] = {1.f, 1.f, 1.f};
             if constexpr (L0) {
-                const float* dr = lin_row_step(qs, qs + s_a, 1) + ii_a;
+                const float* dr = lin_row(qs_j + s_a, 1) + ii_a;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) dq[c] = fmaxf(dr[c * PL], (float)kDemodFloor);
             }
@@ -472,21 +478,19 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             for (int c = 0; c < 3; ++c) {
                 const float u = ub[c * PL], uo = u * ob[c * PL];
                 inner += uo;
-                s_g[c * PL + s_a * RXI + ii_a] = LSW ? u * dq[c] : u * dq[c] * inv;
+                gb[c * PL + s_a * RXI + ii_a] = LSW ? u * dq[c] : u * dq[c] * inv;
                 if constexpr (L0) ub[c * PL] = uo;  // the flush's demod gradient needs u * out
             }
-            s_inn[s_a * RXI + ii_a] = LSW ? inner : inner * inv;
+            gb[3 * PL + s_a * RXI + ii_a] = LSW ? inner : inner * inv;
         }
-        cta_sync<NTH>();
-        if constexpr (!SH::EARLY) {
-            // every thread has finished the previous step and this step's phase A:
-            // the buffers of step i+1 are free
-            if (tid == 0 && i + 1 < nsteps) {
-                fence_proxy_async();
-                issue_step(i + 1);
-            }
+    };
+    // every thread passed step i-1's end barrier: the buffers of step i+NST-1
+    // (those of step i-1) are free -- prefetch NST-1 steps ahead
+    auto issue_ahead = [&](int i) {
+        if (tid == 0 && i + NST - 1 < nsteps) {
+            fence_proxy_async();
+            issue_step(i + NST - 1);
         }
-        if (col_border || qs + R + S > H) patch_rows(qs + R, qs + R + S);
     };
 
     const bool want = a.want_params != 0;
@@ -522,18 +526,43 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         else win[k >> 1][c].x += v;
     };
 
+    if constexpr (SH::AHEAD) {
+        // phase A of step 0 (later steps: at the end of the step before)
+        if (nsteps > 0) {
+            mbar_wait(&bars[0], 0);
+            phase_a_body(0, qstart, lgb_of(0), lgs_of(0), gbuf(0));
+        }
+        cta_sync<NTH>();
+        if (nsteps > 0 && (col_border || qstart + R + S > H)) patch_rows(qstart + R, qstart + R + S);
+    }
     int su_i = 0;  // upstream-ring slot of step i (i mod NBU), kept incrementally
     for (int i = 0; i < nsteps; ++i, sl_i = (sl_i + 1 == NBL) ? 0 : sl_i + 1, su_i = (su_i + 1 == NBU) ? 0 : su_i + 1) {
         const int qs = qstart + i * S;
         // LSW: the logits of this step and their log-sum-exp; softmax pass: the
         // exponentials of this step (lgb) and the logits' staging box
-        float* lgb = LSW ? nullptr : (SEP ? s_lg : s_lg + (i % NST) * LGF);
-        const TL* lgs = reinterpret_cast<const TL*>(
-            LSW ? s_lg + (i % NST) * LGS1 : (SEP ? s_lg + LGF + (SH::EARLY ? (i % NST) * LGS1 : 0) : lgb));
+        float* lgb = lgb_of(i);
+        const TL* lgs = lgs_of(i);
         const float* lsb = s_lse + (i % NST) * LSF;
-        SSB_RT(const long long rt_t0 = clock64();)
-        phase_a(i, qs, lgb, lgs);
-        SSB_RT(const long long rt_t1 = clock64(); rt_acc[0] += rt_tw - rt_t0; rt_acc[1] += rt_t1 - rt_tw;)
+        const float* s_g = gbuf(i);         // G of this step
+        const float* s_inn = s_g + 3 * PL;  // inner of this step
+        SSB_RT(long long rt_t0 = clock64(); long long rt_t1 = rt_t0;)
+        if constexpr (SH::EARLY) issue_ahead(i);
+        if constexpr (!SH::AHEAD) {
+            mbar_wait(&bars[i % NST], (i / NST) & 1);
+            SSB_RT(rt_tw = clock64();)
+            phase_a_body(i, qs, lgb, lgs, gbuf(i));
+            cta_sync<NTH>();
+            if constexpr (!SH::EARLY) {
+                // every thread has finished the previous step and this step's
+                // phase A: the buffers of step i+1 are free
+                if (tid == 0 && i + 1 < nsteps) {
+                    fence_proxy_async();
+                    issue_step(i + 1);
+                }
+            }
+            if (col_border || qs + R + S > H) patch_rows(qs + R, qs + R + S);
+            SSB_RT(rt_t1 = clock64(); rt_acc[0] += rt_tw - rt_t0; rt_acc[1] += rt_t1 - rt_tw;)
+        }
         if (tid < HN) {
             // -------------------------------------------- B1: logit gradients
             const int qy = qs + s, gx = x0 + xi;
@@ -1026,9 +1055,18 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                 for (int c = 0; c < 3; ++c)
                     win[p][c] = p + S / 2 < NPW ? win[p + S / 2][c] : make_float2(0.f, 0.f);
         }
-        SSB_RT(const long long rt_t2 = clock64();)
-        cta_sync<NTH>();  // end of step
-        SSB_RT(const long long rt_t3 = clock64(); rt_acc[2] += rt_t2 - rt_t1; rt_acc[3] += rt_t3 - rt_t2;)
+        SSB_RT(const long long rt_t2 = clock64(); long long rt_t2b = rt_t2;)
+        if constexpr (SH::AHEAD) {
+            // phase A of the next step, as soon as this warp's B work is done
+            if (i + 1 < nsteps) {
+                mbar_wait(&bars[(i + 1) % NST], ((i + 1) / NST) & 1);
+                SSB_RT(rt_tw = clock64(); rt_acc[0] += rt_tw - rt_t2;)
+                phase_a_body(i + 1, qs + S, lgb_of(i + 1), lgs_of(i + 1), gbuf(i + 1));
+                SSB_RT(rt_t2b = clock64(); rt_acc[1] += rt_t2b - rt_tw;)
+            }
+        }
+        cta_sync<NTH>();  // end of step (AHEAD: G / inner of step i+1 published)
+        SSB_RT(const long long rt_t3 = clock64(); rt_acc[2] += rt_t2 - rt_t1; rt_acc[3] += rt_t3 - rt_t2b;)
         if (B3ON && tid < HN) {
             // coarse ghat rows finished by this step (all B3 items are in)
             const bool bottom = qs + S >= H;
@@ -1051,6 +1089,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                     if (c < nc) gc[c * a.c_c] = v[c];
             }
             cnext = cend;
+        }
+        if constexpr (SH::AHEAD) {
+            // the image rows that arrived with step i+1 (converted by its phase A)
+            if (i + 1 < nsteps && (col_border || qs + S + R + S > H)) patch_rows(qs + S + R, qs + S + R + S);
         }
     }
 #ifdef SSB_ROLE_TIMING
