@@ -44,6 +44,7 @@ struct TmaMaps {
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
     CUtensorMap t1;   // CH (level 0 last): T1 = level-1 input gradient incl. the pool chain, box (CB, CT, 3)
     CUtensorMap lse;  // the forward's base-2 log-sum-exp, box (RXI, S, 1)
+    CUtensorMap gd;   // temporal pass: g_demod as level 0 wrote it, box (RXI, S, 3) at the flush rows
 };
 
 // CH: level 0 runs after the coarser levels (pyr_chain.cuh): no upsample
@@ -53,7 +54,13 @@ struct TmaMaps {
 // NST - 1 steps ahead (at the top of step j - NST + 1, right after the end
 // barrier of step j - NST, whose slot it reuses).  TXO != 0 overrides the
 // strip's own-column count (a multiple of RA).
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0>
+// MODE bits: kBwdLsw forces the log-sum-exp weights (LSW) at any k; kBwdTp =
+// the temporal-group pass of level 0 with history (image = the warped
+// history, logits = the temporal channels, flush = g_prev and the history
+// term of g_demod)
+constexpr int kBwdLsw = 1, kBwdTp = 2;
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0,
+          int MODE = 0>
 struct TmaShape {
     static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
     static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
@@ -120,7 +127,8 @@ struct TmaShape {
     // k <= 5 keeps the softmax pass: phase A runs on all 8 warps there and
     // its in-place exponentials are read once by B1 and once by B2.
     // (Measured, same-box A/B: k7 bf16 level 0 -9%; k5 fp32 level 0 +19%.)
-    static constexpr bool LSW = K >= 7;
+    static constexpr bool LSW = K >= 7 || (MODE & kBwdLsw) != 0;
+    static constexpr bool TP = (MODE & kBwdTp) != 0;
     static constexpr bool SEP = !LSW && LGE != 4;  // bf16 softmax pass: separate fp32 exponentials
     // exponentials (softmax pass): fp32 logits = in place in the staging box
     // (pitch RX); bf16 = a separate fp32 buffer with a tighter pitch RXE over
@@ -134,6 +142,7 @@ struct TmaShape {
     // the exponential buffers themselves, in place)
     static constexpr int LGS1 = (LSW || SEP) ? al32((NLOG * S * RX * LGE + 3) / 4) : 0;
     static constexpr int LSF = LSW ? al32(S * RXI) : 0;  // log-sum-exp block (LSW)
+    static constexpr int GDF = TP ? al32(3 * S * RXI) : 0;  // temporal pass: g_demod rows R behind
     static constexpr int DEMOFF = al32(3 * S * RXI);   // demod plane offset inside a ring block
     static constexpr int BLKF = NI * DEMOFF;           // floats per image-ring block
     static constexpr int UPF = al32(3 * S * RXI);      // floats per upstream / output block
@@ -155,7 +164,7 @@ struct TmaShape {
     // transaction bytes (exact box sizes, not the padded buffer sizes)
     static constexpr uint32_t TX_IMG = 3 * S * RXI * 4;
     static constexpr uint32_t TX_STEP = NLOG * S * RX * LGE + (NI + 2) * TX_IMG + (UP ? 3 * CROWS * CB * 4 : 0) +
-                                        (CH ? 3 * CT * CB * 4 : 0) + (LSW ? S * RXI * 4 : 0);
+                                        (CH ? 3 * CT * CB * 4 : 0) + (LSW ? S * RXI * 4 : 0) + (TP ? 3 * S * RXI * 4 : 0);
     static constexpr uint32_t TX_PRO = NPRO * NI * TX_IMG;
     static constexpr int NBU = L0 ? NBU0 : (EARLY ? 2 : 1);
     static constexpr int REDF = B2W ? al32(4 * (B2SPL - 1) * 3 * B2C) : 0;  // B2W partial rows
@@ -169,7 +178,7 @@ struct TmaShape {
     // upsample transpose, +4.5% -- kept in order there.)
     static constexpr bool AHEAD = EARLY && (L0 || LSW);
     static constexpr int NGB = AHEAD ? 2 : 1;
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F + NST * LSF +
+    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F + NST * LSF + NST * GDF +
                                      NGB * 4 * S * RXI + (B3ON ? CR * 3 * TXC : 0) + REDF;
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
@@ -266,11 +275,12 @@ static inline int role_cycles_read(unsigned long long* out8) {
 #define SSB_RT(...)
 #endif
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0>
-__global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>::NTH),
-                                  (TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>::MINB))
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0,
+          int MODE = 0>
+__global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO, MODE>::NTH),
+                                  (TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO, MODE>::MINB))
     k_pyr_bwd_tma(const BwdLevel a, const __grid_constant__ TmaMaps mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO, MODE>;
     constexpr int NTH = SH::NTH, HN = SH::HN;
     constexpr bool B3ON = SH::B3ON;
     constexpr int CT = SH::CT, T1F = SH::T1F;
@@ -298,7 +308,8 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     float* s_lse = s_t1 + NST * T1F;                   // [NST][S][RXI] log-sum-exp (LSW)
     // [NGB][4][S][RXI] per step: G = gout (softmax pass: / sum), then
     // inner = sum_c gin_c out_c (/ sum)
-    float* s_gi = s_lse + NST * LSF;
+    float* s_gd = s_lse + NST * LSF;                   // [NST][3][S][RXI] g_demod rows (TP)
+    float* s_gi = s_gd + NST * SH::GDF;
     float* s_cac = s_gi + SH::NGB * 4 * PL;            // [CR][3][TXC] coarse ghat accumulators
     float* s_red = s_cac + (B3ON ? CR * 3 * TXC : 0);  // [4 (B2SPL-1)][3][B2C] B2W partial rows
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + SH::FLOATS * 4);
@@ -340,10 +351,12 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
         const int js = j % NST;
         uint64_t* bar = &bars[js];
         const int qs = qstart + j * S;
-        mbar_expect_tx(bar, SH::TX_STEP);
+        mbar_expect_tx(bar, SH::TX_STEP - ((SH::TP && !a.gdc_out) ? 3 * S * RXI * 4 : 0));
         if constexpr (LSW) {
-            tma_load_4d(s_lg + js * LGS1, &mp.lg, xs0, qs, 0, b, bar);
+            tma_load_4d(s_lg + js * LGS1, &mp.lg, xs0, qs, a.lg_c0, b, bar);
             tma_load_4d(s_lse + js * LSF, &mp.lse, xsi0, qs, 0, b, bar);
+            if constexpr (SH::TP)
+                if (a.gdc_out) tma_load_4d(s_gd + js * SH::GDF, &mp.gd, xsi0, qs - R, c0, b, bar);
         } else {
             tma_load_4d(SEP ? s_lg + LGF + (SH::EARLY ? js * LGS1 : 0) : s_lg + js * LGF, &mp.lg, xs0, qs, 0, b, bar);
         }
@@ -1014,6 +1027,29 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
                             const float v = fmaf(t1[c * CT * CB], rcnt, vout[r][c]);
                             __stcs(glo + o, v * rd);
                             if (gdo) __stcs(gdo + o, d > (float)kDemodFloor ? (uor[c * PL] - v * xr[c * PL]) * rd : 0.f);
+                        }
+                    } else if constexpr (L0 && SH::TP) {
+                        // temporal pass: g_prev = g(prev_in) / d; the history
+                        // term of g_demod, -g(prev_in) prev_in / d, joins the
+                        // (masked) value the level-0 kernel wrote (pyramid.py:436-447)
+                        const int kk = krow - KB + r * rstep;
+                        const float* xr = B2SPL <= 2 ? sel4(lb4, kk) : lin_row_step(qs, P, 0) + ri2 - DI;
+                        const float* dr = xr + DEMOFF;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            if (c >= nc) break;
+                            const unsigned o = c * hw32 + off;
+                            const float d = dr[c * PL];
+                            const float rd = rcp_fast(fmaxf(d, (float)kDemodFloor));
+                            const float v = vout[r][c];
+                            __stcs(glo + o, v * rd);
+                            if (gdo && d > (float)kDemodFloor) {
+                                // the step's box holds rows qs - R .. qs - R + S - 1 (KB = 0);
+                                // the bottom step's further rows are read directly
+                                const float g0 = KB == 0 ? s_gd[(i % NST) * SH::GDF + (c * S + kk) * RXI + ri2 - DI]
+                                                         : gdo[o];
+                                __stcs(gdo + o, g0 - v * xr[c * PL] * rd);
+                            }
                         }
                     } else if constexpr (L0) {
                         const int kk = krow - KB + r * rstep;

@@ -1,5 +1,6 @@
-// Level forward, TMA-pipelined row walker (fp32 images, fp32 or bf16 logits,
-// no temporal group; other configurations use k_pyr_fwd).
+// Level forward, TMA-pipelined row walker (fp32 images, fp32 or bf16 logits;
+// the temporal group on the one-pixel-per-thread path; other configurations
+// use k_pyr_fwd).
 //
 // CTA = column strip of TXF = 64 own columns x one segment of rows, walked in
 // steps of S = 4 rows (256 threads, one own pixel each).  Per step one thread
@@ -21,15 +22,20 @@ struct FwdTmaMaps {
     CUtensorMap lin;  // noisy (level 0) or L^l, box (RX, S, 3)
     CUtensorMap dem;  // demod (level 0), box (RX, S, 3)
     CUtensorMap lhc;  // coarse Lhat^{l+1}, box (CB, S/2 + 1, 3)
+    CUtensorMap prv;  // PREV: the warped history, box (RX, S, 3)
 };
 
-template <int K, typename TL, bool L0, bool UP, bool TIED>
+// PREV (level 0 with history): the temporal group's K*K logits follow the
+// upsample logits; the history rides in the image ring as a third plane
+// group, divided by max(d, floor) like the noisy image (pyramid.py:302-309,332-334)
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool PREV = false>
 struct FwdTmaShape {
-    static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW = NT + NUP;
-    static constexpr int NLOG = NT + (UP ? (TIED ? 1 : 4) : 0);
+    static constexpr int R = K / 2, NT = K * K, NUP = UP ? 4 : 0, NW0 = NT + NUP, NW = NW0 + (PREV ? NT : 0);
+    static constexpr int NLOG0 = NT + (UP ? (TIED ? 1 : 4) : 0), NLOG = NLOG0 + (PREV ? NT : 0);
     static constexpr int S = 4, TXF = 64, RA = 4, RX = TXF + 2 * RA;
     static constexpr int NPRO = (2 * R + S - 1) / S, NBL = NPRO + 2;
-    static constexpr int NI = L0 ? 2 : 1;
+    static constexpr int NI = L0 ? (PREV ? 3 : 2) : 1;  // image planes per block: x0 [, demod [, history]]
+    static_assert(!PREV || L0, "the temporal group is level 0's");
     static constexpr int CB = 36, CROWS = S / 2 + 1;
     static constexpr int al32(int n) { return (n + 31) & ~31; }
     static constexpr int LGE = (int)sizeof(TL);          // logit element size (4 or 2)
@@ -47,14 +53,15 @@ struct FwdTmaShape {
     // PAIR (bf16 logits, k = 7: instruction bound): 128 threads, each two
     // horizontally adjacent pixels -- 32-bit logit loads carry both pixels,
     // FFMA2 / FADD2 over the pair, one 8-B shared load per two window values
-    static constexpr bool PAIR = LGE == 2 && K == 7;
+    static constexpr bool PAIR = LGE == 2 && K == 7 && !PREV;
     static constexpr int NTH = PAIR ? 128 : 256;
 };
 
-template <int K, typename TL, bool L0, bool UP, bool TIED>
-__global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdTmaShape<K, TL, L0, UP, TIED>::MINB))
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool PREV = false>
+__global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED, PREV>::NTH),
+                                  (FwdTmaShape<K, TL, L0, UP, TIED, PREV>::MINB))
     k_pyr_fwd_tma(const FwdLevel a, const __grid_constant__ FwdTmaMaps mp) {
-    using SH = FwdTmaShape<K, TL, L0, UP, TIED>;
+    using SH = FwdTmaShape<K, TL, L0, UP, TIED, PREV>;
     constexpr int R = SH::R, NT = SH::NT, NW = SH::NW, NLOG = SH::NLOG, S = SH::S;
     constexpr int TXF = SH::TXF, RA = SH::RA, RX = SH::RX, NPRO = SH::NPRO, NBL = SH::NBL;
     constexpr int NI = SH::NI, CB = SH::CB, CROWS = SH::CROWS, LGF = SH::LGF, BLKF = SH::BLKF;
@@ -94,6 +101,7 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
         tma_load_4d((void*)s_lg, &mp.lg, x0, qs, 0, b, bar);
         tma_load_4d(lin_block(j), &mp.lin, xs0, qs + R, c0, b, bar);
         if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, qs + R, c0, b, bar);
+        if constexpr (PREV) tma_load_4d(lin_block(j) + 2 * DEMOFF, &mp.prv, xs0, qs + R, c0, b, bar);
         if constexpr (UP) tma_load_4d(s_lhc + (j & 1) * SH::LHF, &mp.lhc, cxs, qs >> 1, c0, b, bar);
     };
     const bool col_border = xs0 < 0 || xs0 + RX > W;
@@ -120,12 +128,15 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
             __syncthreads();
         }
     };
-    auto convert_rows = [&](float* blk) {  // x0 = noisy / max(d, floor), in place
+    auto convert_rows = [&](float* blk) {  // x0 = noisy / max(d, floor) [, history / max(d, floor)], in place
         if constexpr (L0) {
             for (int i = tid; i < S * RX; i += NTH) {
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    blk[c * PL + i] *= frcp(demod_clamp(blk[DEMOFF + c * PL + i]));
+                for (int c = 0; c < 3; ++c) {
+                    const float r = frcp(demod_clamp(blk[DEMOFF + c * PL + i]));
+                    blk[c * PL + i] *= r;
+                    if constexpr (PREV) blk[2 * DEMOFF + c * PL + i] *= r;
+                }
             }
         }
     };
@@ -142,6 +153,7 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
         for (int j = -NPRO; j < 0; ++j) {
             tma_load_4d(lin_block(j), &mp.lin, xs0, y0 + R + j * S, c0, b, &bars[1]);
             if constexpr (L0) tma_load_4d(lin_block(j) + DEMOFF, &mp.dem, xs0, y0 + R + j * S, c0, b, &bars[1]);
+            if constexpr (PREV) tma_load_4d(lin_block(j) + 2 * DEMOFF, &mp.prv, xs0, y0 + R + j * S, c0, b, &bars[1]);
         }
         issue_step(0);
     }
@@ -296,11 +308,15 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
                 if constexpr (TIED) {
                     const float eb = ex2_ftz(fmaf(z[NT], kLog2e, -mk));
 #pragma unroll
-                    for (int t = NT; t < NW; ++t) e[t] = eb;
+                    for (int t = NT; t < SH::NW0; ++t) e[t] = eb;
                 } else {
 #pragma unroll
-                    for (int t = NT; t < NW; ++t) e[t] = ex2_ftz(fmaf(z[t], kLog2e, -mk));
+                    for (int t = NT; t < SH::NW0; ++t) e[t] = ex2_ftz(fmaf(z[t], kLog2e, -mk));
                 }
+            }
+            if constexpr (PREV) {
+#pragma unroll
+                for (int t = 0; t < NT; ++t) e[SH::NW0 + t] = ex2_ftz(fmaf(z[SH::NLOG0 + t], kLog2e, -mk));
             }
         }
         convert_rows(lin_block(i));
@@ -341,6 +357,19 @@ __global__ void __launch_bounds__((FwdTmaShape<K, TL, L0, UP, TIED>::NTH), (FwdT
 #pragma unroll
                         for (int c = 0; c < 3; ++c) acc[c] = fmaf(wv, lh[(c * CROWS + cy) * CB + cx], acc[c]);
                     }
+            }
+            if constexpr (PREV) {
+                // temporal taps over the (converted) history plane group
+#pragma unroll
+                for (int dy = -R; dy <= R; ++dy) {
+                    const float* pr = lin_row_step(qs, qy + dy, 2) + xi + RA;
+#pragma unroll
+                    for (int dx = -R; dx <= R; ++dx) {
+                        const float wv = e[SH::NW0 + (dy + R) * K + dx + R];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) acc[c] = fmaf(wv, pr[c * PL + dx], acc[c]);
+                    }
+                }
             }
             const unsigned po = (unsigned)qy * (unsigned)W + (unsigned)gx;
             const float* dr = L0 ? lin_row_step(qs, qy, 1) + xi + RA : nullptr;

@@ -62,6 +62,7 @@ struct BwdLevel {
     void* ghat_c;  // coarse ghat^{l+1}
     const void* t1;  // level 0 after the coarse levels (CH): T1 = level-1 input gradient incl. the pool chain
     const float* lse;  // the forward's base-2 log-sum-exp of this level (TMA kernels), (B, H, W)
+    int lg_c0;         // first logit channel the (TMA) kernel reads (temporal pass: K*K + 4)
 };
 
 // Load one pixel's logits in weight order (denoise, 4 upsample -- the tied
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(FWD_TX* FWD_TY)
 
     const T inv = frcp(sum);
     const long long off = (long long)y * W + x;
-    if constexpr (std::is_same<T, float>::value && !PREV) {
+    if constexpr (std::is_same<T, float>::value) {
         // w_t = 2^(z_t log2 e - lse2): the TMA backward's weights
         if (a.lse) ((float*)a.lse)[(long long)b * H * W + off] = mk + __log2f(sum);
     }

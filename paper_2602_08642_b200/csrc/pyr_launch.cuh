@@ -40,13 +40,14 @@ constexpr CUtensorMapDataType tma_dtype() {
     return sizeof(TL) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
 }
 
-// TMA-pipelined level forward (fp32 images, fp32/bf16 logits, no temporal
-// group, demodulated level 0); returns false if the tensors are not
-// TMA-addressable.
-template <int K, typename TL, bool L0, bool UP, bool TIED>
+// TMA-pipelined level forward (fp32 images, fp32/bf16 logits, demodulated
+// level 0, the temporal group on the one-pixel-per-thread path); returns
+// false if the tensors are not TMA-addressable.
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool PREV = false>
 bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
-    using SH = FwdTmaShape<K, TL, L0, UP, TIED>;
+    using SH = FwdTmaShape<K, TL, L0, UP, TIED, PREV>;
     if (L0 && !a0.demod) return false;
+    if (PREV && (!a0.prev || K == 7)) return false;  // (k = 7: 102 weights per pixel exceed the registers)
     if (const char* e = getenv("SSB_NO_TMA")) {
         if (e[0] == '1') return false;
     }
@@ -66,8 +67,11 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
     if (ok && UP)
         ok = make_tma_map_4d(&mp.lhc, base(a0.lhat_c, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc,
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
+    if (ok && PREV)
+        ok = make_tma_map_4d(&mp.prv, base(a0.prev, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                             SH::RX, SH::S, 3);
     if (!ok) return false;
-    auto kern = k_pyr_fwd_tma<K, TL, L0, UP, TIED>;
+    auto kern = k_pyr_fwd_tma<K, TL, L0, UP, TIED, PREV>;
     static std::atomic<unsigned long long> attr_mask{0};
     smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     FwdLevel a = a0;
@@ -80,8 +84,8 @@ bool launch_fwd_tma(const FwdLevel& a0, cudaStream_t s) {
 
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
 void launch_fwd_one(const FwdLevel& a, int B, cudaStream_t s) {
-    if constexpr (std::is_same<T, float>::value && !std::is_same<TL, double>::value && !PREV) {
-        if (launch_fwd_tma<K, TL, L0, UP, TIED>(a, s)) return;
+    if constexpr (std::is_same<T, float>::value && !std::is_same<TL, double>::value) {
+        if (launch_fwd_tma<K, TL, L0, UP, TIED, PREV>(a, s)) return;
     }
     dim3 block(FWD_TX, FWD_TY);
     dim3 grid((a.W + FWD_TX - 1) / FWD_TX, (a.H + FWD_TY - 1) / FWD_TY, B);
@@ -119,9 +123,10 @@ inline bool tma_disabled() {
     return e && e[0] == '1';
 }
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0>
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int SS = 4, int NST = 2, int TXO = 0,
+          int MODE = 0>
 bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TXO, MODE>;
     // needs the forward output (level 0) / Lhat^l for the softmax-backward inner product
     if ((L0 && !a0.demod) || !a0.outp || (SH::LSW && !a0.lse) || tma_disabled()) return false;
     const long long plane = (long long)a0.H * a0.W;
@@ -146,6 +151,9 @@ bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
                              a0.Hc, a0.ctot, a0.batch, SH::CB, SH::CROWS, 3);
     if (ok && SH::LSW)  // the forward's log-sum-exp, (W, H, 1, B)
         ok = make_tma_map_4d(&mp.lse, a0.lse, f32, 4, a0.W, a0.H, 1, a0.batch, SH::RXI, SH::S, 1);
+    if (ok && SH::TP && a0.gdc_out)  // temporal pass: g_demod as level 0 wrote it
+        ok = make_tma_map_4d(&mp.gd, base(a0.gdc_out, plane), f32, 4, a0.W, a0.H, a0.ctot, a0.batch,
+                                           SH::RXI, SH::S, 3);
     if (ok && CH)
         ok = a0.t1 && make_tma_map_4d(&mp.t1, base(a0.t1, (long long)a0.Hc * a0.Wc), f32, 4, a0.Wc, a0.Hc,
                                       a0.ctot, a0.batch, SH::CB, SH::CT, 3);
@@ -244,7 +252,7 @@ void launch_pool(int B, int nc, int H, int W, const T* in, long long in_b, long 
 // float32, 3 channels, no history, demodulated, >= 2 levels: the backward
 // runs level 0 last (pyr_chain.cuh) from the forward's log-sum-exp
 inline bool chain_path(const ssb_pyr_desc* d, const PyrPlan& p, const void* demod) {
-    if (p.esz != 4 || p.C != 3 || d->has_prev || !demod || p.L < 2 || tma_disabled()) return false;
+    if (p.esz != 4 || p.C != 3 || !demod || p.L < 2 || tma_disabled()) return false;
     const char* e = getenv("SSB_NO_CHAIN");
     return !(e && e[0] == '1');
 }
@@ -368,7 +376,9 @@ inline bool bwd_s8() {  // read per call (tests switch it in-process, like SSB_N
     return e && e[0] == '1';
 }
 
-template <int K, typename TL, bool TIED, int SS, int NST = 2, int TXO = 0>
+// MODE = kBwdLsw with history: level 0's denoise / upsample taps from the
+// log-sum-exp of all its logits, then the temporal pass (kBwdTp)
+template <int K, typename TL, bool TIED, int SS, int NST = 2, int TXO = 0, int MODE = 0>
 int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
                           void* ws, cudaStream_t s) {
     const char* tp = (const char*)tape;
@@ -378,7 +388,21 @@ int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr
     BwdLevel a0 = bwd_level<float>(d, p, io, tp, wp, 0, want, accum);
     a0.t1 = wp + p.gl_off[1];
     TmaMaps mp0;
-    if (!prepare_bwd_tma<K, TL, true, true, TIED, true, SS, NST, TXO>(a0, mp0)) return 1;
+    if (!prepare_bwd_tma<K, TL, true, true, TIED, true, SS, NST, TXO, MODE>(a0, mp0)) return 1;
+    // the temporal group (history): same level-0 walk over the warped
+    // history with the temporal logits (channels K*K + 4 ..; + 1 tied)
+    constexpr bool HIST = (MODE & kBwdLsw) != 0;
+    BwdLevel at = a0;
+    TmaMaps mpt;
+    if constexpr (HIST) {
+        if (!d->has_prev || !io->prev || !io->g_prev) return 1;
+        at.lin = io->prev;
+        at.gl_out = io->g_prev;
+        at.t1 = nullptr;
+        at.lg_c0 = K * K + (TIED ? 1 : 4);
+        at.glogits = want ? (void*)((TL*)io->g_logits[0] + (long long)at.lg_c0 * p.H * p.W) : nullptr;
+        if (!prepare_bwd_tma<K, TL, true, false, false, false, SS, NST, TXO, kBwdLsw | kBwdTp>(at, mpt)) return 1;
+    }
     {
         UpTransposeArgs u{};
         u.H = p.H;
@@ -410,14 +434,25 @@ int run_backward_chain_ss(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr
         dim3 grid((p.wl[1] + 127) / 128, (p.hl[1] + 7) / 8, p.B);
         SSB_LAUNCH(s, k_pool_chain<<<grid, dim3(32, 8), 0, s>>>(c));
     }
-    using SH = TmaShape<K, TL, true, true, TIED, true, SS, NST, TXO>;
-    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true, SS, NST, TXO>;
+    using SH = TmaShape<K, TL, true, true, TIED, true, SS, NST, TXO, MODE>;
+    auto kern = k_pyr_bwd_tma<K, TL, true, true, TIED, true, SS, NST, TXO, MODE>;
     static std::atomic<unsigned long long> attr_mask{0};
     smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     const int strips = (a0.W + SH::TXB - 1) / SH::TXB;
     a0.seg_h = pick_segment(strips, a0.H, a0.batch);
     dim3 grid(strips, (a0.H + a0.seg_h - 1) / a0.seg_h, a0.batch);
     SSB_LAUNCH(s, kern<<<grid, SH::NTH, SH::SMEM, s>>>(a0, mp0));
+    if constexpr (HIST) {
+        // after level 0: its g_demod term joins the value level 0 wrote
+        using SHT = TmaShape<K, TL, true, false, false, false, SS, NST, TXO, kBwdLsw | kBwdTp>;
+        auto kt = k_pyr_bwd_tma<K, TL, true, false, false, false, SS, NST, TXO, kBwdLsw | kBwdTp>;
+        static std::atomic<unsigned long long> attr_t{0};
+        smem_attr_once(attr_t, (const void*)kt, (int)SHT::SMEM);
+        const int st = (at.W + SHT::TXB - 1) / SHT::TXB;
+        at.seg_h = pick_segment(st, at.H, at.batch);
+        dim3 gt(st, (at.H + at.seg_h - 1) / at.seg_h, at.batch);
+        SSB_LAUNCH(s, kt<<<gt, SHT::NTH, SHT::SMEM, s>>>(at, mpt));
+    }
     return cuda_check("ssb_pyr_backward");
 }
 
@@ -434,6 +469,7 @@ inline int bwd0_variant() {
 template <int K, typename TL, bool TIED>
 int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bwd_io* io, const void* tape,
                        void* ws, cudaStream_t s) {
+    if (d->has_prev) return run_backward_chain_ss<K, TL, TIED, 4, 2, 0, kBwdLsw>(d, p, io, tape, ws, s);
     if constexpr (K == 5 && std::is_same<TL, float>::value) {
         if (bwd_s8()) return run_backward_chain_ss<K, TL, TIED, 8>(d, p, io, tape, ws, s);
 #ifdef SSB_BWD_VARIANTS

@@ -131,6 +131,13 @@ def oracle_case(h, w, L, k, seed, demod=True, prev=False, blend="native", scale=
     (1, 9, 2, 5, False, "native"),
     (200, 1, 3, 5, True, "native"),
     (256, 256, 4, 5, False, "native"),
+    # history on the TMA path (W % 4 == 0): level 0 by the log-sum-exp
+    # weights + the temporal pass, in the level-0-last order
+    (64, 80, 3, 5, True, "native"),
+    (72, 128, 4, 7, True, "native"),
+    (45, 96, 3, 3, True, "native"),
+    (48, 40, 3, 5, True, "tied"),
+    (37, 52, 4, 7, True, "tied"),
 ])
 @pytest.mark.parametrize("precision", ["f32", "f64"])
 def test_oracle_cases(ops, h, w, L, k, prev, blend, precision):
@@ -339,19 +346,23 @@ def test_tma_and_generic_paths_agree(ops, monkeypatch):
         assert (a_ - b_).abs().max().item() <= 2e-5 * scale
 
 
-@pytest.mark.parametrize("H,W,L,k,ldt", [(67, 132, 3, 5, "f32"), (66, 136, 2, 5, "f32"), (45, 96, 4, 7, "bf16"),
-                                         (33, 64, 5, 3, "f32")])
-def test_level0_last_order_matches_general_order(H, W, L, k, ldt, monkeypatch):
+@pytest.mark.parametrize("H,W,L,k,ldt,hist", [(67, 132, 3, 5, "f32", False), (66, 136, 2, 5, "f32", False),
+                                              (45, 96, 4, 7, "bf16", False), (33, 64, 5, 3, "f32", False),
+                                              (67, 132, 3, 5, "f32", True), (45, 96, 4, 7, "bf16", True),
+                                              (33, 64, 5, 3, "f32", True)])
+def test_level0_last_order_matches_general_order(H, W, L, k, ldt, hist, monkeypatch):
     """The level-0-last backward (up-transpose pre-pass, pool chain, level 0
-    writing final outputs; csrc/pyr_chain.cuh) against the general order
+    writing final outputs; csrc/pyr_chain.cuh; with history: level 0 by the
+    log-sum-exp weights plus the temporal pass) against the general order
     (fine -> coarse + the coarse -> fine sweep kernel) on the same inputs."""
     from paper_2602_08642_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(H * W + L)
     dev = torch.device("cuda")
     noisy = torch.rand((2, 3, H, W), device=dev, generator=g) * 2
     demod = torch.rand((2, 3, H, W), device=dev, generator=g) * 0.99 + 0.0005
+    prev = torch.rand((2, 3, H, W), device=dev, generator=g) * 2 if hist else None
     shapes = ops.level_shapes(H, W, L)
-    logits = [torch.randn((2, ops.logit_channels(l, L, k), h, w), device=dev, generator=g)
+    logits = [torch.randn((2, ops.logit_channels(l, L, k, has_prev=hist and l == 0), h, w), device=dev, generator=g)
               for l, (h, w) in enumerate(shapes)]
     if ldt == "bf16":
         logits = [z.to(torch.bfloat16) for z in logits]
@@ -360,13 +371,16 @@ def test_level0_last_order_matches_general_order(H, W, L, k, ldt, monkeypatch):
     for mode in ("chain", "general"):
         if mode == "general":
             monkeypatch.setenv("SSB_NO_CHAIN", "1")
-        out, tape = ops.pyramid_forward(noisy, logits, demod, ksize=k)
+        out, tape = ops.pyramid_forward(noisy, logits, demod, prev, ksize=k)
         gr = ops.pyramid_backward(tape, up)
         res[mode] = (out, gr)
         monkeypatch.delenv("SSB_NO_CHAIN", raising=False)
     (o1, g1), (o2, g2) = res["chain"], res["general"]
     assert torch.equal(o1, o2)
-    for a, b in [(g1.input, g2.input), (g1.demod, g2.demod)] + list(zip(g1.logits, g2.logits)):
+    pairs = [(g1.input, g2.input), (g1.demod, g2.demod)] + list(zip(g1.logits, g2.logits))
+    if hist:
+        pairs.append((g1.prev, g2.prev))
+    for a, b in pairs:
         a, b = a.double(), b.double()
         tol = 2e-2 if ldt == "bf16" else 1e-5
         assert torch.allclose(a, b, rtol=tol, atol=tol * b.abs().max().item()), (a - b).abs().max().item()
