@@ -838,20 +838,28 @@ def call_shapes(peak, frames=4, H=1080, W=1920, L=3, k=5):
                               device=dev) for l, (h, w) in enumerate(shapes)]
         up = torch.randn(frames, C, H, W, generator=g, device=dev)
 
+        # the batched draws' backward takes no parameter gradients
+        # (optimize.py:467: reconstruct_backward(..., want_param_grads=False))
+        want = name != "draws_c12"
+
         def step():
             o, t = ops.pyramid_forward(noisy, logits, demod, prev, ksize=k)
-            ops.pyramid_backward(t, up)
+            ops.pyramid_backward(t, up, want_param_grads=want)
         ms = _time_cuda(step, steps=10, warmup=3)
         img = 4 * C
         lg = sum(a * b * ops.logit_channels(l, L, k, has_prev=hist and l == 0) for l, (a, b) in enumerate(shapes))
         n0 = H * W
         fwd = n0 * img * ((3 if dem else 2) + (1 if hist else 0)) + lg * 4
-        bwd = n0 * img * ((6 if dem else 4) + (2 if hist else 0)) + lg * 8
+        if want:
+            bwd = n0 * img * ((6 if dem else 4) + (2 if hist else 0)) + lg * 8
+        else:  # logits, upstream, demod in; g_noisy out
+            bwd = n0 * img * (3 if dem else 2) + lg * 4
         out[f"shape_{name}"] = {
             "workload": f"{frames} x 1920x1080 L3 k5 fp32 fwd+bwd, " + {
                 "history": "with the temporal group over a warped history (evaluate_step frame 1)",
                 "no_demod": "demod=None (reconstruct_core's default)",
-                "draws_c12": "C = 12 (4 batched draws sharing the kernels)"}[name],
+                "draws_c12": "C = 12 (4 batched draws sharing the kernels), no parameter gradients "
+                             "(optimize.py:467)"}[name],
             "mpix_s": round(frames * n0 / (ms * 1e-3) / 1e6, 1), "ms_per_step": round(ms, 4),
             "frac_of_hbm": round(frames * (fwd + bwd) / (ms * 1e-3) / 1e9 / peak, 4)}
         del noisy, demod, prev, logits, up
