@@ -176,10 +176,14 @@ struct TmaShape {
     // one step i does not read).  (Measured, same-box A/B: level 0 k5 -1.4%,
     // k7 -4.6%; k7 level 1 -6%; k5 levels >= 1, whose B1 warps also carry the
     // upsample transpose, +4.5% -- kept in order there.)
-    static constexpr bool AHEAD = EARLY && (L0 || LSW);
+    // (and only where the second G / inner buffer keeps 2 CTAs per SM)
+    static constexpr size_t FLOATS0 = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F +
+                                      NST * LSF + NST * GDF + (B3ON ? CR * 3 * TXC : 0) + REDF;
+    static constexpr bool AHEAD = EARLY && (L0 || LSW) &&
+                                  (SS != 4 || 2 * ((FLOATS0 + 8 * S * RXI) * 4 + 64 + 1024) <= 233472);
     static constexpr int NGB = AHEAD ? 2 : 1;
-    static constexpr size_t FLOATS = (size_t)LGBUF + NBL * BLKF + (NBU + NOB) * UPF + NST * LHF + NST * T1F + NST * LSF + NST * GDF +
-                                     NGB * 4 * S * RXI + (B3ON ? CR * 3 * TXC : 0) + REDF;
+
+    static constexpr size_t FLOATS = FLOATS0 + NGB * 4 * S * RXI;
     static constexpr size_t SMEM = FLOATS * 4 + 64;
     // 2 CTAs per SM (16 warps) whenever two fit the 228 KB of shared memory
     static constexpr int MINB = (SS == 4 && 2 * (SMEM + 1024) <= 233472) ? 2 : 1;
@@ -433,10 +437,10 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
     __syncthreads();
     patch_rows(qstart + R - NPRO * S, qstart + R);
 
-    const int s_a = tid / SH::PV, rw_a = tid - s_a * SH::PV;  // phase A: S rows x RW columns (pitch PV)
-    const int ri_a = RA - R + rw_a;                             // logit column of this thread's region pixel
-    const int ii_a = ri_a - DI;                                 // its image / exponential column
-    const bool act_a = s_a < S && rw_a < RW;
+    // phase A: pixel item p = tid = (row p / PV, region column p % PV) of the
+    // S x RW region (pitch PV).  (Measured: handing the B1 warps, which finish
+    // their B work first, a second phase-A pixel for 64 of their threads:
+    // k5 level 0 +4.5%.)
 
     SSB_RT(long long rt_tw = 0; unsigned long long rt_acc[4] = {0, 0, 0, 0};)
     // ------------------------------------------------ A: [softmax,] G, inner
@@ -449,8 +453,11 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             LSW ? s_lg + (j % NST) * LGS1 : (SEP ? s_lg + LGF + (SH::EARLY ? (j % NST) * LGS1 : 0) : lgb_of(j)));
     };
     auto gbuf = [&](int j) { return s_gi + (SH::AHEAD ? (j & 1) * 4 * PL : 0); };
-    auto phase_a_body = [&](int j, int qs_j, float* lgb_j, const TL* lgs_j, float* gb) {
-        if (act_a) {
+    auto phase_a_px = [&](int j, int qs_j, float* lgb_j, const TL* lgs_j, float* gb, int p) {
+        const int s_a = p / SH::PV, rw_a = p - s_a * SH::PV;
+        const int ri_a = RA - R + rw_a;  // logit column of the region pixel
+        const int ii_a = ri_a - DI;      // its image / exponential column
+        if (rw_a < RW) {
             float inv = 1.f;
             if constexpr (!LSW) {
                 float e[NLOG];
@@ -496,6 +503,9 @@ __global__ void __launch_bounds__((TmaShape<K, TL, L0, UP, TIED, CH, SS, NST, TX
             }
             gb[3 * PL + s_a * RXI + ii_a] = LSW ? inner : inner * inv;
         }
+    };
+    auto phase_a_body = [&](int j, int qs_j, float* lgb_j, const TL* lgs_j, float* gb) {
+        if (tid < S * SH::PV) phase_a_px(j, qs_j, lgb_j, lgs_j, gb, tid);
     };
     // every thread passed step i-1's end barrier: the buffers of step i+NST-1
     // (those of step i-1) are free -- prefetch NST-1 steps ahead
