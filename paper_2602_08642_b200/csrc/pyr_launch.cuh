@@ -160,12 +160,35 @@ bool prepare_bwd_tma(const BwdLevel& a0, TmaMaps& mp) {
     return ok;
 }
 
-template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false>
+// strip width of the k = 5 fp32 backward per level width: the default 60
+// own columns tile 1080p-family widths exactly; for others (c2's 256 / 128 /
+// 64 / 32) the last strip can be mostly empty -- pick the width minimising
+// strips x (own + 8 halo columns) among the instantiated 60 / 52 / 44 / 36
+inline int pick_bwd_strip(int W) {
+    static const bool off = [] {
+        const char* e = getenv("SSB_BWD_STRIP60");
+        return e && e[0] == '1';
+    }();
+    if (off) return 0;
+    const int cand[4] = {60, 52, 44, 36};
+    int best = 0;
+    long long bc = 0;
+    for (int t : cand) {
+        const long long c = (long long)((W + t - 1) / t) * (t + 8);
+        if (best == 0 || c < bc) {
+            best = t;
+            bc = c;
+        }
+    }
+    return best == 60 ? 0 : best;
+}
+
+template <int K, typename TL, bool L0, bool UP, bool TIED, bool CH = false, int TXO = 0>
 bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
-    using SH = TmaShape<K, TL, L0, UP, TIED, CH>;
+    using SH = TmaShape<K, TL, L0, UP, TIED, CH, 4, 2, TXO>;
     TmaMaps mp;
-    if (!prepare_bwd_tma<K, TL, L0, UP, TIED, CH>(a0, mp)) return false;
-    auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED, CH>;
+    if (!prepare_bwd_tma<K, TL, L0, UP, TIED, CH, 4, 2, TXO>(a0, mp)) return false;
+    auto kern = k_pyr_bwd_tma<K, TL, L0, UP, TIED, CH, 4, 2, TXO>;
     static std::atomic<unsigned long long> attr_mask{0};
     smem_attr_once(attr_mask, (const void*)kern, (int)SH::SMEM);
     BwdLevel a = a0;
@@ -179,6 +202,14 @@ bool launch_bwd_tma(const BwdLevel& a0, cudaStream_t s) {
 template <int K, typename TL, typename T, bool L0, bool UP, bool TIED, bool PREV>
 void launch_bwd_one(const BwdLevel& a0, int B, cudaStream_t s) {
     if constexpr (std::is_same<T, float>::value && !std::is_same<TL, double>::value && !PREV) {
+        if constexpr (K == 5 && std::is_same<TL, float>::value) {
+            switch (pick_bwd_strip(a0.W)) {
+                case 52: if (launch_bwd_tma<K, TL, L0, UP, TIED, false, 52>(a0, s)) return; break;
+                case 44: if (launch_bwd_tma<K, TL, L0, UP, TIED, false, 44>(a0, s)) return; break;
+                case 36: if (launch_bwd_tma<K, TL, L0, UP, TIED, false, 36>(a0, s)) return; break;
+                default: break;
+            }
+        }
         if (launch_bwd_tma<K, TL, L0, UP, TIED>(a0, s)) return;
     }
     using SH = BwdShape<K, UP, PREV, T>;
@@ -482,6 +513,12 @@ int run_backward_chain(const ssb_pyr_desc* d, const PyrPlan& p, const ssb_pyr_bw
             default: break;
         }
 #endif
+        switch (pick_bwd_strip(p.W)) {
+            case 52: return run_backward_chain_ss<K, TL, TIED, 4, 2, 52>(d, p, io, tape, ws, s);
+            case 44: return run_backward_chain_ss<K, TL, TIED, 4, 2, 44>(d, p, io, tape, ws, s);
+            case 36: return run_backward_chain_ss<K, TL, TIED, 4, 2, 36>(d, p, io, tape, ws, s);
+            default: break;
+        }
     }
     if constexpr (K == 7 && std::is_same<TL, __nv_bfloat16>::value) {
 #ifdef SSB_BWD_VARIANTS
