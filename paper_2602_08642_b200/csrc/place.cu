@@ -386,6 +386,7 @@ struct PlaceArgs {
     uint64_t seed;
     int64_t frame0;
     double budget, lam, temp, floor_;
+    float gainf;  // relaxed fast path: (float)(2 lam / (2 lam - 1))
     const float* scores;
     const float* bank;
     const double* stat;
@@ -393,24 +394,28 @@ struct PlaceArgs {
     uint8_t *taken, *drawn;
 };
 
-// one pixel: the allocation decision and the estimator outputs
+// one pixel: the allocation decision and the estimator outputs (pending:
+// the float32 fast path could not decide it and the caller runs it again
+// with the float64 path -- compacted across the warp, see k_place)
 struct PlacePx {
     float noisy[3], grad[3], spp;
     uint8_t taken, drawn;
+    bool pending;
 };
 
-template <int VAR, bool S2>
+template <int VAR, bool S2, bool DEFER = false>
 __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double ssum, double uni, double adaptive,
                                             uint64_t hf, int x, int y, float score, const float* bp, long long hw,
                                             const double* t2) {
     PlacePx o;
+    o.pending = false;
     // key_hash with the (seed, frame) prefix hoisted: rng.py:43-48
     uint64_t h = mix64(hf ^ ((uint64_t)x * kGold + kGold));
     h = mix64(h ^ ((uint64_t)y * kGold + kGold));
     h = mix64(h ^ kGold);  // stream STREAM_ALLOC = 0
     const double k53 = (double)(h >> 11);  // u = k53 * 2^-53 exactly
     const int S = S2 ? 2 : a.S;
-    if constexpr (VAR == SSB_VAR_STOCHASTIC) {
+    if constexpr (VAR == SSB_VAR_STOCHASTIC || VAR == SSB_VAR_RELAXED) {
         // float32 fast path with a rigorous bound on |spp32 - spp64|.  The
         // exponent x = (score - max) log2 e is carried as x_hi + x_lo (TwoSum
         // of the difference, split product with the float log2 e and its
@@ -433,13 +438,54 @@ __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double
         const float fl32 = floorf(spp32), fr32 = spp32 - fl32;
         const float err = fmaf(1.5e-6f, spp32, 1e-7f);
         const float u32 = (float)(h >> 11) * 0x1.0p-53f;  // |u32 - u| <= 6e-8
-        if (fr32 > err && fr32 < 1.0f - err && fabsf(u32 - fr32) > err + 1e-7f && spp32 < 8388608.0f) {
+        // relaxed (estimators.py:101-113): drawn = u >= 1 - frac; the values
+        // take the fast path where they depend on spp alone -- not drawn
+        // (contrib 0) or the ramp clipped at 1 (contrib = hold * gain); the
+        // linear part of the ramp (~frac / lam of the pixels, its value
+        // sensitive to frac) and every ambiguous decision go to float64
+        bool relaxed_fast = false, rdrawn = false;
+        if constexpr (VAR == SSB_VAR_RELAXED) {
+            const float lamf = (float)a.lam;
+            const float dd = (u32 + fr32) - 1.0f;  // u - (1 - frac)
+            const float md = err + 2e-7f;
+            rdrawn = dd > 0.0f;
+            relaxed_fast = fr32 > err && fr32 < 1.0f - err && fabsf(dd) > md && spp32 < 8388608.0f &&
+                           (!rdrawn || fmaf(lamf, dd, -fr32) > (lamf + 1.0f) * md + 1e-6f);
+        }
+        if constexpr (VAR == SSB_VAR_RELAXED) {
+            if (relaxed_fast) {
+                o.taken = o.drawn = rdrawn;
+                o.spp = a.spp ? (float)(uni + adaptive * exp_neg((double)score - m, t2)) : spp32;  // (optional output)
+                const int idx = (int)(fl32 < (float)(S - 1) ? fl32 : (float)(S - 1));
+                const float sden = spp32 > (float)a.floor_ ? spp32 : (float)a.floor_;
+                const float rs = __frcp_rn(sden);  // == 1.0f / sden (both correctly rounded)
+                const float gain = a.gainf;  // 2 lam / (2 lam - 1), rounded once on the host
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float acc = 0.0f;
+                    if (S2) {
+                        if (idx == 1) acc = bp[(0 * 3 + c) * hw];
+                    } else {
+                        for (int j = 0; j < idx; ++j) acc += bp[(j * 3 + c) * hw];
+                    }
+                    if (rdrawn) acc += bp[(idx * 3 + c) * hw] * gain;
+                    const float nv = acc * rs;
+                    o.noisy[c] = nv > 0.0f ? nv : 0.0f;
+                    o.grad[c] = -nv * rs;
+                }
+                return o;
+            }
+            if constexpr (DEFER) {
+                o.pending = true;
+                return o;
+            }
+        } else if (fr32 > err && fr32 < 1.0f - err && fabsf(u32 - fr32) > err + 1e-7f && spp32 < 8388608.0f) {
             const bool tk = u32 < fr32;
             o.taken = o.drawn = tk;
             o.spp = a.spp ? (float)(uni + adaptive * exp_neg((double)score - m, t2)) : spp32;  // (optional output)
             const int idx = (int)(fl32 < (float)(S - 1) ? fl32 : (float)(S - 1));
             const float sden = spp32 > (float)a.floor_ ? spp32 : (float)a.floor_;
-            const float rs = 1.0f / sden;
+            const float rs = __frcp_rn(sden);  // == 1.0f / sden (both correctly rounded)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 float acc = 0.0f;
@@ -471,7 +517,7 @@ __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double
         o.taken = o.drawn = tk;
         // the estimator value only feeds float32 outputs: float32 from here
         const float sden = (float)(spp > a.floor_ ? spp : a.floor_);
-        const float rs = 1.0f / sden;
+        const float rs = __frcp_rn(sden);  // == 1.0f / sden (both correctly rounded)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             float acc = 0.0f;
@@ -529,6 +575,9 @@ __global__ void __launch_bounds__(kPlThreads) k_place_finish(const double* __res
     }
 }
 
+template <bool VEC>
+__device__ __forceinline__ void store_px(const PlaceArgs& a, int b, long long hw, long long p0, const PlacePx* px);
+
 template <int VAR, bool S2, bool VEC>
 __global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
     __shared__ double t2[64];
@@ -543,21 +592,65 @@ __global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
     const float* bankb = a.bank + (long long)b * S * 3 * hw;
     constexpr int NPX = VEC ? 4 : 1;
     const long long p0 = ((long long)blockIdx.x * kPlThreads + threadIdx.x) * NPX;
-    if (p0 >= hw) return;
-    const int y = (int)(p0 / a.W), x0 = (int)(p0 - (long long)y * a.W);
-    float sc[NPX];
-    if constexpr (VEC) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(a.scores + (long long)b * hw + p0));
-        sc[0] = v.x;
-        sc[1] = v.y;
-        sc[2] = v.z;
-        sc[3] = v.w;
-    } else {
-        sc[0] = a.scores[(long long)b * hw + p0];
-    }
+    // relaxed: the float64 fallback (the linear part of the ramp, ~frac / lam
+    // of the pixels) would run divergently in almost every warp -- defer it,
+    // then run the warp's deferred pixels together after the stores
+    constexpr bool DEFER = VAR == SSB_VAR_RELAXED;
+    const bool act = p0 < hw;
+    if (!DEFER && !act) return;
     PlacePx px[NPX];
 #pragma unroll
-    for (int j = 0; j < NPX; ++j) px[j] = place_px<VAR, S2>(a, m, ssum, uni, adaptive, hf, x0 + j, y, sc[j], bankb + p0 + j, hw, t2);
+    for (int j = 0; j < NPX; ++j) px[j].pending = false;
+    if (act) {
+        const int y = (int)(p0 / a.W), x0 = (int)(p0 - (long long)y * a.W);
+        float sc[NPX];
+        if constexpr (VEC) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(a.scores + (long long)b * hw + p0));
+            sc[0] = v.x;
+            sc[1] = v.y;
+            sc[2] = v.z;
+            sc[3] = v.w;
+        } else {
+            sc[0] = a.scores[(long long)b * hw + p0];
+        }
+#pragma unroll
+        for (int j = 0; j < NPX; ++j)
+            px[j] = place_px<VAR, S2, DEFER>(a, m, ssum, uni, adaptive, hf, x0 + j, y, sc[j], bankb + p0 + j, hw, t2);
+        store_px<VEC>(a, b, hw, p0, px);
+    }
+    if constexpr (DEFER) {
+        __shared__ int s_def[kPlThreads / 32][32 * NPX];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        unsigned pend = 0;
+#pragma unroll
+        for (int j = 0; j < NPX; ++j) pend |= px[j].pending ? 1u << j : 0u;
+        const int cnt = __popc(pend);
+        int inc = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += n;
+        }
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        int w = inc - cnt;
+#pragma unroll
+        for (int j = 0; j < NPX; ++j)
+            if (pend & (1u << j)) s_def[wid][w++] = (int)(p0 + j);
+        __syncwarp();
+        for (int e = lane; e < total; e += 32) {
+            const long long q = s_def[wid][e];
+            const int yq = (int)(q / a.W), xq = (int)(q - (long long)yq * a.W);
+            PlacePx r[1];
+            r[0] = place_px<VAR, S2>(a, m, ssum, uni, adaptive, hf, xq, yq, a.scores[(long long)b * hw + q], bankb + q,
+                                     hw, t2);
+            store_px<false>(a, b, hw, q, r);
+        }
+    }
+}
+
+// the outputs of NPX = 4 (VEC) or 1 horizontally adjacent pixels from p0
+template <bool VEC>
+__device__ __forceinline__ void store_px(const PlaceArgs& a, int b, long long hw, long long p0, const PlacePx* px) {
     float* nz = a.noisy + (long long)b * 3 * hw + p0;
     float* gr = a.grad ? a.grad + (long long)b * 3 * hw + p0 : nullptr;
     if constexpr (VEC) {
@@ -774,6 +867,7 @@ int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place
     a.frame0 = d->frame0;
     a.budget = d->budget;
     a.lam = cfg ? cfg->lam : 10.0;
+    a.gainf = (float)(2.0f * (float)a.lam / (2.0f * (float)a.lam - 1.0f));
     a.temp = cfg ? cfg->gumbel_temp : 1.0;
     a.floor_ = cfg ? cfg->density_floor : 1e-8;
     a.scores = io->scores;
