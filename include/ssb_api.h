@@ -234,6 +234,21 @@ typedef struct ssb_place_io {
 int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place_io* io, void* workspace,
               ssb_stream_t stream);
 
+/* Small frames (BASELINE c0): the inference path -- the stochastic fused
+ * placement (as ssb_place_fused, capacity 2: identical noisy) followed by
+ * reconstruct_core (pyramid.py:292-345) with demod, native blend, 3
+ * channels, float32 -- in ONE cooperative kernel with grid-wide barriers
+ * between the stages (the partial pairs and their fold, place, one pooled
+ * level per barrier, one forward level per barrier) instead of eight
+ * dependent launches.  logits[l] (B, k^2 (+4 below the top level), H_l, W_l).
+ * Returns SSB_EUNSUPPORTED outside B <= 8, B*H*W <= 2^20, W % 4 == 0, k in
+ * {3,5,7} (the caller then runs ssb_place_fused + ssb_pyr_forward).  No tape:
+ * inference only. */
+int ssb_infer_small_workspace_bytes(int B, int H, int W, int levels, size_t* bytes);
+int ssb_infer_small(const ssb_place_desc* pd, const float* scores, const float* bank, const float* demod,
+                    int levels, int ksize, const float* const* logits, float* noisy, float* out,
+                    void* workspace, ssb_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * Row bands: one 8K frame split into G row bands,
  * one per GPU, exchanging only r rows of each pooled level and one Lhat row

@@ -18,6 +18,7 @@ SSB_F32, SSB_BF16, SSB_F64 = 0, 1, 2
 SSB_BLEND_NATIVE, SSB_BLEND_TIED = 0, 1
 RULES = {"stochastic": 0, "relaxed": 1, "gumbel": 2}
 VARIANTS = {"stochastic": 0, "relaxed": 1, "straight-through": 2, "gumbel": 3}
+SSB_EUNSUPPORTED = -3  # ssb_api.h
 
 # every symbol include/ssb_api.h declares (tests check the .so exports them all)
 EXPORTS = (
@@ -31,6 +32,7 @@ EXPORTS = (
     "ssb_score_grad_workspace_bytes", "ssb_score_grad",
     "ssb_tonemap", "ssb_tonemap_backward", "ssb_losses_workspace_bytes", "ssb_losses", "ssb_epilogue",
     "ssb_pyr_forward_level", "ssb_pool2_strided", "ssb_halo_put", "ssb_flag_wait", "ssb_enable_peer",
+    "ssb_infer_small_workspace_bytes", "ssb_infer_small",
 )
 
 vp = C.c_void_p
@@ -144,6 +146,8 @@ def load(build_if_missing: bool = False):
             "ssb_estimate": (C.c_int, [P(EstimateDesc)] + [vp] * 11),
             "ssb_place_fused": (C.c_int, [P(PlaceDesc)] + [vp] * 7),
             "ssb_place": (C.c_int, [P(PlaceDesc), P(PlaceCfg), P(PlaceIO), vp, vp]),
+            "ssb_infer_small_workspace_bytes": (C.c_int, [C.c_int] * 4 + [P(C.c_size_t)]),
+            "ssb_infer_small": (C.c_int, [P(PlaceDesc), vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
             "ssb_pyr_forward_level": (C.c_int, [P(PyrLevelDesc)] + [vp] * 6),
             "ssb_pool2_strided": (C.c_int, [C.c_int] * 5 + [vp, C.c_longlong, C.c_longlong, vp, vp,
                                                              C.c_longlong, C.c_longlong, vp]),

@@ -8,7 +8,11 @@
 #include <string>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ssb {
 void set_error(const std::string& msg);
@@ -292,6 +296,16 @@ __global__ void k_density_apply(long long n, const double* scores, const double*
 //    the bank read (S = 2 specialised) and the estimator.
 constexpr int kPlThreads = 256;
 constexpr int kPlParts = 512;  // max partial pairs per frame
+
+// partial pairs per frame of `units` score groups (float4s, or scalars):
+// ~4 groups per thread, but at least 128 pairs where the frame has a group
+// per thread for them (small frames: the pass spreads over the SMs)
+__host__ __device__ inline int place_nparts(long long units) {
+    long long np = (units + kPlThreads * 4 - 1) / (kPlThreads * 4);
+    const long long lo = units / kPlThreads < 128 ? units / kPlThreads : 128;
+    np = np < lo ? lo : np;
+    return (int)(np < 1 ? 1 : (np > kPlParts ? kPlParts : np));
+}
 
 // exp(d) for d <= 0 in float64, ~3 ulp (the frame softmax's terms; not the
 // compat normalize_density, which keeps libdevice exp): d = (64 n + j) ln2/64
@@ -698,6 +712,238 @@ static void launch_reductions(int B, long long n, const TS* scores, double* pmax
     (void)sgrid;
 }
 
+
+// ---------------------------------------------------------------------------
+// Small frames (BASELINE c0: one 256^2 frame): the whole inference path --
+// placement (the partial pairs, their fold, place), the pooled pyramid and the
+// forward levels coarse to fine -- in ONE cooperative kernel with grid-wide
+// barriers between the stages, instead of eight dependent launches whose fixed
+// cost dominates at this size.  Placement: the same partition into partial
+// pairs, the same fold and the same place_px as ssb_place (identical noisy);
+// the pyramid: k_pool2's arithmetic per level; the forward per pixel from
+// global memory (L2-resident at these sizes) in k_pyr_fwd's form, native
+// blend, float32 (pyramid.py:292-345).
+constexpr int kInfMaxB = 8;
+struct InferArgs {
+    PlaceArgs pa;  // stochastic placement, pa.stat unused
+    int nparts, L;
+    double* parts;  // B x kPlParts x 2
+    const float* demod;
+    const float* logits[SSB_MAX_LEVELS];
+    int hl[SSB_MAX_LEVELS], wl[SSB_MAX_LEVELS], nlog[SSB_MAX_LEVELS];
+    float* x0;                      // (B,3,H,W) noisy / max(d, floor)
+    float* lv[SSB_MAX_LEVELS];      // pooled levels, l >= 1
+    float* lh[SSB_MAX_LEVELS];      // Lhat, l >= 1
+    float* out;                     // (B,3,H,W)
+};
+
+// the k x k gather + upsample of one level pixel (k_pyr_fwd's arithmetic)
+template <int K>
+__device__ __forceinline__ void inf_fwd_px(const InferArgs& a, int l, int b, int y, int x) {
+    constexpr int R = K / 2, NT = K * K;
+    const int H = a.hl[l], W = a.wl[l];
+    const bool up = l + 1 < a.L;
+    const unsigned hw = (unsigned)H * (unsigned)W;
+    const float* lg = a.logits[l] + (size_t)b * a.nlog[l] * hw + (unsigned)y * (unsigned)W + (unsigned)x;
+    float e[NT + 4];
+    float m = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < NT + 4; ++t) {
+        e[t] = (t < NT || up) ? __ldg(lg + (size_t)t * hw) : -INFINITY;
+        m = fmaxf(m, e[t]);
+    }
+    const float mk = prep_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int t = 0; t < NT + 4; ++t) {
+        e[t] = (t < NT || up) ? softmax_exp(e[t], mk) : 0.f;
+        sum += e[t];
+    }
+    const float inv = frcp(sum);
+    const float* src = l == 0 ? a.x0 + (size_t)b * 3 * hw : a.lv[l] + (size_t)b * 3 * hw;
+    int ro[K], co[K];
+#pragma unroll
+    for (int d = 0; d < K; ++d) {
+        ro[d] = clampi(y + d - R, 0, H - 1) * W;
+        co[d] = clampi(x + d - R, 0, W - 1);
+    }
+    int cy0 = 0, cy1 = 0, cx0 = 0, cx1 = 0, Wc = 1;
+    const float* lhc = nullptr;
+    if (up) {
+        const int Hc = a.hl[l + 1];
+        Wc = a.wl[l + 1];
+        cy0 = min(y >> 1, Hc - 1);
+        cy1 = min((y + 1) >> 1, Hc - 1);
+        cx0 = min(x >> 1, Wc - 1);
+        cx1 = min((x + 1) >> 1, Wc - 1);
+        lhc = a.lh[l + 1] + (size_t)b * 3 * Hc * Wc;
+    }
+    const unsigned o = (unsigned)y * (unsigned)W + (unsigned)x;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float* sc = src + (size_t)c * hw;
+        float acc = 0.f;
+#pragma unroll
+        for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < K; ++dx) acc += e[dy * K + dx] * sc[ro[dy] + co[dx]];
+        if (up) {
+            const float* cp = lhc + (size_t)c * a.hl[l + 1] * Wc;
+            acc += e[NT + 0] * cp[cy0 * Wc + cx0];
+            acc += e[NT + 1] * cp[cy0 * Wc + cx1];
+            acc += e[NT + 2] * cp[cy1 * Wc + cx0];
+            acc += e[NT + 3] * cp[cy1 * Wc + cx1];
+        }
+        acc *= inv;
+        if (l == 0) {
+            acc *= demod_clamp(a.demod[((size_t)b * 3 + c) * hw + o]);
+            a.out[((size_t)b * 3 + c) * hw + o] = acc;
+        } else {
+            a.lh[l][((size_t)b * 3 + c) * hw + o] = acc;
+        }
+    }
+}
+
+// one level-l pixel (Y, X) = k_pool2 of its 2x2 children at level l - 1
+__device__ __forceinline__ void inf_pool_px(const InferArgs& a, int l, int b, int Y, int X) {
+    const int H = a.hl[l - 1], W = a.wl[l - 1], Wc = a.wl[l];
+    const float* in = (l == 1 ? a.x0 : a.lv[l - 1]) + (size_t)b * 3 * H * W;
+    const int yb = 2 * Y, xb = 2 * X;
+    const bool hy = yb + 1 < H, hx = xb + 1 < W;
+    const float rcnt = (hy && hx) ? 0.25f : ((hy || hx) ? 0.5f : 1.f);
+    const long long o00 = (long long)yb * W + xb;
+    const long long o01 = hx ? o00 + 1 : o00, o10 = hy ? o00 + W : o00, o11 = hy ? o01 + W : o01;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float* p = in + (size_t)c * H * W;
+        const float s01 = hx ? p[o01] : 0.f, s10 = hy ? p[o10] : 0.f, s11 = (hx && hy) ? p[o11] : 0.f;
+        a.lv[l][((size_t)b * 3 + c) * a.hl[l] * Wc + (long long)Y * Wc + X] = ((p[o00] + s01) + (s10 + s11)) * rcnt;
+    }
+}
+
+#ifdef SSB_INF_TIMING
+static __device__ unsigned long long g_inf_t[16];
+#define SSB_INF_T(k) \
+    if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_inf_t[k]));
+#else
+#define SSB_INF_T(k)
+#endif
+template <int K>
+__global__ void __launch_bounds__(kPlThreads, 2) k_infer_small(InferArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    SSB_INF_T(0)
+    __shared__ double t2[64];
+    __shared__ double s_ms[kInfMaxB][2];
+    __shared__ double bm;
+    load_exp_table(t2);
+    __syncthreads();
+    const PlaceArgs& pa = a.pa;
+    const int B = pa.B;
+    const long long hw = (long long)pa.H * pa.W;
+    const long long gtid = (long long)blockIdx.x * kPlThreads + threadIdx.x, gthreads = (long long)gridDim.x * kPlThreads;
+    // 1. partial pairs: virtual block j of frame b = k_place_partials<VEC> block j
+    for (int vb = blockIdx.x; vb < B * a.nparts; vb += gridDim.x) {
+        const int b = vb / a.nparts, j = vb - b * a.nparts;
+        const float4* p4 = reinterpret_cast<const float4*>(pa.scores + (long long)b * hw);
+        const long long t0 = (long long)j * kPlThreads + threadIdx.x, step = (long long)a.nparts * kPlThreads;
+        float mf = -INFINITY;
+        for (long long g = t0; g < (hw >> 2); g += step) {
+            const float4 v = __ldg(p4 + g);
+            mf = fmaxf(fmaxf(mf, fmaxf(v.x, v.y)), fmaxf(v.z, v.w));
+        }
+        const double mb = block_reduce((double)mf, true);
+        if (threadIdx.x == 0) bm = mb;
+        __syncthreads();
+        const double m = bm;
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (long long g = t0; g < (hw >> 2); g += step) {
+            const float4 v = __ldg(p4 + g);
+            s4[0] += exp_neg((double)v.x - m, t2);
+            s4[1] += exp_neg((double)v.y - m, t2);
+            s4[2] += exp_neg((double)v.z - m, t2);
+            s4[3] += exp_neg((double)v.w - m, t2);
+        }
+        const double sb = block_reduce((s4[0] + s4[1]) + (s4[2] + s4[3]), false);
+        if (threadIdx.x == 0) {
+            a.parts[2 * ((long long)b * kPlParts + j)] = m;
+            a.parts[2 * ((long long)b * kPlParts + j) + 1] = sb;
+        }
+    }
+    grid.sync();
+    SSB_INF_T(1)
+    // 2. every CTA folds each frame's pairs (k_place_finish's order), then places
+    for (int b = 0; b < B; ++b) {
+        const double* pb = a.parts + 2 * (long long)b * kPlParts;
+        double m = -INFINITY;
+        for (int k = threadIdx.x; k < a.nparts; k += kPlThreads) m = fmax(m, pb[2 * k]);
+        const double mm = block_reduce(m, true);
+        if (threadIdx.x == 0) bm = mm;
+        __syncthreads();
+        double sl = 0.0;
+        for (int k = threadIdx.x; k < a.nparts; k += kPlThreads) sl += pb[2 * k + 1] * exp_neg(pb[2 * k] - bm, t2);
+        const double ss = block_reduce(sl, false);
+        if (threadIdx.x == 0) {
+            s_ms[b][0] = bm;
+            s_ms[b][1] = ss;
+        }
+        __syncthreads();
+    }
+    const double uni = 0.125 * pa.budget;
+    for (long long it = gtid; it < B * (hw >> 2); it += gthreads) {
+        const int b = (int)(it / (hw >> 2));
+        const long long p0 = (it - (long long)b * (hw >> 2)) * 4;
+        const double m = s_ms[b][0], ssum = s_ms[b][1];
+        const double adaptive = (1.0 - 0.125) * pa.budget * (double)hw / ssum;
+        const uint64_t hf = mix64(mix64(pa.seed + kGold) ^ ((uint64_t)(pa.frame0 + b) * kGold + kGold));
+        const float* bankb = pa.bank + (long long)b * 2 * 3 * hw;
+        const int y = (int)(p0 / pa.W), x0 = (int)(p0 - (long long)y * pa.W);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(pa.scores + (long long)b * hw + p0));
+        const float sc[4] = {v.x, v.y, v.z, v.w};
+        PlacePx px[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            px[j] = place_px<SSB_VAR_STOCHASTIC, true>(pa, m, ssum, uni, adaptive, hf, x0 + j, y, sc[j], bankb + p0 + j,
+                                                       hw, t2);
+        store_px<true>(pa, b, hw, p0, px);
+        // the demodulated input of the pyramid (k_pool2's / the forward's x0)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float4 d = __ldg(reinterpret_cast<const float4*>(a.demod + ((long long)b * 3 + c) * hw + p0));
+            *reinterpret_cast<float4*>(a.x0 + ((long long)b * 3 + c) * hw + p0) =
+                make_float4(fdiv(px[0].noisy[c], demod_clamp(d.x)), fdiv(px[1].noisy[c], demod_clamp(d.y)),
+                            fdiv(px[2].noisy[c], demod_clamp(d.z)), fdiv(px[3].noisy[c], demod_clamp(d.w)));
+        }
+    }
+    grid.sync();
+    SSB_INF_T(2)
+    // 3. the pooled pyramid, one level per barrier (measured: a thread per
+    // level-2 pixel pooling its four level-1 children first is slower -- its
+    // dependent loads serialise)
+    for (int l = 1; l < a.L; ++l) {
+        const long long n = (long long)a.hl[l] * a.wl[l];
+        for (long long it = gtid; it < B * n; it += gthreads) {
+            const int b = (int)(it / n);
+            const int q = (int)(it - (long long)b * n);
+            inf_pool_px(a, l, b, q / a.wl[l], q % a.wl[l]);
+        }
+        grid.sync();
+        SSB_INF_T(3)
+    }
+    // 4. the forward, coarse to fine
+    for (int l = a.L - 1; l >= 0; --l) {
+        const long long n = (long long)a.hl[l] * a.wl[l];
+        for (long long it = gtid; it < B * n; it += gthreads) {
+            const int b = (int)(it / n);
+            const int q = (int)(it - (long long)b * n);
+            inf_fwd_px<K>(a, l, b, q / a.wl[l], q % a.wl[l]);
+        }
+        if (l > 0) grid.sync();
+        if (l > 0) {
+            SSB_INF_T(4 + (a.L - 1 - l))
+        }
+    }
+    SSB_INF_T(12)
+}
 }  // namespace ssb
 
 using namespace ssb;
@@ -847,8 +1093,7 @@ int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place
     // partial pairs: ~4 float4 groups (16 scores) per thread, at most kPlParts
     // per frame (measured: 1 group per thread and 2048 pairs is no faster)
     const long long units = vec ? n / 4 : n;
-    long long np = (units + kPlThreads * 4 - 1) / (kPlThreads * 4);
-    np = np < 1 ? 1 : (np > kPlParts ? kPlParts : np);
+    const long long np = place_nparts(units);
     double* parts = (double*)workspace;  // B x kPlParts x 2 doubles + B x 2 (inside the density workspace)
     dim3 pgrid((unsigned)np, d->B);
     if (vec) SSB_LAUNCH(s, k_place_partials<true><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np));
@@ -907,4 +1152,112 @@ int ssb_place_fused(const ssb_place_desc* d, const float* scores, const float* b
     return ssb_place(d, nullptr, &io, workspace, stream);
 }
 
+
+static size_t inf_al(size_t n) { return (n + 255) & ~(size_t)255; }
+
+#ifdef SSB_INF_TIMING
+int ssb_debug_inf_times(unsigned long long* out16) {
+    return cudaMemcpyFromSymbol(out16, g_inf_t, 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -2;
+}
+#endif
+
+int ssb_infer_small_workspace_bytes(int B, int H, int W, int levels, size_t* bytes) {
+    if (!bytes || B < 1 || H < 1 || W < 1 || levels < 1 || levels > SSB_MAX_LEVELS) {
+        set_error("ssb_infer_small_workspace_bytes: bad arguments");
+        return SSB_EINVAL;
+    }
+    size_t t = inf_al((size_t)B * kPlParts * 2 * sizeof(double)) + inf_al((size_t)B * 3 * H * W * sizeof(float));
+    int h = H, w = W;
+    for (int l = 1; l < levels; ++l) {
+        h = (h + 1) / 2;
+        w = (w + 1) / 2;
+        t += 2 * inf_al((size_t)B * 3 * h * w * sizeof(float));
+    }
+    *bytes = t;
+    return SSB_OK;
+}
+
+int ssb_infer_small(const ssb_place_desc* pd, const float* scores, const float* bank, const float* demod,
+                    int levels, int ksize, const float* const* logits, float* noisy, float* out, void* workspace,
+                    ssb_stream_t stream) {
+    if (!pd || !scores || !bank || !demod || !logits || !noisy || !out || !workspace || levels < 1 ||
+        levels > SSB_MAX_LEVELS || pd->B < 1 || pd->H < 1 || pd->W < 1 || !(pd->budget > 0.0)) {
+        set_error("ssb_infer_small: bad arguments");
+        return SSB_EINVAL;
+    }
+    for (int l = 0; l < levels; ++l)
+        if (!logits[l]) {
+            set_error("ssb_infer_small: missing logits");
+            return SSB_EINVAL;
+        }
+    const long long n = (long long)pd->H * pd->W;
+    if (pd->variant != SSB_VAR_STOCHASTIC || pd->capacity != 2 || pd->W % 4 != 0 || pd->B > kInfMaxB ||
+        (ksize != 3 && ksize != 5 && ksize != 7) || n * pd->B > (1ll << 20)) {
+        set_error("ssb_infer_small: unsupported (stochastic, capacity 2, W % 4 == 0, <= 2^20 pixels, k 3/5/7)");
+        return SSB_EUNSUPPORTED;
+    }
+    InferArgs a{};
+    a.pa.B = pd->B;
+    a.pa.H = pd->H;
+    a.pa.W = pd->W;
+    a.pa.S = 2;
+    a.pa.variant = SSB_VAR_STOCHASTIC;
+    a.pa.seed = pd->seed;
+    a.pa.frame0 = pd->frame0;
+    a.pa.budget = pd->budget;
+    a.pa.lam = 10.0;
+    a.pa.temp = 1.0;
+    a.pa.floor_ = 1e-8;
+    a.pa.scores = scores;
+    a.pa.bank = bank;
+    a.pa.noisy = noisy;
+    const long long units = n / 4;
+    a.nparts = place_nparts(units);
+    a.L = levels;
+    a.demod = demod;
+    char* w = (char*)workspace;
+    a.parts = (double*)w;
+    w += inf_al((size_t)pd->B * kPlParts * 2 * sizeof(double));
+    a.x0 = (float*)w;
+    w += inf_al((size_t)pd->B * 3 * n * sizeof(float));
+    a.hl[0] = pd->H;
+    a.wl[0] = pd->W;
+    for (int l = 0; l < levels; ++l) {
+        if (l > 0) {
+            a.hl[l] = (a.hl[l - 1] + 1) / 2;
+            a.wl[l] = (a.wl[l - 1] + 1) / 2;
+            const size_t sz = inf_al((size_t)pd->B * 3 * a.hl[l] * a.wl[l] * sizeof(float));
+            a.lv[l] = (float*)w;
+            w += sz;
+            a.lh[l] = (float*)w;
+            w += sz;
+        }
+        a.logits[l] = logits[l];
+        a.nlog[l] = ksize * ksize + (l + 1 < levels ? 4 : 0);
+    }
+    a.out = out;
+    cudaStream_t s = (cudaStream_t)stream;
+    const void* kern = ksize == 3 ? (const void*)k_infer_small<3>
+                                  : (ksize == 5 ? (const void*)k_infer_small<5> : (const void*)k_infer_small<7>);
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPlThreads, 0);
+    if (per_sm < 1) {
+        set_error("ssb_infer_small: no co-resident CTA");
+        return SSB_ECUDA;
+    }
+    // one thread per level-0 pixel for the forward stage, at most what is
+    // co-resident
+    const long long want = (pd->B * n + kPlThreads - 1) / kPlThreads;
+    const long long cap = (long long)nsm * per_sm;
+    const unsigned grid = (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
+    void* args[] = {&a};
+    SSB_LAUNCH(s, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kPlThreads), args, 0, s));
+    return cuda_check("ssb_infer_small");
+}
 }  // extern "C"

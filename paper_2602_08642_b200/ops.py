@@ -601,6 +601,54 @@ def place_fused(scores, bank, budget: float, seed: int = 0, frame0: int = 0, noi
     return r["noisy"], r["spp"], r["taken"]
 
 
+def infer(scores, bank, demod, logits, budget: float, *, ksize, seed: int = 0, frame0: int = 0,
+          noisy=None, out=None, workspace=None):
+    """The inference path of one (batch of) frame(s): the stochastic fused
+    placement, then reconstruct_core with demod (density.py:55-65,209-233;
+    estimators.py:90-149; pyramid.py:292-345), float32, native blend.  Small
+    frames (B*H*W <= 2^20, bank capacity 2, W % 4 == 0) run as ONE cooperative
+    kernel (``ssb_infer_small``: noisy identical to ``place_fused``, the
+    output within float32 rounding of ``pyramid_forward``); others as
+    place_fused + pyramid_forward.  Returns (out, noisy)."""
+    lib = _lib.load()
+    _need(scores, "scores", dtype=torch.float32)
+    B, H, W = scores.shape
+    dev = scores.device
+    if noisy is None:
+        noisy = torch.empty((B, 3, H, W), dtype=torch.float32, device=dev)
+    if out is None:
+        out = torch.empty((B, 3, H, W), dtype=torch.float32, device=dev)
+    small = (B * H * W <= (1 << 20) and bank.dim() == 5 and bank.shape[1] == 2 and W % 4 == 0 and B <= 8
+             and all(z.dtype == torch.float32 for z in logits) and ksize in (3, 5, 7))
+    if small:
+        _need(bank, "bank", dev, torch.float32)
+        _need(demod, "demod", dev, torch.float32)
+        L = len(logits)
+        shapes = level_shapes(H, W, L)
+        for l, (z, (h, w)) in enumerate(zip(logits, shapes)):
+            _need(z, f"logits[{l}]", dev, torch.float32)
+            if tuple(z.shape) != (B, logit_channels(l, L, ksize), h, w):
+                raise ValueError(f"logits[{l}] must be {(B, logit_channels(l, L, ksize), h, w)}")
+        if tuple(bank.shape) != (B, 2, 3, H, W) or tuple(demod.shape) != (B, 3, H, W):
+            raise ValueError("bank must be (B, 2, 3, H, W) and demod (B, 3, H, W)")
+        if workspace is None:
+            wb = C.c_size_t()
+            check(lib.ssb_infer_small_workspace_bytes(B, H, W, L, C.byref(wb)), "ssb_infer_small_workspace_bytes")
+            workspace = torch.empty(wb.value, dtype=torch.uint8, device=dev)
+        d = _lib.PlaceDesc(B, H, W, 2, _lib.VARIANTS["stochastic"], 0, seed & (2**64 - 1), frame0, float(budget))
+        lp = (C.c_void_p * L)(*[z.data_ptr() for z in logits])
+        with torch.cuda.device(dev):
+            rc = lib.ssb_infer_small(C.byref(d), _ptr(scores), _ptr(bank), _ptr(demod), L, ksize, lp, _ptr(noisy),
+                                     _ptr(out), _ptr(workspace), _stream(dev))
+        if rc == 0:
+            return out, noisy
+        if rc != _lib.SSB_EUNSUPPORTED:
+            check(rc, "ssb_infer_small")
+    place_fused(scores, bank, budget, seed=seed, frame0=frame0, noisy=noisy)
+    pyramid_forward(noisy, logits, demod, ksize=ksize, out=out)
+    return out, noisy
+
+
 # ---------------------------------------------------------------------------
 # temporal path (SURVEY.md 8(f) row 2): images.py warp_array / warp_backward
 
