@@ -109,8 +109,17 @@ inline int pick_segment(int strips, int H, int B) {
         const long long v = e ? atoll(e) : 148 * 8;
         return v >= 1 ? v : 148 * 8;
     }();
+    // levels of < 4 Mpx (the coarse levels of one 4K frame, c2's frames):
+    // SSB_MIN_CTAS_SMALL (experiment; default: the same target)
+    static const long long min_small = [] {
+        const char* e = getenv("SSB_MIN_CTAS_SMALL");
+        const long long v = e ? atoll(e) : 0;
+        return v >= 1 ? v : 0;
+    }();
+    const bool small = (long long)strips * 64 * H * B < (4ll << 20);
+    const long long want = (small && min_small) ? min_small : min_ctas;
     int nseg = (H + target - 1) / target;
-    while ((long long)strips * nseg * B < min_ctas && (H + nseg - 1) / nseg > 16) nseg *= 2;
+    while ((long long)strips * nseg * B < want && (H + nseg - 1) / nseg > 16) nseg *= 2;
     const int seg = (H + nseg - 1) / nseg;
     return (seg + 3) & ~3;
 }
