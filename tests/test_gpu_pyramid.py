@@ -469,3 +469,35 @@ def test_no_demod_identity_path(ops, monkeypatch, h, w, L, k, ldt):
         res.append((out, g))
     (o1, g1), (o2, g2) = res
     assert (o1 - o2).abs().max().item() <= 2e-5 * o2.abs().max().item()
+
+
+@pytest.mark.parametrize("k,ldt", [(5, "f32"), (7, "bf16")])
+def test_history_without_param_grads_matches_general_order(k, ldt, monkeypatch):
+    """History on the TMA path without parameter gradients (no g_demod, no
+    logit gradients: the temporal pass without its g_demod box) against the
+    general order -- g_noisy and g_prev."""
+    from paper_2602_08642_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(31 + k)
+    dev = torch.device("cuda")
+    H, W, L = 52, 96, 3
+    noisy = torch.rand((2, 3, H, W), device=dev, generator=g) * 2
+    demod = torch.rand((2, 3, H, W), device=dev, generator=g) * 0.99 + 0.0005
+    prev = torch.rand((2, 3, H, W), device=dev, generator=g) * 2
+    logits = [torch.randn((2, ops.logit_channels(l, L, k, has_prev=l == 0), h, w), device=dev, generator=g)
+              for l, (h, w) in enumerate(ops.level_shapes(H, W, L))]
+    if ldt == "bf16":
+        logits = [z.to(torch.bfloat16) for z in logits]
+    up = torch.randn((2, 3, H, W), device=dev, generator=g)
+    res = {}
+    for mode in ("chain", "general"):
+        if mode == "general":
+            monkeypatch.setenv("SSB_NO_CHAIN", "1")
+        _, tape = ops.pyramid_forward(noisy, logits, demod, prev, ksize=k)
+        res[mode] = ops.pyramid_backward(tape, up, want_param_grads=False)
+        monkeypatch.delenv("SSB_NO_CHAIN", raising=False)
+    a, b = res["chain"], res["general"]
+    assert a.demod is None and a.logits is None
+    tol = 2e-2 if ldt == "bf16" else 1e-5
+    for x, y in ((a.input, b.input), (a.prev, b.prev)):
+        x, y = x.double(), y.double()
+        assert torch.allclose(x, y, rtol=tol, atol=tol * y.abs().max().item()), (x - y).abs().max().item()
