@@ -501,3 +501,26 @@ def test_history_without_param_grads_matches_general_order(k, ldt, monkeypatch):
     for x, y in ((a.input, b.input), (a.prev, b.prev)):
         x, y = x.double(), y.double()
         assert torch.allclose(x, y, rtol=tol, atol=tol * y.abs().max().item()), (x - y).abs().max().item()
+
+
+def test_history_accumulate_into_tma_path():
+    """accumulate_into with history on the TMA path (the temporal pass adds
+    into the temporal channels, level 0 into the others): two accumulated
+    backward passes equal twice one pass."""
+    from paper_2602_08642_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(77)
+    dev = torch.device("cuda")
+    H, W, L, k = 40, 64, 3, 5
+    noisy = torch.rand((1, 3, H, W), device=dev, generator=g) * 2
+    demod = torch.rand((1, 3, H, W), device=dev, generator=g) * 0.99 + 0.01
+    prev = torch.rand((1, 3, H, W), device=dev, generator=g) * 2
+    logits = [torch.randn((1, ops.logit_channels(l, L, k, has_prev=l == 0), h, w), device=dev, generator=g)
+              for l, (h, w) in enumerate(ops.level_shapes(H, W, L))]
+    up = torch.randn((1, 3, H, W), device=dev, generator=g)
+    _, tape = ops.pyramid_forward(noisy, logits, demod, prev, ksize=k)
+    one = ops.pyramid_backward(tape, up)
+    acc = [torch.zeros_like(z) for z in logits]
+    ops.pyramid_backward(tape, up, accumulate_into=acc)
+    ops.pyramid_backward(tape, up, accumulate_into=acc)
+    for a, b in zip(acc, one.logits):
+        assert torch.allclose(a, 2 * b, rtol=1e-6, atol=1e-6 * b.abs().max().item())
