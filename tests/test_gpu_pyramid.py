@@ -161,7 +161,8 @@ def test_oracle_cases(ops, h, w, L, k, prev, blend, precision):
         assert_close(planar_to_hwc(g.prev), ref["g_prev"], rtol, "g_prev")
 
 
-@pytest.mark.parametrize("k,L,h,w", [(5, 3, 90, 132), (7, 4, 90, 132), (7, 4, 72, 128), (5, 3, 64, 96)])
+@pytest.mark.parametrize("k,L,h,w", [(5, 3, 90, 132), (7, 4, 90, 132), (7, 4, 72, 128), (5, 3, 64, 96),
+                                     (3, 3, 72, 128), (3, 4, 64, 112)])
 def test_bf16_logits(ops, k, L, h, w):
     """bf16 logits, fp32 radiance and accumulation: within 2e-2 of the oracle
     fed the bf16-rounded logits.  W % 8 == 0 at every level (72 x 128, 64 x
