@@ -525,3 +525,21 @@ def test_history_accumulate_into_tma_path():
     ops.pyramid_backward(tape, up, accumulate_into=acc)
     for a, b in zip(acc, one.logits):
         assert torch.allclose(a, 2 * b, rtol=1e-6, atol=1e-6 * b.abs().max().item())
+
+
+@pytest.mark.parametrize("h,w,L,k", [(48, 64, 3, 5), (37, 56, 4, 7), (30, 40, 3, 3)])
+def test_history_without_demod_vs_oracle(ops, h, w, L, k):
+    """reconstruct_core with a history and demod=None (the identity
+    demodulation on the fused kernels: level 0 by the log-sum-exp weights +
+    the temporal pass) against the float64 oracle, float32, every level."""
+    noisy, logits, dm, pv, up, ref = oracle_case(h, w, L, k, seed=h + w + k, demod=False, prev=True)
+    assert dm is None
+    dt = torch.float32
+    out, tape = ops.pyramid_forward(hwc_to_planar(noisy, dt), [hwc_to_planar(z, dt) for z in logits], None,
+                                    hwc_to_planar(pv, dt), ksize=k)
+    g = ops.pyramid_backward(tape, hwc_to_planar(up, dt))
+    assert g.demod is None
+    assert_close(planar_to_hwc(out), ref["out"], 1e-5, "out")
+    assert_close(planar_to_hwc(g.input), ref["g_input"], 1e-5, "g_input")
+    assert_close(planar_to_hwc(g.prev), ref["g_prev"], 1e-5, "g_prev")
+    assert_levels_close([planar_to_hwc(z) for z in g.logits], ref["g_logits"], 1e-5, scales=ref["scales"])
