@@ -543,3 +543,21 @@ def test_history_without_demod_vs_oracle(ops, h, w, L, k):
     assert_close(planar_to_hwc(g.input), ref["g_input"], 1e-5, "g_input")
     assert_close(planar_to_hwc(g.prev), ref["g_prev"], 1e-5, "g_prev")
     assert_levels_close([planar_to_hwc(z) for z in g.logits], ref["g_logits"], 1e-5, scales=ref["scales"])
+
+
+@pytest.mark.parametrize("h,w,L,k,prev", [(40, 64, 3, 7, False), (48, 64, 3, 5, True), (36, 56, 4, 7, True)])
+def test_peaky_logits_log_sum_exp_path(ops, h, w, L, k, prev):
+    """Large-magnitude logits (scale 8: near one-hot softmaxes, exponents far
+    below the max) on the paths that evaluate the weights from the forward's
+    log-sum-exp (k = 7, history): float32 within 1e-5 of the oracle."""
+    noisy, logits, dm, pv, up, ref = oracle_case(h, w, L, k, seed=7 * h + w, prev=prev, scale=8.0)
+    dt = torch.float32
+    out, tape = ops.pyramid_forward(hwc_to_planar(noisy, dt), [hwc_to_planar(z, dt) for z in logits],
+                                    hwc_to_planar(dm, dt), hwc_to_planar(pv, dt) if prev else None, ksize=k)
+    g = ops.pyramid_backward(tape, hwc_to_planar(up, dt))
+    assert_close(planar_to_hwc(out), ref["out"], 1e-5, "out")
+    assert_close(planar_to_hwc(g.input), ref["g_input"], 1e-5, "g_input")
+    assert_close(planar_to_hwc(g.demod), ref["g_demod"], 1e-5, "g_demod")
+    if prev:
+        assert_close(planar_to_hwc(g.prev), ref["g_prev"], 1e-5, "g_prev")
+    assert_levels_close([planar_to_hwc(z) for z in g.logits], ref["g_logits"], 1e-5, scales=ref["scales"])
