@@ -1239,12 +1239,9 @@ int ssb_infer_small(const ssb_place_desc* pd, const float* scores, const float* 
     cudaStream_t s = (cudaStream_t)stream;
     const void* kern = ksize == 3 ? (const void*)k_infer_small<3>
                                   : (ksize == 5 ? (const void*)k_infer_small<5> : (const void*)k_infer_small<7>);
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int dev = 0, nsm = 0;  // (per call: the current device's SM count)
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPlThreads, 0);
     if (per_sm < 1) {
