@@ -633,26 +633,20 @@ __global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
         store_px<VEC>(a, b, hw, p0, px);
     }
     if constexpr (DEFER) {
-        __shared__ int s_def[kPlThreads / 32][32 * NPX];
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        unsigned pend = 0;
-#pragma unroll
-        for (int j = 0; j < NPX; ++j) pend |= px[j].pending ? 1u << j : 0u;
-        const int cnt = __popc(pend);
-        int inc = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int n = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += n;
-        }
-        const int total = __shfl_sync(0xffffffffu, inc, 31);
-        int w = inc - cnt;
+        // compacted over the whole CTA (the float64 path then runs on ~2 of its
+        // 8 warps instead of once in nearly every warp); each deferred pixel is
+        // computed on its own, so the slot order does not affect any result
+        __shared__ long long s_def[kPlThreads * NPX];
+        __shared__ int s_cnt;
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
 #pragma unroll
         for (int j = 0; j < NPX; ++j)
-            if (pend & (1u << j)) s_def[wid][w++] = (int)(p0 + j);
-        __syncwarp();
-        for (int e = lane; e < total; e += 32) {
-            const long long q = s_def[wid][e];
+            if (px[j].pending) s_def[atomicAdd(&s_cnt, 1)] = p0 + j;
+        __syncthreads();
+        const int total = s_cnt;
+        for (int e = threadIdx.x; e < total; e += kPlThreads) {
+            const long long q = s_def[e];
             const int yq = (int)(q / a.W), xq = (int)(q - (long long)yq * a.W);
             PlacePx r[1];
             r[0] = place_px<VAR, S2>(a, m, ssum, uni, adaptive, hf, xq, yq, a.scores[(long long)b * hw + q], bankb + q,
