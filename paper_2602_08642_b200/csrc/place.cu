@@ -429,7 +429,7 @@ __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double
     h = mix64(h ^ kGold);  // stream STREAM_ALLOC = 0
     const double k53 = (double)(h >> 11);  // u = k53 * 2^-53 exactly
     const int S = S2 ? 2 : a.S;
-    if constexpr (VAR == SSB_VAR_STOCHASTIC || VAR == SSB_VAR_RELAXED) {
+    if constexpr (VAR == SSB_VAR_STOCHASTIC || VAR == SSB_VAR_RELAXED || VAR == SSB_VAR_STRAIGHT_THROUGH) {
         // float32 fast path with a rigorous bound on |spp32 - spp64|.  The
         // exponent x = (score - max) log2 e is carried as x_hi + x_lo (TwoSum
         // of the difference, split product with the float log2 e and its
@@ -494,8 +494,13 @@ __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double
                 return o;
             }
         } else if (fr32 > err && fr32 < 1.0f - err && fabsf(u32 - fr32) > err + 1e-7f && spp32 < 8388608.0f) {
+            // stochastic; straight-through (estimators.py:114-121): the same
+            // take decision, drawn = frac > 0 (here always), and the gradient
+            // (hold - noisy) / s
+            constexpr bool ST = VAR == SSB_VAR_STRAIGHT_THROUGH;
             const bool tk = u32 < fr32;
-            o.taken = o.drawn = tk;
+            o.taken = tk;
+            o.drawn = ST ? 1 : tk;
             o.spp = a.spp ? (float)(uni + adaptive * exp_neg((double)score - m, t2)) : spp32;  // (optional output)
             const int idx = (int)(fl32 < (float)(S - 1) ? fl32 : (float)(S - 1));
             const float sden = spp32 > (float)a.floor_ ? spp32 : (float)a.floor_;
@@ -508,10 +513,11 @@ __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double
                 } else {
                     for (int j = 0; j < idx; ++j) acc += bp[(j * 3 + c) * hw];
                 }
-                if (tk) acc += bp[(idx * 3 + c) * hw];
+                const float hold = (ST || tk) ? bp[(idx * 3 + c) * hw] : 0.0f;  // (stochastic: read if taken)
+                if (tk) acc += hold;
                 const float nv = acc * rs;
                 o.noisy[c] = nv > 0.0f ? nv : 0.0f;
-                o.grad[c] = -nv * rs;
+                o.grad[c] = ST ? (hold - nv) * rs : -nv * rs;
             }
             return o;
         }
