@@ -352,8 +352,16 @@ __device__ __forceinline__ double exp_neg(double d, const double* t2) {
 
 template <bool VEC>
 __global__ void __launch_bounds__(kPlThreads) k_place_partials(long long n, const float* __restrict__ scores,
-                                                              double* __restrict__ parts, int nparts) {
+                                                              double* __restrict__ parts, int nparts, int W,
+                                                              uint64_t seed, int64_t frame0, uint64_t* __restrict__ hx) {
     __shared__ double t2[64];
+    {
+        // the frame's column hashes for k_place (key_hash's first two rounds)
+        const int bb = blockIdx.y;
+        const uint64_t hf = mix64(mix64(seed + kGold) ^ ((uint64_t)(frame0 + bb) * kGold + kGold));
+        for (int x = blockIdx.x * kPlThreads + threadIdx.x; x < W; x += nparts * kPlThreads)
+            hx[(long long)bb * W + x] = mix64(hf ^ ((uint64_t)x * kGold + kGold));
+    }
     __shared__ double bm;
     load_exp_table(t2);
     const int b = blockIdx.y;
@@ -401,6 +409,7 @@ struct PlaceArgs {
     int64_t frame0;
     double budget, lam, temp, floor_;
     float gainf;  // relaxed fast path: (float)(2 lam / (2 lam - 1))
+    const uint64_t* hx;  // (B, W) column hashes mix64(prefix(seed, frame) ^ key(x)), from k_place_partials
     const float* scores;
     const float* bank;
     const double* stat;
@@ -419,13 +428,14 @@ struct PlacePx {
 
 template <int VAR, bool S2, bool DEFER = false>
 __device__ __forceinline__ PlacePx place_px(const PlaceArgs& a, double m, double ssum, double uni, double adaptive,
-                                            uint64_t hf, int x, int y, float score, const float* bp, long long hw,
+                                            uint64_t h1, int y, float score, const float* bp, long long hw,
                                             const double* t2) {
     PlacePx o;
     o.pending = false;
-    // key_hash with the (seed, frame) prefix hoisted: rng.py:43-48
-    uint64_t h = mix64(hf ^ ((uint64_t)x * kGold + kGold));
-    h = mix64(h ^ ((uint64_t)y * kGold + kGold));
+    // key_hash with the (seed, frame) prefix and the column step hoisted
+    // (h1 = mix64(prefix ^ key(x)), from the per-frame column table):
+    // rng.py:43-48
+    uint64_t h = mix64(h1 ^ ((uint64_t)y * kGold + kGold));
     h = mix64(h ^ kGold);  // stream STREAM_ALLOC = 0
     const double k53 = (double)(h >> 11);  // u = k53 * 2^-53 exactly
     const int S = S2 ? 2 : a.S;
@@ -599,7 +609,8 @@ template <bool VEC>
 __device__ __forceinline__ void store_px(const PlaceArgs& a, int b, long long hw, long long p0, const PlacePx* px);
 
 template <int VAR, bool S2, bool VEC>
-__global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
+__global__ void __launch_bounds__(kPlThreads, (VAR == SSB_VAR_STOCHASTIC || VAR == SSB_VAR_RELAXED) ? 4 : 1)
+    k_place(PlaceArgs a) {
     __shared__ double t2[64];
     load_exp_table(t2);
     __syncthreads();
@@ -607,7 +618,6 @@ __global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
     const double m = a.stat[2 * b], ssum = a.stat[2 * b + 1];
     const long long hw = (long long)a.H * a.W;
     const double uni = 0.125 * a.budget, adaptive = (1.0 - 0.125) * a.budget * (double)hw / ssum;
-    const uint64_t hf = mix64(mix64(a.seed + kGold) ^ ((uint64_t)(a.frame0 + b) * kGold + kGold));
     const int S = S2 ? 2 : a.S;
     const float* bankb = a.bank + (long long)b * S * 3 * hw;
     constexpr int NPX = VEC ? 4 : 1;
@@ -633,9 +643,22 @@ __global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
         } else {
             sc[0] = a.scores[(long long)b * hw + p0];
         }
+        // the column hashes of the frame (k_place_partials' table)
+        uint64_t h1[NPX];
+        const uint64_t* hxr = a.hx + (long long)b * a.W + x0;
+        if constexpr (VEC) {
+            const ulonglong2 u01 = __ldg(reinterpret_cast<const ulonglong2*>(hxr));
+            const ulonglong2 u23 = __ldg(reinterpret_cast<const ulonglong2*>(hxr) + 1);
+            h1[0] = u01.x;
+            h1[1] = u01.y;
+            h1[2] = u23.x;
+            h1[3] = u23.y;
+        } else {
+            h1[0] = __ldg(hxr);
+        }
 #pragma unroll
         for (int j = 0; j < NPX; ++j)
-            px[j] = place_px<VAR, S2, DEFER>(a, m, ssum, uni, adaptive, hf, x0 + j, y, sc[j], bankb + p0 + j, hw, t2);
+            px[j] = place_px<VAR, S2, DEFER>(a, m, ssum, uni, adaptive, h1[j], y, sc[j], bankb + p0 + j, hw, t2);
         store_px<VEC>(a, b, hw, p0, px);
     }
     if constexpr (DEFER) {
@@ -655,7 +678,8 @@ __global__ void __launch_bounds__(kPlThreads) k_place(PlaceArgs a) {
             const long long q = s_def[e];
             const int yq = (int)(q / a.W), xq = (int)(q - (long long)yq * a.W);
             PlacePx r[1];
-            r[0] = place_px<VAR, S2>(a, m, ssum, uni, adaptive, hf, xq, yq, a.scores[(long long)b * hw + q], bankb + q,
+            r[0] = place_px<VAR, S2>(a, m, ssum, uni, adaptive, a.hx[(long long)b * a.W + xq], yq,
+                                     a.scores[(long long)b * hw + q], bankb + q,
                                      hw, t2);
             store_px<false>(a, b, hw, q, r);
         }
@@ -902,7 +926,9 @@ __global__ void __launch_bounds__(kPlThreads, 2) k_infer_small(InferArgs a) {
         PlacePx px[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            px[j] = place_px<SSB_VAR_STOCHASTIC, true>(pa, m, ssum, uni, adaptive, hf, x0 + j, y, sc[j], bankb + p0 + j,
+            px[j] = place_px<SSB_VAR_STOCHASTIC, true>(pa, m, ssum, uni, adaptive,
+                                                       mix64(hf ^ ((uint64_t)(x0 + j) * kGold + kGold)), y, sc[j],
+                                                       bankb + p0 + j,
                                                        hw, t2);
         store_px<true>(pa, b, hw, p0, px);
         // the demodulated input of the pyramid (k_pool2's / the forward's x0)
@@ -976,8 +1002,10 @@ int ssb_density_workspace_bytes(int B, int H, int W, size_t* bytes) {
         set_error("ssb_density_workspace_bytes: bad arguments");
         return SSB_EINVAL;
     }
-    // (the fused placement uses 2 x kPlParts + 2 doubles per frame of it)
-    *bytes = ((size_t)2 * B * (kRedBlocks > kPlParts ? kRedBlocks : kPlParts) + 2 * (size_t)B) * sizeof(double);
+    // (the fused placement uses 2 x kPlParts + 2 doubles per frame of it and
+    // then B x W column hashes)
+    *bytes = ((size_t)2 * B * (kRedBlocks > kPlParts ? kRedBlocks : kPlParts) + 2 * (size_t)B) * sizeof(double) +
+             (size_t)B * W * sizeof(uint64_t);
     return SSB_OK;
 }
 
@@ -1096,9 +1124,14 @@ int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place
     const long long np = place_nparts(units);
     double* parts = (double*)workspace;  // B x kPlParts x 2 doubles + B x 2 (inside the density workspace)
     dim3 pgrid((unsigned)np, d->B);
-    if (vec) SSB_LAUNCH(s, k_place_partials<true><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np));
-    else SSB_LAUNCH(s, k_place_partials<false><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np));
     double* stat = parts + (size_t)2 * d->B * kPlParts;
+    uint64_t* hx = reinterpret_cast<uint64_t*>(stat + 2 * d->B);  // (B, W) column hashes
+    if (vec)
+        SSB_LAUNCH(s, k_place_partials<true><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np, d->W, d->seed,
+                                                                          d->frame0, hx));
+    else
+        SSB_LAUNCH(s, k_place_partials<false><<<pgrid, kPlThreads, 0, s>>>(n, io->scores, parts, (int)np, d->W, d->seed,
+                                                                           d->frame0, hx));
     SSB_LAUNCH(s, k_place_finish<<<d->B, kPlThreads, 0, s>>>(parts, (int)np, stat));
 
     PlaceArgs a{};
@@ -1118,6 +1151,7 @@ int ssb_place(const ssb_place_desc* d, const ssb_place_cfg* cfg, const ssb_place
     a.scores = io->scores;
     a.bank = io->bank;
     a.stat = stat;
+    a.hx = hx;
     a.noisy = io->noisy;
     a.grad = io->grad;
     a.spp = io->spp;
