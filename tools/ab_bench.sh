@@ -9,7 +9,7 @@ for r in $(seq ${ROUNDS:-2}); do
 import json,sys
 l=sys.stdin.read()
 try:
-  d=json.loads(l); print('$v', d['config']['workload'][:12], d['value'], 'step_frac', d['step_roofline']['frac'], 'clk', d['clocks'].get('sm_mhz'), 'bwd_l0', d['kernels_ms'].get('bwd_l0'), 'bwd_l1', d['kernels_ms'].get('bwd_l1'), 'bwd_l2', d['kernels_ms'].get('bwd_l2'), 'fwd_l0', d['kernels_ms'].get('fwd_l0'), 'up', d['kernels_ms'].get('bwd_up'))
+  d=json.loads(l); print('$v', d['config']['workload'][:12], d['value'], 'step_frac', d['step_roofline']['frac'], 'clk', d['clocks'].get('sm_mhz'), 'bwd_l0', d['kernels_ms'].get('bwd_l0'), 'bwd_l1', d['kernels_ms'].get('bwd_l1'), 'bwd_l2', d['kernels_ms'].get('bwd_l2'), 'fwd_l0', d['kernels_ms'].get('fwd_l0'), 'up', d['kernels_ms'].get('bwd_up'), 'pool', d['kernels_ms'].get('pool0->1'))
 except Exception as e: print('ERR', l[-1500:])
 "
     done
