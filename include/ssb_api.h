@@ -142,11 +142,13 @@ enum {
 int ssb_uniform_grid(uint64_t seed, int64_t frame0, const int64_t* frames, int B, int H, int W,
                      uint64_t stream_id, double* u, ssb_stream_t stream);
 
-/* normalize_density: spp = budget/8 + 7/8*budget*N*softmax(scores) per frame.
- * scores f64 (B, H, W); workspace from ssb_density_workspace_bytes. */
 /* one variate of the same hash (rng.pixel_uniform, rng.py:51-54) */
 int ssb_uniform_at(uint64_t seed, int64_t frame, int64_t x, int64_t y, uint64_t stream_id, double* u,
                    ssb_stream_t stream);
+
+/* normalize_density: spp = budget/8 + 7/8*budget*N*softmax(scores) per frame.
+ * scores f64 (B, H, W); workspace from ssb_density_workspace_bytes (also
+ * sized for ssb_place: its partial pairs and per-frame column hashes). */
 int ssb_density_workspace_bytes(int B, int H, int W, size_t* bytes);
 int ssb_normalize_density(int B, int H, int W, const double* scores, double budget,
                           double* spp, void* workspace, ssb_stream_t stream);
