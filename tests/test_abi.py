@@ -85,3 +85,28 @@ def test_missing_buffers_rejected(lib):
     io = _lib.PyrFwdIO()
     assert lib.ssb_pyr_forward(C.byref(d), C.byref(io), None, None) == -1
     assert b"required" in lib.ssb_last_error()
+
+
+def test_infer_small_rejects_before_the_device(lib):
+    """ssb_infer_small validates its arguments before any CUDA call: missing
+    buffers -> SSB_EINVAL; shapes outside the small-frame path (capacity 3,
+    W % 4 != 0, > 2^20 pixels, k = 9) -> SSB_EUNSUPPORTED (the caller then
+    runs ssb_place_fused + ssb_pyr_forward)."""
+    P = C.c_void_p
+    fake = C.c_void_p(0x1000)  # never dereferenced: rejected first
+    logits = (C.c_void_p * 3)(fake, fake, fake)
+
+    def call(B=1, H=64, W=64, S=2, k=5, levels=3, scores=fake, lg=logits):
+        d = _lib.PlaceDesc(B, H, W, S, _lib.VARIANTS["stochastic"], 0, 1, 0, 0.25)
+        return lib.ssb_infer_small(C.byref(d), scores, fake, fake, levels, k, lg, fake, fake, fake, None)
+
+    assert call(scores=P(0)) == -1
+    assert call(lg=(C.c_void_p * 3)(fake, None, fake)) == -1
+    assert call(levels=0) == -1
+    assert call(S=3) == -3
+    assert call(W=66) == -3
+    assert call(H=1100, W=1000) == -3
+    assert call(k=9) == -3
+    wb = C.c_size_t()
+    assert lib.ssb_infer_small_workspace_bytes(1, 256, 256, 3, C.byref(wb)) == 0 and wb.value > 256 * 256 * 12
+    assert lib.ssb_infer_small_workspace_bytes(1, 256, 256, 0, C.byref(wb)) == -1
