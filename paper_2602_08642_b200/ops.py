@@ -609,7 +609,9 @@ def infer(scores, bank, demod, logits, budget: float, *, ksize, seed: int = 0, f
     frames (B*H*W <= 2^20, bank capacity 2, W % 4 == 0) run as ONE cooperative
     kernel (``ssb_infer_small``: noisy identical to ``place_fused``, the
     output within float32 rounding of ``pyramid_forward``); others as
-    place_fused + pyramid_forward.  Returns (out, noisy)."""
+    place_fused + pyramid_forward.  ``workspace``: the small-frame kernel's
+    (``ssb_infer_small_workspace_bytes``; allocated when None, unused on the
+    two-call path).  Returns (out, noisy)."""
     lib = _lib.load()
     _need(scores, "scores", dtype=torch.float32)
     B, H, W = scores.shape
