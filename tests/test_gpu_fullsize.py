@@ -72,3 +72,38 @@ def test_full_frame_vs_oracle(name, H, W, L, k, ldt, rtol):
     assert_levels_close(gpu["g_logits"], ref_g.logits, rtol, f"{name} g_logits", scales=ref_g.operand_scale)
     for l, (z, s) in enumerate(zip(ref_g.logits, ref_g.operand_scale)):
         print(f"{name} level {l}: max|ref| {np.abs(z).max():.3e}, operand scale {s:.3e}")
+
+
+def test_full_frame_history_vs_oracle():
+    """evaluate_step's frame-1 call shape at a full 1080p frame: L3 k5 fp32
+    with the 25-tap temporal group over a warped history (the TMA path:
+    log-sum-exp level-0 weights + the temporal pass), against the float64
+    oracle -- every tensor and level within 1e-5."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2602_08642_b200 import ops
+    dev = torch.device("cuda:0")
+    H, W, L, k = 1080, 1920, 3, 5
+    noisy, demod, logits, up = bench.synthetic_inputs(1, H, W, L, k, "f32", dev, seed=29)
+    g = torch.Generator(device=dev).manual_seed(30)
+    prev = torch.exp(-1.0 + 1.0 * torch.randn(1, 3, H, W, generator=g, device=dev))
+    logits[0] = torch.cat([logits[0], torch.randn(1, k * k, H, W, generator=g, device=dev)], dim=1).contiguous()
+    out, tape = ops.pyramid_forward(noisy, logits, demod, prev, ksize=k)
+    gr = ops.pyramid_backward(tape, up)
+    torch.cuda.synchronize()
+    gpu = {"out": _host(out), "g_input": _host(gr.input), "g_demod": _host(gr.demod), "g_prev": _host(gr.prev),
+           "g_logits": [_host(z) for z in gr.logits]}
+    ins = {"noisy": _host(noisy), "demod": _host(demod), "up": _host(up), "prev": _host(prev),
+           "logits": [_host(z) for z in logits]}
+    del out, tape, gr, noisy, demod, logits, up, prev
+    torch.cuda.empty_cache()
+    ref_out, ref_tape = op.forward(ins["noisy"], ins["logits"], ins["prev"], ins["demod"], k=k)
+    ref_g = op.backward(ref_tape, ins["up"])
+    del ref_tape
+    assert_close(gpu["out"], ref_out, 1e-5, "c1h out")
+    assert_close(gpu["g_input"], ref_g.input, 1e-5, "c1h g_noisy")
+    assert_close(gpu["g_demod"], ref_g.demod, 1e-5, "c1h g_demod")
+    assert_close(gpu["g_prev"], ref_g.prev, 1e-5, "c1h g_prev")
+    assert_levels_close(gpu["g_logits"], ref_g.logits, 1e-5, "c1h g_logits", scales=ref_g.operand_scale)
